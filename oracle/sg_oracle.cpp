@@ -1,0 +1,687 @@
+// sg_oracle.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A plain, slow, single-threaded CPU implementation of the sparse-grid
+// semantics of AsyncTaichi (arXiv 2012.08141).  It executes the UNOPTIMIZED
+// lowered task stream one task at a time, in program order (PAPER.md:84-85
+// "eagerly launches"; PAPER.md:97/250 the optimizer must not change results).
+// It is the parity reference for the CUDA path in paper_2012_08141_b200/ and
+// shares no code, header, table or helper with it.  Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+// may load it.  The product path never does.
+//
+// Data model (restated from the paper):
+//   * SNode tree (Fig. 2): root -> chains of
+//     dense / bitmasked / pointer levels -> place leaves.
+//   * Mask state: per sparse level, the std::set of active
+//     level-global cell coordinates.  A leaf cell is active iff every sparse
+//     ancestor covering it is active; dense levels add no mask (PAPER.md:162,
+//     Fig. 3 caption "Because of the constraints of the dense node, y[0] and
+//     y[2] are also activated").
+//   * Value state: per field a map coord -> value; an inactive
+//     voxel reads 0 ("the inactive voxel has value 0").
+//   * List state ("Lists of each layer are defined to be a
+//     collection of active node indices"): per level the last
+//     generated list; struct-for iterates that list.
+//   * Allocator state: counters of pointer children allocated
+//     and freed.
+// Float arithmetic (reading R14/R15): storage is f32 (values are
+// rounded to float at the end of each task), arithmetic is f64, and every
+// element carries a shadow magnitude M (sum of |terms| that produced it) used
+// for the 1e-5 tolerance.  Index-deciding f32 expressions are evaluated with the
+// same f32 operation order as the device; this file is compiled with
+// -ffp-contract=off.
+//
+// Parity status per function: see DESIGN.md "Oracle pins".  All functions
+// below are pinned by tests/test_oracle_*.py except where marked
+// "parity unpinned".
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+#include <array>
+#include <algorithm>
+
+namespace {
+
+enum { K_ROOT = 0, K_DENSE = 1, K_BITMASKED = 2, K_POINTER = 3, K_PLACE = 4 };
+enum { T_F32 = 0, T_I32 = 1 };
+enum {
+  OK = 0, E_ARG = -1, E_LAYOUT = -2, E_RANGE = -3, E_TRAP = -6, E_OVERFLOW = -7
+};
+// Op ids of the oracle's own vocabulary (mapped from names in oracle/__init__.py).
+enum {
+  OP_FILL = 1, OP_ADD_CONST = 2, OP_INC = 3, OP_AXPY = 4, OP_STENCIL = 5,
+  OP_JACOBI = 6, OP_REDUCE_SUM = 7, OP_DOWNSAMPLE = 8, OP_JITTER = 9,
+  OP_CLEAR_SCALAR = 10,
+  OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22
+};
+
+typedef std::array<int64_t, 3> Coord;
+
+struct Node {
+  int kind, parent, nd, e[3], dtype;
+  std::vector<int> children;
+  int tree = -1;
+  int64_t res[3] = {1, 1, 1};    // level-global resolution
+  int64_t below[3] = {1, 1, 1};  // leaf cells per cell of this level (per axis)
+};
+
+struct Tree {
+  std::vector<int> levels;   // snode ids root->leaf (empty for a 0-D tree)
+  std::vector<int> fields;   // field ids placed at the leaf
+  int nd = 0;
+};
+
+struct Field {
+  int snode, tree, dtype;
+  std::map<Coord, double> val;   // only active cells have entries
+  std::map<Coord, double> mag;   // shadow magnitude M
+};
+
+struct Array {
+  int64_t n; int ncomp;
+  std::vector<double> val, mag;  // [comp][n]
+};
+
+struct Grid {
+  std::vector<Node> nodes;
+  std::vector<Tree> trees;
+  std::vector<Field> fields;
+  std::vector<Array> arrays;
+  std::map<int, std::set<Coord>> active;     // sparse level -> active cells
+  std::map<int, std::vector<Coord>> lists;   // level -> last generated list
+  std::map<int, int64_t> allocated, freed;   // pointer level -> counters
+  int64_t tasks = 0, listgens = 0;
+  std::string err;
+  // per-task bookkeeping: cells whose value must be rounded to storage type
+  std::set<std::pair<int, Coord>> touched;
+};
+
+inline bool is_pow2(int v) { return v >= 1 && (v & (v - 1)) == 0; }
+inline bool sparse(int k) { return k == K_BITMASKED || k == K_POINTER; }
+
+int fail(Grid* g, int code, const std::string& m) { g->err = m; return code; }
+
+// ---------------------------------------------------------------------------
+// Layout (SPEC.md:46-51 validation rules; Fig. 2)
+// ---------------------------------------------------------------------------
+int build_layout(Grid* g, const int32_t* d, int n) {
+  if (n < 1 || d[0] != K_ROOT || d[1] != -1) return fail(g, E_LAYOUT, "row 0 must be the root");
+  for (int i = 0; i < n; i++) {
+    Node nd;
+    nd.kind = d[i * 7 + 0]; nd.parent = d[i * 7 + 1]; nd.nd = d[i * 7 + 2];
+    for (int a = 0; a < 3; a++) nd.e[a] = d[i * 7 + 3 + a];
+    nd.dtype = d[i * 7 + 6];
+    if (i > 0) {
+      if (nd.kind == K_ROOT) return fail(g, E_LAYOUT, "second root");
+      if (nd.kind < 0 || nd.kind > K_PLACE) return fail(g, E_LAYOUT, "bad kind");
+      if (nd.parent < 0 || nd.parent >= i) return fail(g, E_LAYOUT, "parent must precede child");
+      if (g->nodes[nd.parent].kind == K_PLACE) return fail(g, E_LAYOUT, "place with children");
+      if (nd.nd < 0 || nd.nd > 3) return fail(g, E_LAYOUT, "ndim out of range");
+      for (int a = 0; a < 3; a++) {
+        if (!is_pow2(nd.e[a])) return fail(g, E_LAYOUT, "extent not a power of two");
+        if (a >= nd.nd && nd.e[a] != 1) return fail(g, E_LAYOUT, "extent on unused axis");
+      }
+      if (nd.kind == K_PLACE && (nd.dtype != T_F32 && nd.dtype != T_I32))
+        return fail(g, E_LAYOUT, "bad dtype");
+      g->nodes[nd.parent].children.push_back(i);
+    }
+    g->nodes.push_back(nd);
+  }
+  // Trees: each structural child of the root starts a chain; a place under the
+  // root is a 0-D tree.
+  for (int c : g->nodes[0].children) {
+    Tree t;
+    if (g->nodes[c].kind == K_PLACE) {
+      if (g->nodes[c].nd != 0) return fail(g, E_LAYOUT, "place under root must be 0-D");
+      t.nd = 0;
+      t.fields.push_back(c);
+    } else {
+      int cur = c;
+      t.nd = g->nodes[c].nd;
+      int64_t res[3] = {1, 1, 1};
+      while (true) {
+        Node& nn = g->nodes[cur];
+        if (nn.nd != t.nd) return fail(g, E_LAYOUT, "axis mismatch along chain");
+        for (int a = 0; a < 3; a++) { res[a] *= nn.e[a]; nn.res[a] = res[a]; }
+        t.levels.push_back(cur);
+        int structural = -1, places = 0;
+        for (int ch : nn.children) {
+          if (g->nodes[ch].kind == K_PLACE) places++;
+          else if (structural >= 0) return fail(g, E_LAYOUT, "level with two structural children");
+          else structural = ch;
+        }
+        if (structural >= 0 && places) return fail(g, E_LAYOUT, "places only at the leaf level");
+        if (structural < 0) {
+          if (!places) return fail(g, E_LAYOUT, "leaf level without place");
+          if (nn.kind == K_POINTER) return fail(g, E_LAYOUT, "pointer level cannot be the leaf");
+          for (int ch : nn.children) {
+            if (g->nodes[ch].nd != t.nd) return fail(g, E_LAYOUT, "place ndim mismatch");
+            t.fields.push_back(ch);
+          }
+          break;
+        }
+        cur = structural;
+      }
+      // below[] of each level: product of extents of deeper levels
+      for (size_t k = 0; k < t.levels.size(); k++) {
+        Node& nn = g->nodes[t.levels[k]];
+        for (int a = 0; a < 3; a++) {
+          int64_t b = 1;
+          for (size_t m = k + 1; m < t.levels.size(); m++) b *= g->nodes[t.levels[m]].e[a];
+          nn.below[a] = b;
+        }
+      }
+    }
+    int tid = (int)g->trees.size();
+    for (int l : t.levels) g->nodes[l].tree = tid;
+    g->trees.push_back(t);
+  }
+  // fields in order of place rows
+  for (int i = 0; i < n; i++) {
+    if (g->nodes[i].kind != K_PLACE) continue;
+    Field f;
+    f.snode = i; f.dtype = g->nodes[i].dtype; f.tree = -1;
+    for (size_t t = 0; t < g->trees.size(); t++)
+      for (int pl : g->trees[t].fields) if (pl == i) f.tree = (int)t;
+    if (f.tree < 0) return fail(g, E_LAYOUT, "place not reachable");
+    g->nodes[i].tree = f.tree;
+    g->fields.push_back(f);
+  }
+  return OK;
+}
+
+Tree& tree_of_field(Grid* g, int f) { return g->trees[g->fields[f].tree]; }
+
+const int64_t* leaf_res(Grid* g, const Tree& t) {
+  static const int64_t one[3] = {1, 1, 1};
+  return t.levels.empty() ? one : g->nodes[t.levels.back()].res;
+}
+
+bool in_range(Grid* g, const Tree& t, const Coord& c) {
+  const int64_t* r = leaf_res(g, t);
+  for (int a = 0; a < 3; a++) {
+    if (a < t.nd) { if (c[a] < 0 || c[a] >= r[a]) return false; }
+    else if (c[a] != 0) return false;
+  }
+  return true;
+}
+
+Coord level_coord(const Node& n, const Coord& c) {
+  return Coord{c[0] / n.below[0], c[1] / n.below[1], c[2] / n.below[2]};
+}
+
+// is_active: AND over the sparse ancestors
+bool is_active(Grid* g, const Tree& t, const Coord& c) {
+  for (int l : t.levels) {
+    const Node& n = g->nodes[l];
+    if (!sparse(n.kind)) continue;
+    auto it = g->active.find(l);
+    if (it == g->active.end() || !it->second.count(level_coord(n, c))) return false;
+  }
+  return true;
+}
+
+// activate: top-down insertion of every sparse ancestor
+void activate_cell(Grid* g, const Tree& t, const Coord& c) {
+  for (int l : t.levels) {
+    const Node& n = g->nodes[l];
+    if (!sparse(n.kind)) continue;
+    bool fresh = g->active[l].insert(level_coord(n, c)).second;
+    if (fresh && n.kind == K_POINTER) g->allocated[l]++;
+  }
+}
+
+// read never activates; inactive or out-of-bound reads give 0 (
+// reading R8 for out-of-bound stencil neighbours)
+double read(Grid* g, int f, const Coord& c) {
+  Tree& t = tree_of_field(g, f);
+  if (!in_range(g, t, c) || !is_active(g, t, c)) return 0.0;
+  auto& m = g->fields[f].val;
+  auto it = m.find(c);
+  return it == m.end() ? 0.0 : it->second;
+}
+
+double read_mag(Grid* g, int f, const Coord& c) {
+  Tree& t = tree_of_field(g, f);
+  if (!in_range(g, t, c) || !is_active(g, t, c)) return 0.0;
+  auto& m = g->fields[f].mag;
+  auto it = m.find(c);
+  if (it != m.end()) return it->second;
+  return std::fabs(read(g, f, c));
+}
+
+// write / atomic_add (SPEC.md:74-78 demotion trap)
+int prepare_write(Grid* g, int f, const Coord& c, bool activating) {
+  Tree& t = tree_of_field(g, f);
+  if (!in_range(g, t, c)) return fail(g, E_RANGE, "write out of range");
+  if (activating) activate_cell(g, t, c);
+  else if (!is_active(g, t, c)) return fail(g, E_TRAP, "non-activating write to an inactive cell");
+  g->touched.insert({f, c});
+  return OK;
+}
+
+int write(Grid* g, int f, const Coord& c, double v, bool activating, double m) {
+  int rc = prepare_write(g, f, c, activating);
+  if (rc) return rc;
+  g->fields[f].val[c] = v;
+  g->fields[f].mag[c] = m;
+  return OK;
+}
+
+int atomic_add(Grid* g, int f, const Coord& c, double v, bool activating) {
+  double old = read(g, f, c), om = read_mag(g, f, c);
+  int rc = prepare_write(g, f, c, activating);
+  if (rc) return rc;
+  g->fields[f].val[c] = old + v;
+  g->fields[f].mag[c] = om + std::fabs(v);
+  return OK;
+}
+
+// End of task: values are stored as f32 / i32 (reading R14).
+int end_task(Grid* g) {
+  for (auto& tc : g->touched) {
+    Field& fl = g->fields[tc.first];
+    auto it = fl.val.find(tc.second);
+    if (it == fl.val.end()) continue;
+    double v = it->second;
+    if (fl.dtype == T_F32) {
+      it->second = (double)(float)v;
+    } else {
+      if (v != std::floor(v) || v > 2147483647.0 || v < -2147483648.0) {
+        g->touched.clear();
+        return fail(g, E_OVERFLOW, "i32 overflow or non-integral value");
+      }
+    }
+  }
+  g->touched.clear();
+  g->tasks++;
+  return OK;
+}
+
+// Nearest sparse ancestor level of level index k in the chain (-1 = root list).
+int parent_sparse(Grid* g, const Tree& t, size_t k) {
+  for (int m = (int)k - 1; m >= 0; m--)
+    if (sparse(g->nodes[t.levels[m]].kind)) return (int)m;
+  return -1;
+}
+
+// Enumerate the cells of a box [lo, lo+ext) in ascending lexicographic order.
+template <class F>
+void for_box(const Coord& lo, const int64_t ext[3], F fn) {
+  for (int64_t i = 0; i < ext[0]; i++)
+    for (int64_t j = 0; j < ext[1]; j++)
+      for (int64_t k = 0; k < ext[2]; k++) fn(Coord{lo[0] + i, lo[1] + j, lo[2] + k});
+}
+
+int chain_index(const Tree& t, int snode) {
+  for (size_t k = 0; k < t.levels.size(); k++) if (t.levels[k] == snode) return (int)k;
+  return -1;
+}
+
+// listgen(S): for every entry
+// p of the parent's list, every S-cell under p that is active is appended;
+// the result is sorted.  The root's list is the constant {root}.
+int listgen(Grid* g, int snode) {
+  if (snode <= 0 || snode >= (int)g->nodes.size()) return fail(g, E_ARG, "bad snode");
+  const Node& n = g->nodes[snode];
+  if (!sparse(n.kind)) return fail(g, E_ARG, "listgen on a non-sparse level");
+  const Tree& t = g->trees[n.tree];
+  int k = chain_index(t, snode);
+  int pk = parent_sparse(g, t, k);
+  std::vector<Coord> parents;
+  int64_t ratio[3];
+  if (pk < 0) {
+    parents.push_back(Coord{0, 0, 0});
+    for (int a = 0; a < 3; a++) ratio[a] = n.res[a];
+  } else {
+    parents = g->lists[t.levels[pk]];
+    for (int a = 0; a < 3; a++) ratio[a] = n.res[a] / g->nodes[t.levels[pk]].res[a];
+  }
+  std::vector<Coord> out;
+  const std::set<Coord>& act = g->active[snode];
+  for (const Coord& p : parents) {
+    Coord lo{p[0] * ratio[0], p[1] * ratio[1], p[2] * ratio[2]};
+    for_box(lo, ratio, [&](const Coord& q) { if (act.count(q)) out.push_back(q); });
+  }
+  std::sort(out.begin(), out.end());
+  g->lists[snode] = out;
+  g->listgens++;
+  g->tasks++;
+  return OK;
+}
+
+// Driving level of a struct-for over a tree: the deepest sparse level, except
+// a bitmasked leaf whose bits are tested per cell (reading R5).
+int driving_level(Grid* g, const Tree& t) {
+  for (int m = (int)t.levels.size() - 1; m >= 0; m--) {
+    const Node& n = g->nodes[t.levels[m]];
+    if (!sparse(n.kind)) continue;
+    if (m == (int)t.levels.size() - 1 && n.kind == K_BITMASKED) continue;
+    return m;
+  }
+  return -1;
+}
+
+// Visit the cells a struct-for over tree t iterates:
+// for every entry of the driving list, every leaf cell below it, testing the
+// leaf bit if the leaf is bitmasked.  The list is the one current at task
+// start, so cells activated by the task itself are not visited.
+template <class F>
+void for_struct(Grid* g, const Tree& t, F fn) {
+  if (t.levels.empty()) { fn(Coord{0, 0, 0}); return; }
+  int leaf = t.levels.back();
+  const Node& ln = g->nodes[leaf];
+  int dk = driving_level(g, t);
+  std::vector<Coord> cells;
+  const std::set<Coord>* leafmask = nullptr;
+  if (ln.kind == K_BITMASKED) leafmask = &g->active[leaf];
+  auto visit = [&](const Coord& c) {
+    if (leafmask && !leafmask->count(c)) return;
+    cells.push_back(c);
+  };
+  if (dk < 0) {
+    for_box(Coord{0, 0, 0}, ln.res, visit);
+  } else {
+    const Node& dn = g->nodes[t.levels[dk]];
+    std::vector<Coord> entries = g->lists[t.levels[dk]];
+    for (const Coord& p : entries) {
+      Coord lo{p[0] * dn.below[0], p[1] * dn.below[1], p[2] * dn.below[2]};
+      for_box(lo, dn.below, visit);
+    }
+  }
+  for (const Coord& c : cells) fn(c);
+}
+
+Coord shift(const Coord& c, int axis, int64_t d) { Coord r = c; r[axis] += d; return r; }
+
+bool act_bit(uint32_t activating, int slot) { return (activating >> slot) & 1u; }
+
+int field_ok(Grid* g, int f) { return f >= 0 && f < (int)g->fields.size(); }
+
+// ---------------------------------------------------------------------------
+// Struct-for bodies (the op vocabulary).  Every body is
+// race-free by construction, so sequential order equals any parallel order up
+// to float reassociation.
+// ---------------------------------------------------------------------------
+int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const float* p, int np,
+               uint32_t activating) {
+  if (leaf_snode <= 0 || leaf_snode >= (int)g->nodes.size()) return fail(g, E_ARG, "bad snode");
+  const Node& ln = g->nodes[leaf_snode];
+  if (ln.kind == K_PLACE || ln.tree < 0) return fail(g, E_ARG, "struct-for snode must be a level");
+  const Tree& t = g->trees[ln.tree];
+  if (t.levels.back() != leaf_snode) return fail(g, E_ARG, "struct-for snode must be the leaf level");
+  for (int i = 0; i < nf; i++) if (f[i] >= 0 && !field_ok(g, f[i])) return fail(g, E_ARG, "bad field");
+  auto P = [&](int i) { return i < np ? (double)p[i] : 0.0; };
+  int D = t.nd;
+  int rc = OK;
+  auto need = [&](int cnt) { return nf >= cnt; };
+  switch (op) {
+    case OP_FILL:
+      if (!need(1)) return fail(g, E_ARG, "FILL needs 1 field");
+      for_struct(g, t, [&](const Coord& c) {
+        if (!rc) rc = write(g, f[0], c, P(0), act_bit(activating, 0), std::fabs(P(0)));
+      });
+      break;
+    case OP_ADD_CONST:
+      if (!need(2)) return fail(g, E_ARG, "ADD_CONST needs 2 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        double x = read(g, f[1], c);
+        if (!rc) rc = write(g, f[0], c, x + P(0), act_bit(activating, 0), read_mag(g, f[1], c) + std::fabs(P(0)));
+      });
+      break;
+    case OP_INC:
+      if (!need(1)) return fail(g, E_ARG, "INC needs 1 field");
+      for_struct(g, t, [&](const Coord& c) {
+        if (!rc) rc = atomic_add(g, f[0], c, P(0), act_bit(activating, 0));
+      });
+      break;
+    case OP_AXPY:
+      if (!need(3)) return fail(g, E_ARG, "AXPY needs 3 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        double x = read(g, f[1], c), y = read(g, f[2], c);
+        double m = std::fabs(P(0)) * read_mag(g, f[1], c) + read_mag(g, f[2], c);
+        if (!rc) rc = write(g, f[0], c, P(0) * x + y, act_bit(activating, 0), m);
+      });
+      break;
+    case OP_STENCIL:
+      // y = sum_{a<D} (x[c+e_a] + x[c-e_a]) - 2D x[c]   (5-/7-point Laplacian)
+      if (!need(2)) return fail(g, E_ARG, "STENCIL needs 2 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        double s = 0, m = 0;
+        for (int a = 0; a < D; a++) {
+          double u = read(g, f[1], shift(c, a, +1)), d = read(g, f[1], shift(c, a, -1));
+          s += u + d;
+          m += read_mag(g, f[1], shift(c, a, +1)) + read_mag(g, f[1], shift(c, a, -1));
+        }
+        s -= 2.0 * D * read(g, f[1], c);
+        m += 2.0 * D * read_mag(g, f[1], c);
+        if (!rc) rc = write(g, f[0], c, s, act_bit(activating, 0), m);
+      });
+      break;
+    case OP_JACOBI:
+      // x1 = (b + sum of neighbours of x0) / (2D): Jacobi for -Lap x = b, h = 1
+      if (!need(3)) return fail(g, E_ARG, "JACOBI needs 3 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        double s = read(g, f[2], c), m = read_mag(g, f[2], c);
+        for (int a = 0; a < D; a++) {
+          s += read(g, f[1], shift(c, a, +1)) + read(g, f[1], shift(c, a, -1));
+          m += read_mag(g, f[1], shift(c, a, +1)) + read_mag(g, f[1], shift(c, a, -1));
+        }
+        if (!rc) rc = write(g, f[0], c, s / (2.0 * D), act_bit(activating, 0), m / (2.0 * D));
+      });
+      break;
+    case OP_REDUCE_SUM:
+      if (!need(2)) return fail(g, E_ARG, "REDUCE_SUM needs 2 fields");
+      if (g->trees[g->fields[f[0]].tree].nd != 0) return fail(g, E_ARG, "REDUCE_SUM target must be 0-D");
+      for_struct(g, t, [&](const Coord& c) {
+        if (!rc) rc = atomic_add(g, f[0], Coord{0, 0, 0}, read(g, f[1], c), act_bit(activating, 0));
+      });
+      break;
+    case OP_DOWNSAMPLE:
+      // y[c // 2] += p0 * x[c] + p1   (PAPER.md:350 restriction; Fig. 3 with p0=0,p1=1)
+      if (!need(1)) return fail(g, E_ARG, "DOWNSAMPLE needs a target");
+      for_struct(g, t, [&](const Coord& c) {
+        Coord h{c[0] / 2, c[1] / 2, c[2] / 2};
+        double x = (nf > 1 && f[1] >= 0) ? read(g, f[1], c) : 0.0;
+        if (!rc) rc = atomic_add(g, f[0], h, P(0) * x + P(1), act_bit(activating, 0));
+      });
+      break;
+    case OP_JITTER:
+      // x[i] += x[i + 1] for even i along axis 0 (PAPER.md:505 deep_hierarchy)
+      if (!need(1)) return fail(g, E_ARG, "JITTER needs 1 field");
+      for_struct(g, t, [&](const Coord& c) {
+        if (c[0] % 2 != 0) return;
+        double x = read(g, f[0], shift(c, 0, 1));
+        if (!rc) rc = atomic_add(g, f[0], c, x, act_bit(activating, 0));
+      });
+      break;
+    default:
+      return fail(g, E_ARG, "unknown struct-for op");
+  }
+  if (rc) { g->touched.clear(); return rc; }
+  return end_task(g);
+}
+
+int serial(Grid* g, int op, const int32_t* f, int nf, const float* p, int np) {
+  (void)p; (void)np;
+  switch (op) {
+    case OP_CLEAR_SCALAR: {
+      if (nf < 1 || !field_ok(g, f[0])) return fail(g, E_ARG, "CLEAR_SCALAR needs a field");
+      if (g->trees[g->fields[f[0]].tree].nd != 0) return fail(g, E_ARG, "CLEAR_SCALAR target must be 0-D");
+      int rc = write(g, f[0], Coord{0, 0, 0}, 0.0, false, 0.0);
+      if (rc) { g->touched.clear(); return rc; }
+      return end_task(g);
+    }
+    default:
+      return fail(g, E_ARG, "unknown serial op");
+  }
+}
+
+// DEACTIVATE(S): every cell of level S and below becomes inactive, their
+// payload is dropped (reads 0) and pointer children are freed (reading R7).
+int deactivate(Grid* g, int snode) {
+  if (snode <= 0 || snode >= (int)g->nodes.size()) return fail(g, E_ARG, "bad snode");
+  const Node& n = g->nodes[snode];
+  if (!sparse(n.kind)) return fail(g, E_ARG, "deactivate needs a sparse level");
+  const Tree& t = g->trees[n.tree];
+  int k = chain_index(t, snode);
+  for (size_t m = k; m < t.levels.size(); m++) {
+    int l = t.levels[m];
+    if (!sparse(g->nodes[l].kind)) continue;
+    if (g->nodes[l].kind == K_POINTER) g->freed[l] += (int64_t)g->active[l].size();
+    g->active[l].clear();
+  }
+  for (int pl : t.fields) {
+    for (size_t fi = 0; fi < g->fields.size(); fi++)
+      if (g->fields[fi].snode == pl) { g->fields[fi].val.clear(); g->fields[fi].mag.clear(); }
+  }
+  g->tasks++;
+  return OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C API of the oracle (names distinct from the product's sg_*).
+// ---------------------------------------------------------------------------
+extern "C" {
+
+void* orc_create(const int32_t* desc, int32_t n, char* err, int32_t errlen) {
+  Grid* g = new Grid();
+  int rc = build_layout(g, desc, n);
+  if (rc) {
+    if (err && errlen > 0) { std::snprintf(err, errlen, "%s", g->err.c_str()); }
+    delete g;
+    return nullptr;
+  }
+  return g;
+}
+
+void orc_destroy(void* h) { delete (Grid*)h; }
+
+const char* orc_error(void* h) { return ((Grid*)h)->err.c_str(); }
+
+int32_t orc_num_fields(void* h) { return (int32_t)((Grid*)h)->fields.size(); }
+
+int32_t orc_activate(void* h, int32_t field, const int32_t* coords, int64_t n) {
+  Grid* g = (Grid*)h;
+  if (!field_ok(g, field)) return fail(g, E_ARG, "bad field");
+  Tree& t = tree_of_field(g, field);
+  for (int64_t i = 0; i < n; i++) {
+    Coord c{0, 0, 0};
+    for (int a = 0; a < t.nd; a++) c[a] = coords[i * t.nd + a];
+    if (!in_range(g, t, c)) return fail(g, E_RANGE, "activate coordinate out of range");
+  }
+  for (int64_t i = 0; i < n; i++) {
+    Coord c{0, 0, 0};
+    for (int a = 0; a < t.nd; a++) c[a] = coords[i * t.nd + a];
+    activate_cell(g, t, c);
+  }
+  g->tasks++;
+  return OK;
+}
+
+int32_t orc_listgen(void* h, int32_t snode) { return listgen((Grid*)h, snode); }
+
+int32_t orc_clear_list(void* h, int32_t snode) {
+  Grid* g = (Grid*)h;
+  if (snode <= 0 || snode >= (int)g->nodes.size()) return fail(g, E_ARG, "bad snode");
+  g->lists[snode].clear();
+  g->tasks++;
+  return OK;
+}
+
+int32_t orc_struct_for(void* h, int32_t op, int32_t snode, const int32_t* fields, int32_t nf,
+                       const float* params, int32_t np, uint32_t activating) {
+  return struct_for((Grid*)h, op, snode, fields, nf, params, np, activating);
+}
+
+int32_t orc_serial(void* h, int32_t op, const int32_t* fields, int32_t nf, const float* params, int32_t np) {
+  return serial((Grid*)h, op, fields, nf, params, np);
+}
+
+int32_t orc_deactivate(void* h, int32_t snode) { return deactivate((Grid*)h, snode); }
+
+// Sorted set of active level-global cells of a sparse level.
+int64_t orc_export_mask(void* h, int32_t snode, int32_t* out, int64_t cap) {
+  Grid* g = (Grid*)h;
+  if (snode <= 0 || snode >= (int)g->nodes.size() || !sparse(g->nodes[snode].kind))
+    return fail(g, E_ARG, "bad snode");
+  const std::set<Coord>& s = g->active[snode];
+  int nd = g->nodes[snode].nd;
+  int64_t i = 0;
+  for (const Coord& c : s) {
+    if (i < cap) for (int a = 0; a < nd; a++) out[i * nd + a] = (int32_t)c[a];
+    i++;
+  }
+  return i;
+}
+
+// The level's current list, as stored.
+int64_t orc_export_list(void* h, int32_t snode, int32_t* out, int64_t cap) {
+  Grid* g = (Grid*)h;
+  if (snode <= 0 || snode >= (int)g->nodes.size()) return fail(g, E_ARG, "bad snode");
+  const std::vector<Coord>& s = g->lists[snode];
+  int nd = g->nodes[snode].nd;
+  int64_t i = 0;
+  for (const Coord& c : s) {
+    if (i < cap) for (int a = 0; a < nd; a++) out[i * nd + a] = (int32_t)c[a];
+    i++;
+  }
+  return i;
+}
+
+// Dense bounding array of a field (row-major, last axis fastest), inactive -> 0,
+// plus the shadow magnitude of each element.
+int32_t orc_read_field(void* h, int32_t field, double* out, double* mag, int64_t n) {
+  Grid* g = (Grid*)h;
+  if (!field_ok(g, field)) return fail(g, E_ARG, "bad field");
+  Tree& t = tree_of_field(g, field);
+  const int64_t* r = leaf_res(g, t);
+  int64_t total = 1;
+  for (int a = 0; a < t.nd; a++) total *= r[a];
+  if (n != total) return fail(g, E_ARG, "size mismatch");
+  int64_t e[3] = {t.nd > 0 ? r[0] : 1, t.nd > 1 ? r[1] : 1, t.nd > 2 ? r[2] : 1};
+  int64_t i = 0;
+  for_box(Coord{0, 0, 0}, e, [&](const Coord& c) {
+    out[i] = read(g, field, c);
+    if (mag) mag[i] = read_mag(g, field, c);
+    i++;
+  });
+  return OK;
+}
+
+// Load values of ACTIVE cells from a dense array (single-step state handoff).
+int32_t orc_load_field(void* h, int32_t field, const double* dense, int64_t n) {
+  Grid* g = (Grid*)h;
+  if (!field_ok(g, field)) return fail(g, E_ARG, "bad field");
+  Tree& t = tree_of_field(g, field);
+  const int64_t* r = leaf_res(g, t);
+  int64_t e[3] = {t.nd > 0 ? r[0] : 1, t.nd > 1 ? r[1] : 1, t.nd > 2 ? r[2] : 1};
+  if (n != e[0] * e[1] * e[2]) return fail(g, E_ARG, "size mismatch");
+  int64_t i = 0;
+  Field& fl = g->fields[field];
+  for_box(Coord{0, 0, 0}, e, [&](const Coord& c) {
+    if (is_active(g, t, c)) { fl.val[c] = dense[i]; fl.mag[c] = std::fabs(dense[i]); }
+    i++;
+  });
+  return OK;
+}
+
+// counters: [tasks, listgens, sum allocated, sum freed]
+int32_t orc_counters(void* h, int64_t* out) {
+  Grid* g = (Grid*)h;
+  int64_t a = 0, f = 0;
+  for (auto& kv : g->allocated) a += kv.second;
+  for (auto& kv : g->freed) f += kv.second;
+  out[0] = g->tasks; out[1] = g->listgens; out[2] = a; out[3] = f;
+  return OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,306 @@
+"""Seeded synthetic inputs shared by the oracle and the CUDA path.
+
+This module is the ONLY code both sides see.  It holds no arithmetic of the
+method: it builds layout descriptors (the SNode tree as plain integer rows),
+seeded coordinate / particle buffers, and *programs* -- ordered lists of user
+calls (activate / struct_for / range_for / serial / clear / listgen / flush)
+written as plain dicts.  Each side replays a program through its own API:
+``paper_2012_08141_b200.sg.run_program`` (C-ABI) and ``oracle.run_program``
+(CPU oracle).  Op names are strings; each side maps them to its own ids.
+
+Config recipes follow SURVEY.md s8.0 and DESIGN.md "Input recipe".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# ----------------------------------------------------------------------------
+# Layout descriptor rows: [kind, parent, ndim, e0, e1, e2, dtype]
+# (Fig. 2 caption `ti.root.pointer(ti.i, 4).dense(ti.i, 2).place(x)`;
+#  PAPER.md:187 "Commonly used SNodes include dense, bitmasked, pointer")
+# ----------------------------------------------------------------------------
+ROOT, DENSE, BITMASKED, POINTER, PLACE = 0, 1, 2, 3, 4
+F32, I32 = 0, 1
+KIND = {"root": ROOT, "dense": DENSE, "bitmasked": BITMASKED, "pointer": POINTER}
+DTYPE = {"f32": F32, "i32": I32}
+
+
+class Layout:
+    """Builds the descriptor table.  Field ids are the order of place rows."""
+
+    def __init__(self):
+        self.rows = [[ROOT, -1, 0, 1, 1, 1, 0]]
+        self.fields = {}      # name -> field id
+        self.field_snode = {}  # name -> place snode id
+        self.leaf = {}        # name -> leaf level snode id (parent of place)
+        self.field_dtype = {}
+        self.field_ndim = {}
+
+    def chain(self, levels, fields, ndim=None):
+        """levels: [(kind, extents tuple)], root-to-leaf; fields: [(name, dtype)].
+        Returns the list of level snode ids."""
+        parent = 0
+        ids = []
+        for kind, ext in levels:
+            ext = tuple(int(e) for e in ext)
+            nd = len(ext) if ndim is None else ndim
+            e = list(ext) + [1] * (3 - len(ext))
+            self.rows.append([KIND[kind], parent, nd, e[0], e[1], e[2], 0])
+            parent = len(self.rows) - 1
+            ids.append(parent)
+        nd = self.rows[parent][2] if ids else 0
+        for name, dt in fields:
+            self.rows.append([PLACE, parent, nd, 1, 1, 1, DTYPE[dt]])
+            self.fields[name] = len(self.fields)
+            self.field_snode[name] = len(self.rows) - 1
+            self.leaf[name] = parent
+            self.field_dtype[name] = dt
+            self.field_ndim[name] = nd
+        return ids
+
+    def scalar(self, name, dtype="f32"):
+        return self.chain([], [(name, dtype)])
+
+    def desc(self):
+        return np.asarray(self.rows, dtype=np.int32)
+
+    def shape(self, name):
+        """Full-resolution bounding shape of a field (product of ancestor extents)."""
+        s = [1, 1, 1]
+        node = self.rows[self.field_snode[name]][1]
+        while node > 0:
+            r = self.rows[node]
+            for a in range(3):
+                s[a] *= r[3 + a]
+            node = r[1]
+        return tuple(s[: self.field_ndim[name]])
+
+
+def program(layout, calls, arrays=None, name=""):
+    return {"name": name, "layout": layout, "desc": layout.desc(),
+            "arrays": arrays or {}, "calls": calls}
+
+
+# ---- call constructors (plain data) -----------------------------------------
+def activate(field, coords):
+    return {"call": "activate", "field": field, "coords": np.ascontiguousarray(coords, dtype=np.int32)}
+
+
+def struct_for(op, snode, fields, params=(), activating=()):
+    return {"call": "struct_for", "op": op, "snode": int(snode), "fields": list(fields),
+            "params": [float(p) for p in params], "activating": list(activating)}
+
+
+def range_for(op, n, fields=(), arrays=(), params=(), activating=()):
+    return {"call": "range_for", "op": op, "n": int(n), "fields": list(fields), "arrays": list(arrays),
+            "params": [float(p) for p in params], "activating": list(activating)}
+
+
+def serial(op, fields, params=()):
+    return {"call": "serial", "op": op, "fields": list(fields), "params": [float(p) for p in params]}
+
+
+def clear_values(field):
+    return {"call": "clear", "mode": "values", "target": field}
+
+
+def deactivate(snode):
+    return {"call": "clear", "mode": "deactivate", "target": int(snode)}
+
+
+def listgen(snode):
+    return {"call": "listgen", "snode": int(snode)}
+
+
+def flush(passes="all", observed=None):
+    return {"call": "flush", "passes": passes, "observed": observed}
+
+
+# ----------------------------------------------------------------------------
+# C1: 2D 64x64, pointer(16x16) -> bitmasked(4x4) leaf.  Disk r=24 (1,804 cells).
+# ----------------------------------------------------------------------------
+def c1_layout(dtype="f32"):
+    L = Layout()
+    lv = L.chain([("pointer", (16, 16)), ("bitmasked", (4, 4))], [("x", dtype), ("y", dtype)])
+    L.scalar("s", dtype)
+    return L, lv
+
+
+def c1_disk_coords(n=64, r=24.0):
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    m = (i + 0.5 - n / 2) ** 2 + (j + 0.5 - n / 2) ** 2 < r * r
+    return np.stack([i[m], j[m]], axis=1).astype(np.int32)
+
+
+def c1_random_coords(seed=0, p_ptr=0.5, p_bit=0.5):
+    rng = np.random.default_rng(seed)
+    ptr = rng.random((16, 16)) < p_ptr
+    bits = rng.random((64, 64)) < p_bit
+    i, j = np.meshgrid(np.arange(64), np.arange(64), indexing="ij")
+    m = bits & ptr[i // 4, j // 4]
+    return np.stack([i[m], j[m]], axis=1).astype(np.int32)
+
+
+def c1_step_calls(L, lv, coords):
+    """Reading 19: activate, fill x=1, stencil y<-x, clear s, reduce s+=y."""
+    f = L.fields
+    leaf = lv[-1]
+    return [activate(f["x"], coords),
+            struct_for("FILL", leaf, [f["x"]], [1.0]),
+            struct_for("STENCIL", leaf, [f["y"], f["x"]]),
+            serial("CLEAR_SCALAR", [f["s"]]),
+            struct_for("REDUCE_SUM", leaf, [f["s"], f["y"]])]
+
+
+def c1_program(steps=1, disk=True, dtype="f32", passes="all", seed=0):
+    L, lv = c1_layout(dtype)
+    coords = c1_disk_coords() if disk else c1_random_coords(seed)
+    calls = []
+    for _ in range(steps):
+        calls += c1_step_calls(L, lv, coords)
+        calls.append(flush(passes))
+    return program(L, calls, name="C1")
+
+
+# ----------------------------------------------------------------------------
+# C2: 3D 256^3, pointer(8^3)[32^3] -> bitmasked(4^3)[8^3] -> dense(8^3).
+# Block-ball: leaf blocks whose nearest point lies within R voxels of the centre.
+# ----------------------------------------------------------------------------
+def c2_layout(ptr=8, bm=4, dn=8):
+    L = Layout()
+    lv = L.chain([("pointer", (ptr,) * 3), ("bitmasked", (bm,) * 3), ("dense", (dn,) * 3)],
+                 [("x0", "f32"), ("x1", "f32"), ("b", "f32")])
+    L.scalar("s", "f32")
+    return L, lv
+
+
+def block_ball_coords(n_blocks_axis, block, radius):
+    """One cell coordinate (the block origin) per active leaf block."""
+    b = np.arange(n_blocks_axis)
+    bx, by, bz = np.meshgrid(b, b, b, indexing="ij")
+    c = n_blocks_axis * block / 2.0
+    near = lambda q: np.clip(c, q * block, q * block + block)
+    d2 = (near(bx) - c) ** 2 + (near(by) - c) ** 2 + (near(bz) - c) ** 2
+    m = d2 < radius * radius
+    return (np.stack([bx[m], by[m], bz[m]], axis=1) * block).astype(np.int32)
+
+
+def c2_solve_calls(L, lv, coords, iters=50, reduce_result=True):
+    f = L.fields
+    leaf = lv[-1]
+    calls = [activate(f["b"], coords),
+             struct_for("FILL", leaf, [f["b"]], [1.0]),
+             struct_for("FILL", leaf, [f["x0"]], [0.0])]
+    src, dst = f["x0"], f["x1"]
+    for _ in range(iters):
+        calls.append(struct_for("JACOBI", leaf, [dst, src, f["b"]]))
+        src, dst = dst, src
+    if reduce_result:
+        calls += [serial("CLEAR_SCALAR", [f["s"]]),
+                  struct_for("REDUCE_SUM", leaf, [f["s"], src])]
+    return calls, src
+
+
+def c2_program(iters=50, radius=68.0, ptr=8, passes="all", solves=1):
+    L, lv = c2_layout(ptr=ptr)
+    nb = ptr * 4
+    coords = block_ball_coords(nb, 8, radius * ptr / 8)
+    calls = []
+    for _ in range(solves):
+        c, _ = c2_solve_calls(L, lv, coords, iters)
+        calls += c + [flush(passes)]
+    return program(L, calls, name="C2")
+
+
+def c2_small_program(iters=6, passes="all"):
+    """Oracle-sized C2 variant: 64^3 bound (pointer 2^3), ball R=20 -> spans several
+    containers, ragged block set."""
+    L, lv = c2_layout(ptr=2)
+    coords = block_ball_coords(8, 8, 20.0)
+    c, _ = c2_solve_calls(L, lv, coords, iters)
+    return program(L, c + [flush(passes)], name="C2-small")
+
+
+# ----------------------------------------------------------------------------
+# Random integer programs (SPEC.md:386/454 fuzzer idea: seeded layouts of
+# depth <= 4, a handful of kernels, integer fields for exact comparison).
+# ----------------------------------------------------------------------------
+def fuzz_layout(rng):
+    nd = int(rng.integers(1, 4))
+    depth = int(rng.integers(1, 5))
+    kinds = []
+    for k in range(depth):
+        last = k == depth - 1
+        choices = ["dense", "bitmasked"] if last else ["dense", "bitmasked", "pointer"]
+        kinds.append(choices[int(rng.integers(0, len(choices)))])
+    # per-axis total resolution: <=64 (1D), <=16 (2D), <=8 (3D)
+    max_log = {1: 6, 2: 4, 3: 3}[nd]
+    logs = np.zeros((depth, nd), dtype=int)
+    for a in range(nd):
+        budget = int(rng.integers(1, max_log + 1))
+        for _ in range(budget):
+            logs[int(rng.integers(0, depth)), a] += 1
+    if logs[-1].min() == 0:  # leaf extent >= 2 on every axis so DOWNSAMPLE has a coarse twin
+        for a in range(nd):
+            if logs[-1, a] == 0:
+                logs[-1, a] = 1
+    levels = [(kinds[k], tuple(int(2 ** logs[k, a]) for a in range(nd))) for k in range(depth)]
+    coarse = levels[:-1] + [(levels[-1][0], tuple(e // 2 for e in levels[-1][1]))]
+    L = Layout()
+    main = L.chain(levels, [("a", "i32"), ("b", "i32"), ("c", "i32")])
+    half = L.chain(coarse, [("h", "i32")])
+    L.scalar("s", "i32")
+    return L, main, half
+
+
+def fuzz_program(seed, n_ops=None, passes="all"):
+    rng = np.random.default_rng(seed)
+    L, main, half = fuzz_layout(rng)
+    f = L.fields
+    shape = L.shape("a")
+    nd = len(shape)
+    leaf, hleaf = main[-1], half[-1]
+    sparse_main = [s for s in main if L.rows[s][0] in (BITMASKED, POINTER)]
+    calls = []
+
+    def rand_cells(k):
+        return np.stack([rng.integers(0, shape[a], size=k) for a in range(nd)], axis=1).astype(np.int32)
+
+    calls.append(activate(f["a"], rand_cells(int(rng.integers(1, 6)))))
+    n_ops = int(rng.integers(3, 9)) if n_ops is None else n_ops
+    fl = ["a", "b", "c"]
+    for _ in range(n_ops):
+        r = int(rng.integers(0, 14))
+        x, y, z = (fl[i] for i in rng.permutation(3))
+        act = [bool(rng.integers(0, 2))]
+        k = float(rng.integers(-3, 4))
+        if r == 0:
+            calls.append(activate(f[x], rand_cells(int(rng.integers(1, 4)))))
+        elif r == 1:
+            calls.append(struct_for("FILL", leaf, [f[x]], [k], act))
+        elif r == 2:
+            calls.append(struct_for("INC", leaf, [f[x]], [k], act))
+        elif r == 3:
+            calls.append(struct_for("ADD_CONST", leaf, [f[x], f[y]], [k], act))
+        elif r == 4:
+            calls.append(struct_for("AXPY", leaf, [f[x], f[y], f[z]], [k], act))
+        elif r == 5:
+            calls.append(struct_for("STENCIL", leaf, [f[x], f[y]], [], act))
+        elif r == 6:
+            calls.append(struct_for("JITTER", leaf, [f[x]], [], act))
+        elif r == 7:
+            calls.append(struct_for("DOWNSAMPLE", leaf, [f["h"], f[x]], [k, float(rng.integers(0, 3))], [True]))
+        elif r == 8:
+            calls += [serial("CLEAR_SCALAR", [f["s"]]), struct_for("REDUCE_SUM", leaf, [f["s"], f[x]])]
+        elif r == 9:
+            calls.append(clear_values(f[x]))
+        elif r == 10 and sparse_main:
+            calls.append(deactivate(sparse_main[int(rng.integers(0, len(sparse_main)))]))
+        elif r == 11:
+            calls.append(struct_for("INC", hleaf, [f["h"]], [k], act))
+        elif r == 12:
+            calls.append(flush(passes))
+        else:
+            calls.append(struct_for("FILL", leaf, [f[x]], [k], act))
+    calls.append(flush(passes))
+    return program(L, calls, name=f"fuzz{seed}")
