@@ -1,0 +1,210 @@
+/* sg.h -- C-ABI of the B200 sparse-grid task engine (libsg.so).
+ *
+ * The boundary of the hot path that AsyncTaichi (arXiv 2012.08141) optimizes:
+ * sparse-grid task execution over an SNode hierarchy (root -> pointer ->
+ * bitmasked -> dense -> place).  Calls follow the paper's statement of the
+ * problem: tasks are queued and nothing runs until a synchronization point
+ * (section 7.1 "We store all tasks into a queue until
+ * synchronization"), where the whole queue is optimized by the state-flow-graph
+ * passes (section 6) and launched.  The optimization is
+ * transparent: results equal eager execution (PAPER.md:97, PAPER.md:250
+ * "Order independency").
+ *
+ * Conventions (every entry point):
+ *   - Return SG_OK (0) or a negative sg_status; sg_last_error() gives a
+ *     thread-local message for the last failure on the calling thread.
+ *   - sg_grid is opaque, single-owner and not thread-safe.
+ *   - Device pointers passed in (coordinates, particle arrays) are BORROWED:
+ *     they must stay valid and unmodified until the flush that consumes them
+ *     has completed on the grid's stream (ordinary stream ordering).
+ *   - Host pointers are only read/written during the call.
+ *   - Enqueue calls (sg_activate, sg_listgen, sg_struct_for, sg_clear) do no
+ *     device work.  sg_flush plans and enqueues kernels on the grid's stream and
+ *     returns without synchronizing.  Exports flush, then synchronize.
+ *   - Device-detected errors (pool exhausted, list overflow, demotion trap in
+ *     debug builds) are latched in a device error word and reported by the next
+ *     sg_sync / export; after one, the grid state is undefined until
+ *     sg_destroy.
+ *   - Layout: every field's payload is stored SoA in 4-byte elements (f32 or
+ *     i32) inside leaf containers, each leaf block contiguous.
+ */
+#ifndef SG_H_
+#define SG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t sg_status;
+enum {
+  SG_OK = 0,
+  SG_ERR_ARG = -1,             /* bad argument / unknown id / wrong operand count */
+  SG_ERR_LAYOUT = -2,          /* invalid SNode tree */
+  SG_ERR_RANGE = -3,           /* coordinate outside the field's bounding shape */
+  SG_ERR_CUDA = -4,            /* CUDA runtime failure */
+  SG_ERR_NCCL = -5,            /* collective failure (multi-GPU) */
+  SG_ERR_DEMOTION_TRAP = -6,   /* debug: non-activating write to an inactive cell */
+  SG_ERR_OVERFLOW = -7,        /* reserved */
+  SG_ERR_POOL_EXHAUSTED = -8,  /* device: pointer pool has no free container */
+  SG_ERR_LIST_OVERFLOW = -9,   /* device: element list exceeded its capacity */
+  SG_ERR_STATE = -10           /* call not valid in this state (e.g. plan-only grid) */
+};
+
+/* --- SNode tree (Fig. 2 caption; section 4) ---------- */
+enum { SG_ROOT = 0, SG_DENSE = 1, SG_BITMASKED = 2, SG_POINTER = 3, SG_PLACE = 4 };
+enum { SG_F32 = 0, SG_I32 = 1 };
+
+/* One row per node.  Row 0 is the root (parent -1).  Each structural child of
+ * the root starts a chain ("tree") of levels; every level of a chain has the
+ * same ndim (1..3) and power-of-two extents (1 on unused axes); places (fields)
+ * hang only from the last level of a chain, which must be dense or bitmasked;
+ * a place directly under the root is a 0-D scalar field.  Field ids are the
+ * order of place rows.  snode ids are row indices. */
+typedef struct {
+  int32_t kind;       /* SG_ROOT / SG_DENSE / SG_BITMASKED / SG_POINTER / SG_PLACE */
+  int32_t parent;     /* row index of the parent, -1 for the root */
+  int32_t ndim;       /* number of axes of the chain (0 for 0-D places) */
+  int32_t extent[3];  /* per-axis extent of this level (power of two) */
+  int32_t dtype;      /* SG_PLACE only: SG_F32 or SG_I32 */
+} sg_snode_desc;
+
+/* Device memory callbacks (e.g. torch's caching allocator).  NULL -> cudaMalloc. */
+typedef void* (*sg_alloc_fn)(void* ctx, size_t bytes, void* stream);
+typedef void (*sg_free_fn)(void* ctx, void* ptr, void* stream);
+
+typedef struct {
+  int32_t device;          /* CUDA device ordinal */
+  int32_t debug;           /* 1: device checks (demotion trap, range) */
+  int32_t plan_only;       /* 1: no device at all; sg_flush plans and counts only */
+  int32_t lowering;        /* 0: folded (no clear-list tasks); 1: paper-faithful
+                              clear-list + listgen per sparse level */
+  void* stream;            /* cudaStream_t the grid launches on (borrowed); NULL = default */
+  sg_alloc_fn alloc;
+  sg_free_fn free;
+  void* alloc_ctx;
+  int64_t pool_capacity;   /* max containers per pointer level; 0 = every pointer cell */
+  int64_t list_capacity;   /* max entries of any element list; 0 = derived from pools */
+} sg_opts;
+
+typedef struct sg_grid sg_grid;
+
+/* Validates the tree, derives the container layout and allocates: per pointer
+ * level a pool of containers (zeroed: zero-on-free invariant), per sparse level
+ * a list buffer with a device-side count, and the device error word. */
+sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_opts* opts, sg_grid** out);
+sg_status sg_destroy(sg_grid* g);
+
+/* Registers an external SoA particle array (ncomp components of n elements,
+ * component c at dev_ptr + c*n) as a Value state usable by range-for ops. */
+sg_status sg_register_array(sg_grid* g, void* dev_ptr, int64_t n, int32_t dtype, int32_t ncomp, int32_t* id);
+
+/* --- task vocabulary --------------------------------------------------------- */
+enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
+
+/* Ops.  Operand roles by slot (fields[i]); params p[i].  Access patterns are
+ * what the planner's fusion/demotion rules read.
+ *   FILL        struct-for  f0[c] = p0                        f0 identity, complete
+ *   ADD_CONST   struct-for  f0[c] = f1[c] + p0                 chain_copy
+ *   INC         struct-for  f0[c] += p0                        increments
+ *   AXPY        struct-for  f0[c] = p0*f1[c] + f2[c]           sparse_saxpy
+ *   STENCIL     struct-for  f0[c] = sum_nbr f1 - 2D f1[c]      f1 neighbour access
+ *   JACOBI      struct-for  f0[c] = (f2[c] + sum_nbr f1)/(2D)  f1 neighbour access
+ *   REDUCE_SUM  struct-for  f0[] += f1[c]                      f0 0-D
+ *   DOWNSAMPLE  struct-for  f0[c//2] += p0*f1[c] + p1          PAPER.md:350, Fig. 3
+ *   JITTER      struct-for  f0[c] += f0[c+e0] for even c0      deep_hierarchy
+ *   CLEAR_SCALAR serial     f0[] = 0
+ *   P2G / GRID_OP / G2P     MLS-MPM transfer ops
+ * Inactive or out-of-bound reads give 0. */
+enum {
+  SG_OP_FILL = 1, SG_OP_ADD_CONST = 2, SG_OP_INC = 3, SG_OP_AXPY = 4, SG_OP_STENCIL = 5,
+  SG_OP_JACOBI = 6, SG_OP_REDUCE_SUM = 7, SG_OP_DOWNSAMPLE = 8, SG_OP_JITTER = 9,
+  SG_OP_CLEAR_SCALAR = 10,
+  SG_OP_P2G = 20, SG_OP_GRID_OP = 21, SG_OP_G2P = 22
+};
+
+typedef struct {
+  int32_t kind;         /* SG_TASK_* */
+  int32_t op;           /* SG_OP_* */
+  int32_t snode;        /* struct-for: the LEAF level of the iterated tree */
+  int32_t pad_;
+  int64_t range_n;      /* range-for: loop extent */
+  int32_t fields[8];    /* operand field ids, -1 = unused */
+  int32_t arrays[8];    /* operand array ids (range-for), -1 = unused */
+  uint32_t activating;  /* bit i: fields[i] is written with activation-on-write */
+  float params[8];
+} sg_task;
+
+/* Enqueue: activate the cells at `dev_coords` (n x ndim int32, row-major,
+ * device memory, borrowed) of `field`'s tree: every sparse ancestor becomes
+ * active; newly active cells read 0. */
+sg_status sg_activate(sg_grid* g, int32_t field, const int32_t* dev_coords, int64_t n);
+/* Enqueue: generate the element lists of every sparse level from the top of
+ * snode's chain down to snode. */
+sg_status sg_listgen(sg_grid* g, int32_t snode);
+/* Enqueue one kernel-level task (struct-for / range-for / serial). */
+sg_status sg_struct_for(sg_grid* g, const sg_task* t);
+
+enum { SG_CLEAR_VALUES = 0, SG_DEACTIVATE = 1 };
+/* Enqueue: SG_CLEAR_VALUES: target = field id, store 0 on every active cell.
+ *          SG_DEACTIVATE:   target = sparse snode id, every cell of that level
+ *          and below becomes inactive, payload zeroed, pointer children freed. */
+sg_status sg_clear(sg_grid* g, int32_t target, int32_t mode);
+
+/* Pass toggles: */
+enum {
+  SG_PASS_LISTGEN_REMOVAL = 1,   /* section 6.2 */
+  SG_PASS_ACT_DEMOTION = 2,      /* section 6.3 */
+  SG_PASS_FUSION = 4,            /* section 6.4 */
+  SG_PASS_DSE = 8,               /* section 6.5 */
+  SG_PASS_ALL = 15
+};
+
+typedef struct {
+  int64_t tasks_lowered;        /* tasks in the eager lowering of this flush */
+  int64_t launches;             /* kernels launched by this flush */
+  int64_t listgen_launched;
+  int64_t clear_list_launched;
+  int64_t listgens_removed;
+  int64_t demotions;            /* activating operands demoted (incl. removed repeats) */
+  int64_t tasks_fused;          /* tasks merged into another task */
+  int64_t dead_removed;         /* tasks removed by DSE */
+  int64_t plan_cache_hits;
+  int64_t plan_cache_misses;
+  double plan_us;               /* host planning time of this flush */
+} sg_stats;
+
+/* Optimize and launch the queue.  passes = 0 launches one kernel per lowered
+ * task in program order (the eager baseline).  observed: field ids whose final
+ * values the caller will read (NULL / n_observed < 0: every field and array);
+ * masks are always observed.  out may be NULL. */
+sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observed, int32_t n_observed, sg_stats* out);
+/* Wait for the grid's stream; report a latched device error. */
+sg_status sg_sync(sg_grid* g);
+
+/* Exports (flush + sync).  Coordinates are level-global (row-major n x ndim). */
+sg_status sg_export_mask(sg_grid* g, int32_t snode, int32_t* host_coords, int64_t cap, int64_t* count);
+sg_status sg_export_list(sg_grid* g, int32_t snode, int32_t* host_coords, int64_t cap, int64_t* count);
+/* Dense bounding array of a field (row-major, last axis fastest); inactive -> 0. */
+sg_status sg_read_field(sg_grid* g, int32_t field, void* host_dense, int64_t bytes);
+/* State handoff: overwrite the values of the ACTIVE cells of a field from a
+ * dense host array (inactive entries ignored). */
+sg_status sg_load_field(sg_grid* g, int32_t field, const void* host_dense, int64_t bytes);
+
+/* The launch plan of the last flush, for host-side tests: `count` records of
+ * 6 int32 {group, task_type, call_index, snode, activating, flags}.  task_type:
+ * 0 activate, 1 listgen, 2 clear_list, 3 struct_for, 4 range_for, 5 serial,
+ * 6 deactivate.  call_index = index of the enqueue call within the flush window. */
+sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count);
+
+/* Device pointer of the payload pool / counters, for benchmarks (read-only). */
+sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
+
+const char* sg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SG_H_ */

@@ -1,0 +1,990 @@
+// kernels.cu -- sm_100a kernels of the sparse-grid hot path.
+//
+//   k_activate      explicit activation: CAS-published pointer
+//                   allocation from a zeroed pool + atomicOr on bitmask words.
+//   k_listgen       element-list generation: 32 children
+//                   per thread as one bit word, block scan, single-pass decoupled
+//                   look-back for a deterministic order; persistent grid with
+//                   dynamic tile order; counts stay on the device.
+//   k_struct_for    fused struct-for megakernel:
+//                   one tile of leaf blocks per CTA iteration, an op table
+//                   interpreted per cell with every identity access kept in the
+//                   same thread (atomic demotion).
+//   k_deactivate    DEACTIVATE(S): zero payload of active blocks, clear masks,
+//                   push pointer children to the free list (zero-on-free).
+//   k_serial / k_range_for, export helpers.
+// No host synchronization anywhere on the hot path: list counts are read on
+// the device and every kernel grid-strides over them.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <algorithm>
+#include "sg_internal.h"
+#include "mpm_ops.cuh"
+
+namespace sg {
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) { return *(volatile const uint32_t*)p; }
+__device__ __forceinline__ uint64_t ld_volatile64(const uint64_t* p) { return *(volatile const uint64_t*)p; }
+
+__device__ __forceinline__ void set_err(const DevCtx& C, int code, int task) {
+  if (atomicCAS(&C.err[0], 0u, (uint32_t)code) == 0u) C.err[1] = (uint32_t)task;
+}
+
+__device__ __forceinline__ uint32_t local_lin(const DLevel& L, const int c[3]) {
+  uint32_t l0 = ((uint32_t)c[0] >> L.lbelow[0]) & ((1u << L.le[0]) - 1u);
+  uint32_t l1 = ((uint32_t)c[1] >> L.lbelow[1]) & ((1u << L.le[1]) - 1u);
+  uint32_t l2 = ((uint32_t)c[2] >> L.lbelow[2]) & ((1u << L.le[2]) - 1u);
+  return (((l0 << L.le[1]) | l1) << L.le[2]) | l2;
+}
+
+__device__ __forceinline__ bool in_domain(const DTree& T, const int c[3]) {
+  const DLevel& L = T.lev[T.nlev - 1];
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+    if (c[a] < 0 || c[a] >= (1 << L.lres[a])) return false;
+  return true;
+}
+
+__device__ __forceinline__ uint32_t* cont_ptr(const DTree& T, int seg, uint32_t slot) {
+  return T.seg[seg].base + (uint64_t)slot * T.seg[seg].stride;
+}
+
+// Non-activating tree walk: leaf container + leaf index of cell c, or null if
+// a pointer ancestor is NULL.  Bitmasks are not tested (zero-on-free).
+__device__ __forceinline__ uint32_t* locate(const DTree& T, const int c[3], uint32_t& idx) {
+  uint32_t* cont = T.seg[0].base;
+  idx = 0;
+  for (int l = 0; l < T.nlev; l++) {
+    const DLevel& L = T.lev[l];
+    idx = (idx << L.lE) | local_lin(L, c);
+    if (L.kind == SG_POINTER) {
+      uint32_t v = cont[L.slot_off + idx];
+      if (v == SG_SLOT_NULL || v == SG_SLOT_BUSY) return nullptr;
+      cont = cont_ptr(T, L.seg + 1, v - 1u);
+      idx = 0;
+    }
+  }
+  return cont;
+}
+
+// Full activity test: every sparse ancestor set.
+__device__ __forceinline__ uint32_t* locate_active(const DTree& T, const int c[3], uint32_t& idx) {
+  uint32_t* cont = T.seg[0].base;
+  idx = 0;
+  for (int l = 0; l < T.nlev; l++) {
+    const DLevel& L = T.lev[l];
+    idx = (idx << L.lE) | local_lin(L, c);
+    if (L.kind == SG_BITMASKED) {
+      if (!((cont[L.mask_off + (idx >> 5)] >> (idx & 31)) & 1u)) return nullptr;
+    } else if (L.kind == SG_POINTER) {
+      uint32_t v = cont[L.slot_off + idx];
+      if (v == SG_SLOT_NULL || v == SG_SLOT_BUSY) return nullptr;
+      cont = cont_ptr(T, L.seg + 1, v - 1u);
+      idx = 0;
+    }
+  }
+  return cont;
+}
+
+__device__ int32_t pool_pop(const DSeg& S) {
+  int32_t top = atomicSub(&S.alloc[1], 1);
+  if (top > 0) return (int32_t)S.free_list[top - 1];
+  atomicAdd(&S.alloc[1], 1);
+  int32_t b = atomicAdd(&S.alloc[0], 1);
+  if (b >= (int32_t)S.capacity) return -1;
+  return b;
+}
+
+// Pointer child acquisition (PAPER.md:166 allocator; SURVEY.md s7 hard part 1):
+// CAS NULL->BUSY, pop the pool, record the origin, publish slot with release.
+__device__ int32_t acquire_child(const DevCtx& C, const DTree& T, const DLevel& L, uint32_t* cont, uint32_t idx,
+                                 const int c[3], int task) {
+  uint32_t* sp = cont + L.slot_off + idx;
+  uint32_t v = ld_acquire(sp);
+  if (v != SG_SLOT_NULL && v != SG_SLOT_BUSY) return (int32_t)(v - 1u);
+  if (v == SG_SLOT_NULL) {
+    uint32_t old = atomicCAS(sp, SG_SLOT_NULL, SG_SLOT_BUSY);
+    if (old == SG_SLOT_NULL) {
+      const DSeg& S = T.seg[L.seg + 1];
+      int32_t got = pool_pop(S);
+      if (got < 0) {
+        set_err(C, SG_ERR_POOL_EXHAUSTED, task);
+        atomicExch(sp, SG_SLOT_NULL);
+        return -1;
+      }
+#pragma unroll
+      for (int a = 0; a < 3; a++) S.origin[got * 3 + a] = c[a] >> L.lbelow[a];
+      __threadfence();
+      atomicExch(sp, (uint32_t)got + 1u);
+      return got;
+    }
+    v = old;
+  }
+  while (v == SG_SLOT_BUSY) {
+    __nanosleep(20);
+    v = ld_acquire(sp);
+  }
+  if (v == SG_SLOT_NULL) return -1;
+  return (int32_t)(v - 1u);
+}
+
+// Activating walk: every sparse ancestor of c becomes
+// active; returns the leaf container + index.  Idempotent; never touches payload.
+__device__ uint32_t* activate_walk(const DevCtx& C, const DTree& T, const int c[3], uint32_t& idx, int task) {
+  uint32_t* cont = T.seg[0].base;
+  idx = 0;
+  for (int l = 0; l < T.nlev; l++) {
+    const DLevel& L = T.lev[l];
+    idx = (idx << L.lE) | local_lin(L, c);
+    if (L.kind == SG_BITMASKED) {
+      uint32_t* w = cont + L.mask_off + (idx >> 5);
+      uint32_t b = 1u << (idx & 31);
+      if (!(ld_volatile(w) & b)) atomicOr(w, b);
+    } else if (L.kind == SG_POINTER) {
+      int32_t s = acquire_child(C, T, L, cont, idx, c, task);
+      if (s < 0) return nullptr;
+      cont = cont_ptr(T, L.seg + 1, (uint32_t)s);
+      idx = 0;
+    }
+  }
+  return cont;
+}
+
+// Level-global coordinates of the level-l cell (container slot cs, index idx).
+__device__ void cell_coords(const DTree& T, int l, uint32_t cs, uint32_t idx, int g[3]) {
+  const DLevel& L = T.lev[l];
+  const DSeg& S = T.seg[L.seg];
+  int acc[3] = {0, 0, 0}, sh[3] = {0, 0, 0};
+  for (int m = l; m >= S.first; m--) {
+    const DLevel& M = T.lev[m];
+    uint32_t d = idx & ((1u << M.lE) - 1u);
+    idx >>= M.lE;
+    uint32_t d2 = d & ((1u << M.le[2]) - 1u);
+    uint32_t d1 = (d >> M.le[2]) & ((1u << M.le[1]) - 1u);
+    uint32_t d0 = d >> (M.le[1] + M.le[2]);
+    acc[0] |= (int)(d0 << sh[0]); sh[0] += M.le[0];
+    acc[1] |= (int)(d1 << sh[1]); sh[1] += M.le[1];
+    acc[2] |= (int)(d2 << sh[2]); sh[2] += M.le[2];
+  }
+  int o[3] = {0, 0, 0};
+  if (L.seg > 0) { o[0] = S.origin[cs * 3]; o[1] = S.origin[cs * 3 + 1]; o[2] = S.origin[cs * 3 + 2]; }
+#pragma unroll
+  for (int a = 0; a < 3; a++) g[a] = (o[a] << sh[a]) | acc[a];
+}
+
+// Index of leaf cell c within its block (levels below the driving level).
+__device__ __forceinline__ uint32_t inblock_idx(const DTree& T, const int c[3]) {
+  uint32_t idx = 0;
+  for (int l = T.driving + 1; l < T.nlev; l++) idx = (idx << T.lev[l].lE) | local_lin(T.lev[l], c);
+  return idx;
+}
+
+// Block-local coordinates of in-block index j.
+__device__ __forceinline__ void inblock_coords(const DTree& T, uint32_t j, int c[3]) {
+  c[0] = c[1] = c[2] = 0;
+  for (int m = T.nlev - 1; m > T.driving; m--) {
+    const DLevel& M = T.lev[m];
+    uint32_t d = j & ((1u << M.lE) - 1u);
+    j >>= M.lE;
+    c[2] |= (int)((d & ((1u << M.le[2]) - 1u)) << M.lbelow[2]);
+    c[1] |= (int)(((d >> M.le[2]) & ((1u << M.le[1]) - 1u)) << M.lbelow[1]);
+    c[0] |= (int)((d >> (M.le[1] + M.le[2])) << M.lbelow[0]);
+  }
+}
+
+// Resolve a driving-list entry to (leaf container, first leaf idx, origin in leaf units).
+__device__ __forceinline__ bool resolve_entry(const DTree& T, uint32_t e, uint32_t*& cont, uint32_t& first,
+                                              int org[3]) {
+  if (T.driving < 0) {
+    cont = T.seg[0].base; first = 0; org[0] = org[1] = org[2] = 0;
+    return true;
+  }
+  const DLevel& D = T.lev[T.driving];
+  uint32_t cs = e >> D.ln, idx = e & ((1u << D.ln) - 1u);
+  int g[3];
+  cell_coords(T, T.driving, cs, idx, g);
+#pragma unroll
+  for (int a = 0; a < 3; a++) org[a] = g[a] << D.lbelow[a];
+  uint32_t* dc = cont_ptr(T, D.seg, cs);
+  if (D.kind == SG_POINTER) {
+    uint32_t v = dc[D.slot_off + idx];
+    if (v == SG_SLOT_NULL || v == SG_SLOT_BUSY) return false;
+    cont = cont_ptr(T, D.seg + 1, v - 1u);
+    first = 0;
+  } else {
+    cont = dc;
+    first = idx << (T.ln_leaf - D.ln);
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Activation
+// ---------------------------------------------------------------------------
+struct ActArgs {
+  DTree T;
+  DevCtx C;
+  const int32_t* coords;
+  int64_t n;
+  int task;
+};
+
+__global__ void __launch_bounds__(256) k_activate(const __grid_constant__ ActArgs a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c[3] = {0, 0, 0};
+    for (int d = 0; d < a.T.nd; d++) c[d] = a.coords[i * a.T.nd + d];
+    if (!in_domain(a.T, c)) { set_err(a.C, SG_ERR_RANGE, a.task); continue; }
+    uint32_t idx;
+    activate_walk(a.C, a.T, c, idx, a.task);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Listgen
+// ---------------------------------------------------------------------------
+struct LGArgs {
+  DTree T;
+  DevCtx C;
+  int ls, lp, mode;     // mode 0: root parent, 1: parent in same segment, 2: parent pointer of previous segment
+  int lratio, lcpp, nbits;
+  const uint32_t* pentries;
+  const uint32_t* pcount;
+  DList out;
+  int task;
+};
+
+constexpr int LG_TPB = 256, LG_CPT = 4, LG_TILE = LG_TPB * LG_CPT;
+
+__device__ __forceinline__ uint32_t lg_chunk(const LGArgs& a, uint64_t chunk, uint32_t& cslot, uint32_t& first) {
+  uint32_t p = (uint32_t)(chunk >> a.lcpp), sub = (uint32_t)(chunk & ((1u << a.lcpp) - 1u));
+  const DLevel& S = a.T.lev[a.ls];
+  const uint32_t* cont;
+  if (a.mode == 0) {
+    cslot = 0; first = sub * 32u; cont = a.T.seg[0].base;
+  } else {
+    const DLevel& P = a.T.lev[a.lp];
+    uint32_t e = a.pentries[p];
+    uint32_t ps = e >> P.ln, pidx = e & ((1u << P.ln) - 1u);
+    if (a.mode == 1) {
+      cslot = ps; first = (pidx << a.lratio) + sub * 32u; cont = cont_ptr(a.T, S.seg, ps);
+    } else {
+      const uint32_t* pc = cont_ptr(a.T, P.seg, ps);
+      uint32_t v = pc[P.slot_off + pidx];
+      if (v == SG_SLOT_NULL || v == SG_SLOT_BUSY) { cslot = 0; first = 0; return 0u; }
+      cslot = v - 1u; first = sub * 32u; cont = cont_ptr(a.T, S.seg, cslot);
+    }
+  }
+  uint32_t bits = 0;
+  if (S.kind == SG_BITMASKED) {
+    uint32_t w = cont[S.mask_off + (first >> 5)];
+    bits = a.nbits == 32 ? w : ((w >> (first & 31u)) & ((1u << a.nbits) - 1u));
+  } else {
+    const uint32_t* sl = cont + S.slot_off + first;
+    for (int k = 0; k < a.nbits; k++) bits |= (sl[k] != SG_SLOT_NULL ? 1u : 0u) << k;
+  }
+  return bits;
+}
+
+__device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint32_t v) {
+  return ((uint64_t)(epoch & 0x3FFFFFFFu) << 34) | ((uint64_t)flag << 32) | v;
+}
+
+__global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGArgs a) {
+  __shared__ uint32_t s_warp[LG_TPB / 32];
+  __shared__ uint32_t s_tile, s_base, s_epoch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_epoch = ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu;
+  uint32_t nparent = a.mode == 0 ? 1u : ld_volatile(a.pcount);
+  uint64_t nchunks = (uint64_t)nparent << a.lcpp;
+  uint32_t ntiles = (uint32_t)((nchunks + LG_TILE - 1) / LG_TILE);
+  const uint32_t lnS = a.T.lev[a.ls].ln;
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  while (true) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&a.out.ctl[0], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    uint32_t bits[LG_CPT], cs[LG_CPT], fs[LG_CPT];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < LG_CPT; k++) {
+      uint64_t ch = (uint64_t)tile * LG_TILE + threadIdx.x * LG_CPT + k;
+      bits[k] = ch < nchunks ? lg_chunk(a, ch, cs[k], fs[k]) : 0u;
+      cnt += __popc(bits[k]);
+    }
+    // block exclusive scan
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = lane < LG_TPB / 32 ? s_warp[lane] : 0u, wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      if (lane < LG_TPB / 32) s_warp[lane] = wi - w;   // exclusive warp offsets
+      uint32_t total = __shfl_sync(0xffffffffu, wi, LG_TPB / 32 - 1);
+      if (lane == 0) {
+        // single-pass decoupled look-back (deterministic order of tiles)
+        uint64_t* st = a.out.status;
+        uint32_t prefix = 0;
+        if (tile == 0) {
+          atomicExch((unsigned long long*)&st[0], (unsigned long long)lb_pack(epoch, 2u, total));
+        } else {
+          atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 1u, total));
+          int64_t j = (int64_t)tile - 1;
+          while (true) {
+            uint64_t s = ld_volatile64(&st[j]);
+            uint32_t ep = (uint32_t)(s >> 34), fl = (uint32_t)(s >> 32) & 3u;
+            if (ep != epoch || fl == 0u) { __nanosleep(8); continue; }
+            prefix += (uint32_t)s;
+            if (fl == 2u) break;
+            j--;
+          }
+          atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, prefix + total));
+        }
+        s_base = prefix;
+        if (tile == ntiles - 1) {
+          uint32_t n = prefix + total;
+          if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
+          *a.out.count = n;
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t off = s_base + s_warp[warp] + (inc - cnt);
+#pragma unroll
+    for (int k = 0; k < LG_CPT; k++) {
+      uint32_t b = bits[k];
+      while (b) {
+        int t = __ffs(b) - 1;
+        b &= b - 1;
+        if (off < a.out.capacity) a.out.entries[off] = (cs[k] << lnS) | (fs[k] + (uint32_t)t);
+        off++;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.out.ctl[1], 1u) == gridDim.x - 1) {
+      if (ntiles == 0) *a.out.count = 0;
+      a.out.ctl[0] = 0;
+      a.out.ctl[1] = 0;
+      a.out.ctl[2] = a.out.ctl[2] + 1u;
+      __threadfence();
+    }
+  }
+}
+
+__global__ void k_clear_list(uint32_t* count) { *count = 0; }
+
+// ---------------------------------------------------------------------------
+// Struct-for megakernel
+// ---------------------------------------------------------------------------
+struct SFArgs {
+  DTree T;
+  DevCtx C;
+  const uint32_t* entries;   // driving list (null when the tree has no driving level)
+  const uint32_t* count;
+  int nops;
+  int need_nbr;
+  int lept;                  // log2 entries per tile
+  int lchunk;                // log2 cells per tile when a block spans several tiles (else -1)
+  int task;
+  DOp ops[SG_MAXOPS];
+  uint64_t aux[SG_MAXOPS];   // 0-D target address per op
+};
+
+constexpr int SF_TPB = 256, SF_MAXE = 256;
+
+struct SFTile {
+  uint32_t* blk0[SF_MAXE];     // payload of field slot 0, first cell of the block
+  uint32_t* cont[SF_MAXE];
+  uint32_t first[SF_MAXE];
+  int org[SF_MAXE][3];
+  uint32_t* nbr[SF_MAXE][6];   // neighbour blocks (field slot 0, first cell), null = absent
+};
+
+template <typename V> __device__ __forceinline__ V ldv(const uint32_t* p);
+template <> __device__ __forceinline__ float ldv<float>(const uint32_t* p) { return __uint_as_float(*p); }
+template <> __device__ __forceinline__ int ldv<int>(const uint32_t* p) { return (int)*p; }
+__device__ __forceinline__ void stv(uint32_t* p, float v) { *p = __float_as_uint(v); }
+__device__ __forceinline__ void stv(uint32_t* p, int v) { *p = (uint32_t)v; }
+
+struct CellCtx {
+  const DTree* T;
+  const SFTile* tile;
+  int e;                 // entry slot in the tile
+  uint32_t j;            // in-block index
+  int c[3];              // leaf coords
+  uint64_t fstride;      // words between field slots
+};
+
+template <typename V>
+__device__ __forceinline__ V ld_id(const CellCtx& x, int slot) {
+  return ldv<V>(x.tile->blk0[x.e] + (uint64_t)slot * x.fstride + x.j);
+}
+template <typename V>
+__device__ __forceinline__ void st_id(const CellCtx& x, int slot, V v) {
+  stv(x.tile->blk0[x.e] + (uint64_t)slot * x.fstride + x.j, v);
+}
+
+// Neighbour value c + d*e_axis (0 when inactive / out of bound).
+template <typename V>
+__device__ __forceinline__ V ld_nbr(const CellCtx& x, int slot, int axis, int d) {
+  const DTree& T = *x.T;
+  int n[3] = {x.c[0], x.c[1], x.c[2]};
+  n[axis] += d;
+  const int bdim = T.driving < 0 ? (1 << T.lev[T.nlev - 1].lres[axis]) : (1 << T.lev[T.driving].lbelow[axis]);
+  int rel = n[axis] - x.tile->org[x.e][axis];
+  const uint32_t* base;
+  if (rel >= 0 && rel < bdim) {
+    base = x.tile->blk0[x.e];
+  } else {
+    if (T.driving < 0) return V(0);
+    base = x.tile->nbr[x.e][axis * 2 + (d > 0 ? 1 : 0)];
+    if (!base) return V(0);
+  }
+  return ldv<V>(base + (uint64_t)slot * x.fstride + inblock_idx(T, n));
+}
+
+template <typename V>
+__device__ __forceinline__ V nbr_sum(const CellCtx& x, int slot) {
+  V s = V(0);
+  for (int a = 0; a < x.T->nd; a++) s += ld_nbr<V>(x, slot, a, -1) + ld_nbr<V>(x, slot, a, +1);
+  return s;
+}
+
+template <typename V>
+__device__ __forceinline__ void apply_downsample(const SFArgs& A, const DOp& op, const CellCtx& x, V val) {
+  const DField& tf = A.C.fields[op.f[0]];
+  const DTree& T2 = A.C.trees[tf.tree];
+  int h[3] = {x.c[0] >> 1, x.c[1] >> 1, x.c[2] >> 1};
+  uint32_t idx;
+  uint32_t* cont;
+  if (op.act & 1u) {
+    cont = activate_walk(A.C, T2, h, idx, A.task);
+  } else {
+    cont = A.C.debug ? locate_active(T2, h, idx) : locate(T2, h, idx);
+    if (!cont && A.C.debug) set_err(A.C, SG_ERR_DEMOTION_TRAP, A.task);
+  }
+  if (!cont) return;
+  uint32_t* p = cont + T2.payload_off + ((uint64_t)tf.slot << T2.ln_leaf) + idx;
+  if (sizeof(V) == 4 && V(0.5) != V(0)) atomicAdd((float*)p, (float)val);
+  else atomicAdd((int*)p, (int)val);
+}
+
+template <typename V>
+__device__ __forceinline__ void apply_op(const SFArgs& A, const DOp& op, int o, const CellCtx& x, V* acc) {
+  const int D = x.T->nd;
+  switch (op.op) {
+    case SG_OP_FILL: st_id<V>(x, op.slot[0], (V)op.p[0]); break;
+    case SG_OP_ADD_CONST: st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[1]) + (V)op.p[0]); break;
+    case SG_OP_INC: st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + (V)op.p[0]); break;
+    case SG_OP_AXPY: st_id<V>(x, op.slot[0], (V)op.p[0] * ld_id<V>(x, op.slot[1]) + ld_id<V>(x, op.slot[2])); break;
+    case SG_OP_STENCIL: {
+      V s = nbr_sum<V>(x, op.slot[1]) - (V)(2 * D) * ld_id<V>(x, op.slot[1]);
+      st_id<V>(x, op.slot[0], s);
+    } break;
+    case SG_OP_JACOBI: {
+      V s = ld_id<V>(x, op.slot[2]) + nbr_sum<V>(x, op.slot[1]);
+      st_id<V>(x, op.slot[0], s / (V)(2 * D));
+    } break;
+    case SG_OP_REDUCE_SUM: acc[o] += ld_id<V>(x, op.slot[1]); break;
+    case SG_OP_DOWNSAMPLE: {
+      V v = op.slot[1] >= 0 ? ld_id<V>(x, op.slot[1]) : V(0);
+      apply_downsample<V>(A, op, x, (V)op.p[0] * v + (V)op.p[1]);
+    } break;
+    case SG_OP_JITTER:
+      if ((x.c[0] & 1) == 0) st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + ld_nbr<V>(x, op.slot[0], 0, +1));
+      break;
+    case SG_OP_GRID_OP: mpm_grid_op(op, x.c, x.tile->blk0[x.e] + x.j, x.fstride); break;
+    default: break;
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void run_cell(const SFArgs& A, const CellCtx& x, V* acc) {
+#pragma unroll
+  for (int o = 0; o < SG_MAXOPS; o++) {
+    if (o >= A.nops) break;
+    apply_op<V>(A, A.ops[o], o, x, acc);
+  }
+}
+
+template <typename V>
+__device__ void block_reduce_add(const SFArgs& A, V* acc) {
+  __shared__ V s_red[SF_TPB / 32];
+#pragma unroll
+  for (int o = 0; o < SG_MAXOPS; o++) {
+    if (o >= A.nops) break;
+    if (A.ops[o].op != SG_OP_REDUCE_SUM) continue;
+    V v = acc[o];
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      V t = V(0);
+      for (int w = 0; w < SF_TPB / 32; w++) t += s_red[w];
+      if (sizeof(V) == 4 && V(0.5) != V(0)) atomicAdd((float*)A.aux[o], (float)t);
+      else atomicAdd((int*)A.aux[o], (int)t);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(SF_TPB) k_struct_for(const __grid_constant__ SFArgs A) {
+  __shared__ SFTile tile;
+  const DTree& T = A.T;
+  const uint32_t nent = A.entries ? ld_volatile(A.count) : 1u;
+  const int lblk = T.lblk;
+  const int ept = 1 << A.lept;
+  uint64_t ntiles;
+  int tiles_per_entry = 1;
+  if (A.lchunk >= 0) {
+    tiles_per_entry = 1 << (lblk - A.lchunk);
+    ntiles = (uint64_t)nent * tiles_per_entry;
+  } else {
+    ntiles = (nent + ept - 1) >> A.lept;
+  }
+  const uint64_t fstride = 1ull << T.ln_leaf;
+  V acc[SG_MAXOPS];
+#pragma unroll
+  for (int o = 0; o < SG_MAXOPS; o++) acc[o] = V(0);
+
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint32_t e0, ne;
+    uint32_t jbase = 0, tcells;
+    if (A.lchunk >= 0) {
+      e0 = (uint32_t)(t / tiles_per_entry);
+      ne = 1;
+      jbase = (uint32_t)(t % tiles_per_entry) << A.lchunk;
+      tcells = 1u << A.lchunk;
+    } else {
+      e0 = (uint32_t)(t << A.lept);
+      ne = min((uint32_t)ept, nent - e0);
+      tcells = ne << lblk;
+    }
+    // resolve the tile's entries (and neighbour blocks) into shared memory
+    for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
+      uint32_t* cont;
+      uint32_t first;
+      int org[3];
+      bool ok = resolve_entry(T, A.entries ? A.entries[e0 + i] : 0u, cont, first, org);
+      tile.cont[i] = ok ? cont : nullptr;
+      tile.blk0[i] = ok ? cont + T.payload_off + first : nullptr;
+      tile.first[i] = first;
+      tile.org[i][0] = org[0]; tile.org[i][1] = org[1]; tile.org[i][2] = org[2];
+    }
+    __syncthreads();
+    if (A.need_nbr && T.driving >= 0) {
+      const int nd2 = 2 * T.nd;
+      for (uint32_t i = threadIdx.x; i < ne * nd2; i += SF_TPB) {
+        uint32_t e = i / nd2;
+        int dir = i % nd2, axis = dir >> 1, s = (dir & 1) ? 1 : -1;
+        int q[3] = {tile.org[e][0], tile.org[e][1], tile.org[e][2]};
+        q[axis] += s > 0 ? (1 << T.lev[T.driving].lbelow[axis]) : -1;
+        uint32_t* nb = nullptr;
+        if (tile.blk0[e] && in_domain(T, q)) {
+          uint32_t idx;
+          uint32_t* c2 = locate(T, q, idx);
+          if (c2) nb = c2 + T.payload_off + (idx & ~((1u << lblk) - 1u));
+        }
+        tile.nbr[e][dir] = nb;
+      }
+      __syncthreads();
+    }
+    for (uint32_t i = threadIdx.x; i < tcells; i += SF_TPB) {
+      CellCtx x;
+      x.T = &T;
+      x.tile = &tile;
+      x.e = A.lchunk >= 0 ? 0 : (int)(i >> lblk);
+      x.j = A.lchunk >= 0 ? jbase + i : (i & ((1u << lblk) - 1u));
+      x.fstride = fstride;
+      if (!tile.blk0[x.e]) continue;
+      if (T.leaf_bitmasked) {
+        const DLevel& LL = T.lev[T.nlev - 1];
+        uint32_t li = tile.first[x.e] + x.j;
+        if (!((tile.cont[x.e][LL.mask_off + (li >> 5)] >> (li & 31)) & 1u)) continue;
+      }
+      int bc[3];
+      inblock_coords(T, x.j, bc);
+      x.c[0] = tile.org[x.e][0] + bc[0];
+      x.c[1] = tile.org[x.e][1] + bc[1];
+      x.c[2] = tile.org[x.e][2] + bc[2];
+      run_cell<V>(A, x, acc);
+    }
+    __syncthreads();
+  }
+  block_reduce_add<V>(A, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Serial and range-for
+// ---------------------------------------------------------------------------
+struct SerArgs {
+  DevCtx C;
+  int nops;
+  DOp ops[SG_MAXOPS];
+  uint64_t aux[SG_MAXOPS];
+};
+
+__global__ void k_serial(const __grid_constant__ SerArgs A) {
+  for (int o = 0; o < A.nops; o++) {
+    if (A.ops[o].op == SG_OP_CLEAR_SCALAR) *(uint32_t*)A.aux[o] = 0u;
+  }
+}
+
+struct RFArgs {
+  DevCtx C;
+  int64_t n;
+  int nops;
+  int task;
+  DOp ops[SG_MAXOPS];
+};
+
+__global__ void __launch_bounds__(128) k_range_for(const __grid_constant__ RFArgs A) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int o = 0; o < A.nops; o++) {
+      const DOp& op = A.ops[o];
+      switch (op.op) {
+        case SG_OP_P2G: mpm_p2g(A.C, op, i, A.task); break;
+        case SG_OP_G2P: mpm_g2p(A.C, op, i); break;
+        default: break;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deactivate (reading R7): payload zeroed, masks cleared, children freed.
+// ---------------------------------------------------------------------------
+struct DeArgs {
+  DTree T;
+  DevCtx C;
+  int ls;
+  const uint32_t* drive_entries;
+  const uint32_t* drive_count;
+  const uint32_t* lent[SG_MAXL];
+  const uint32_t* lcnt[SG_MAXL];
+};
+
+__global__ void __launch_bounds__(256) k_deactivate(const __grid_constant__ DeArgs A) {
+  const DTree& T = A.T;
+  const uint32_t nblk = A.drive_entries ? ld_volatile(A.drive_count) : 1u;
+  const uint32_t blk = 1u << T.lblk;
+  const uint64_t fstride = 1ull << T.ln_leaf;
+  // phase 1: zero the payload (and leaf bits) of every active block
+  for (uint32_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    uint32_t* cont;
+    uint32_t first;
+    int org[3];
+    if (!resolve_entry(T, A.drive_entries ? A.drive_entries[b] : 0u, cont, first, org)) continue;
+    uint32_t* p0 = cont + T.payload_off + first;
+    for (int f = 0; f < T.nfields; f++)
+      for (uint32_t i = threadIdx.x; i < blk; i += blockDim.x) p0[(uint64_t)f * fstride + i] = 0u;
+    if (T.leaf_bitmasked) {
+      const DLevel& LL = T.lev[T.nlev - 1];
+      for (uint32_t w = (first >> 5) + threadIdx.x; w < ((first + blk + 31) >> 5); w += blockDim.x)
+        cont[LL.mask_off + w] = 0u;
+    }
+  }
+  // phase 2: every listed level at/below S
+  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gsz = (uint64_t)gridDim.x * blockDim.x;
+  for (int l = A.ls; l < T.nlev; l++) {
+    if (!A.lent[l]) continue;
+    const DLevel& L = T.lev[l];
+    uint32_t n = ld_volatile(A.lcnt[l]);
+    for (uint64_t i = gtid; i < n; i += gsz) {
+      uint32_t e = A.lent[l][i];
+      uint32_t cs = e >> L.ln, idx = e & ((1u << L.ln) - 1u);
+      uint32_t* cont = cont_ptr(T, L.seg, cs);
+      if (L.kind == SG_BITMASKED) {
+        cont[L.mask_off + (idx >> 5)] = 0u;
+      } else if (L.kind == SG_POINTER) {
+        uint32_t v = cont[L.slot_off + idx];
+        cont[L.slot_off + idx] = SG_SLOT_NULL;
+        if (v != SG_SLOT_NULL && v != SG_SLOT_BUSY) {
+          const DSeg& S = T.seg[L.seg + 1];
+          uint32_t* child = cont_ptr(T, L.seg + 1, v - 1u);
+          for (uint32_t w = 0; w < S.header_words; w++) child[w] = 0u;
+          int32_t pos = atomicAdd(&S.alloc[1], 1);
+          S.free_list[pos] = v - 1u;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Export / handoff helpers (tests and exports only)
+// ---------------------------------------------------------------------------
+struct FieldIO {
+  DTree T;
+  int slot;
+  uint32_t* dense;
+  const uint32_t* src;
+  int64_t total;
+  int sh[3];
+};
+
+__device__ __forceinline__ void dense_coords(const FieldIO& a, int64_t i, int c[3]) {
+  c[2] = (int)(i & ((1ll << a.sh[2]) - 1));
+  c[1] = (int)((i >> a.sh[2]) & ((1ll << a.sh[1]) - 1));
+  c[0] = (int)(i >> (a.sh[1] + a.sh[2]));
+}
+
+__global__ void k_read_field(const __grid_constant__ FieldIO a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.total; i += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    dense_coords(a, i, c);
+    uint32_t idx;
+    uint32_t* cont = locate(a.T, c, idx);
+    a.dense[i] = cont ? cont[a.T.payload_off + ((uint64_t)a.slot << a.T.ln_leaf) + idx] : 0u;
+  }
+}
+
+__global__ void k_load_field(const __grid_constant__ FieldIO a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.total; i += (int64_t)gridDim.x * blockDim.x) {
+    int c[3];
+    dense_coords(a, i, c);
+    uint32_t idx;
+    uint32_t* cont = locate_active(a.T, c, idx);
+    if (cont) cont[a.T.payload_off + ((uint64_t)a.slot << a.T.ln_leaf) + idx] = a.src[i];
+  }
+}
+
+struct MaskScan {
+  DTree T;
+  int level;
+  uint8_t* flags;
+  int64_t total;
+  int sh[3];
+};
+
+__global__ void k_mask_scan(const __grid_constant__ MaskScan a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.total; i += (int64_t)gridDim.x * blockDim.x) {
+    int g[3];
+    g[2] = (int)(i & ((1ll << a.sh[2]) - 1));
+    g[1] = (int)((i >> a.sh[2]) & ((1ll << a.sh[1]) - 1));
+    g[0] = (int)(i >> (a.sh[1] + a.sh[2]));
+    const DLevel& S = a.T.lev[a.level];
+    int c[3] = {g[0] << S.lbelow[0], g[1] << S.lbelow[1], g[2] << S.lbelow[2]};
+    uint32_t* cont = a.T.seg[0].base;
+    uint32_t idx = 0;
+    uint8_t act = 1;
+    for (int l = 0; l <= a.level; l++) {
+      const DLevel& L = a.T.lev[l];
+      idx = (idx << L.lE) | local_lin(L, c);
+      if (L.kind == SG_BITMASKED) {
+        if (!((cont[L.mask_off + (idx >> 5)] >> (idx & 31)) & 1u)) { act = 0; break; }
+      } else if (L.kind == SG_POINTER) {
+        uint32_t v = cont[L.slot_off + idx];
+        if (v == SG_SLOT_NULL || v == SG_SLOT_BUSY) { act = 0; break; }
+        if (l < a.level) { cont = cont_ptr(a.T, L.seg + 1, v - 1u); idx = 0; }
+      }
+    }
+    a.flags[i] = act;
+  }
+}
+
+struct ListDecode {
+  DTree T;
+  int level;
+  const uint32_t* entries;
+  const uint32_t* count;
+  int32_t* coords;
+};
+
+__global__ void k_list_decode(const __grid_constant__ ListDecode a) {
+  uint32_t n = *a.count;
+  const DLevel& L = a.T.lev[a.level];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t e = a.entries[i];
+    int g[3];
+    cell_coords(a.T, a.level, e >> L.ln, e & ((1u << L.ln) - 1u), g);
+    for (int d = 0; d < a.T.nd; d++) a.coords[(uint64_t)i * a.T.nd + d] = g[d];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+static int check_launch() { return cudaGetLastError() == cudaSuccess ? 0 : SG_ERR_CUDA; }
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int launch_activate(const DevCtx& c, const DTree& t, int, int, const int32_t* coords, int64_t n, int task,
+                    void* stream) {
+  if (n <= 0) return 0;
+  ActArgs a{t, c, coords, n, task};
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+  k_activate<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+int launch_listgen(const DevCtx& c, const DTree& t, int, int level, int parent_level, const DList* parent,
+                   const DList& out, int task, void* stream, int grid_hint) {
+  LGArgs a;
+  a.T = t; a.C = c; a.ls = level; a.lp = parent_level; a.out = out; a.task = task;
+  const DLevel& S = t.lev[level];
+  int lratio;
+  if (parent_level < 0) { a.mode = 0; lratio = S.ln; }
+  else if (t.lev[parent_level].seg == S.seg) { a.mode = 1; lratio = S.ln - t.lev[parent_level].ln; }
+  else { a.mode = 2; lratio = S.ln; }
+  a.lratio = lratio;
+  a.lcpp = lratio > 5 ? lratio - 5 : 0;
+  a.nbits = lratio >= 5 ? 32 : (1 << lratio);
+  a.pentries = parent ? parent->entries : nullptr;
+  a.pcount = parent ? parent->count : nullptr;
+  int grid = grid_hint > 0 ? grid_hint : 1;
+  grid = max(1, min(grid, num_sms() * 4));
+  k_listgen<<<grid, LG_TPB, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+int launch_clear_list(const DList& l, void* stream) {
+  k_clear_list<<<1, 1, 0, (cudaStream_t)stream>>>(l.count);
+  return check_launch();
+}
+
+static int ilog2(uint64_t v) { int r = 0; while ((1ull << r) < v) r++; return r; }
+
+int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, const DOp* ops, int nops,
+                      int task, void* stream, int grid_hint) {
+  SFArgs* a = new SFArgs();
+  a->T = t; a->C = c; a->task = task; a->nops = nops;
+  a->entries = drive ? drive->entries : nullptr;
+  a->count = drive ? drive->count : nullptr;
+  a->need_nbr = 0;
+  bool i32 = false;
+  for (int o = 0; o < nops; o++) {
+    a->ops[o] = ops[o];
+    int op = ops[o].op;
+    if (op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER) a->need_nbr = 1;
+    a->aux[o] = 0;
+  }
+  // dtype of the group (validated uniform by the host)
+  i32 = ops[0].dt == SG_I32;
+  for (int o = 0; o < nops; o++)
+    if (ops[o].scalar >= 0) a->aux[o] = (uint64_t)(c.scalars + ops[o].scalar);
+  const int lblk = t.lblk;
+  const int TILE_LOG = 10;  // 1024 cells
+  if (lblk > TILE_LOG) { a->lchunk = TILE_LOG; a->lept = 0; }
+  else {
+    a->lchunk = -1;
+    int lept = TILE_LOG - lblk;
+    if (lept > 8) lept = 8;  // at most SF_MAXE entries
+    a->lept = lept;
+  }
+  int grid = grid_hint > 0 ? grid_hint : num_sms() * 8;
+  grid = max(1, min(grid, num_sms() * 8));
+  if (i32) k_struct_for<int><<<grid, SF_TPB, 0, (cudaStream_t)stream>>>(*a);
+  else k_struct_for<float><<<grid, SF_TPB, 0, (cudaStream_t)stream>>>(*a);
+  delete a;
+  return check_launch();
+}
+
+int launch_range_for(const DevCtx& c, int64_t n, const DOp* ops, int nops, int task, void* stream) {
+  if (n <= 0) return 0;
+  RFArgs* a = new RFArgs();
+  a->C = c; a->n = n; a->nops = nops; a->task = task;
+  for (int o = 0; o < nops; o++) a->ops[o] = ops[o];
+  int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms() * 16);
+  k_range_for<<<grid, 128, 0, (cudaStream_t)stream>>>(*a);
+  delete a;
+  return check_launch();
+}
+
+int launch_serial(const DevCtx& c, const DOp* ops, int nops, int, void* stream) {
+  SerArgs* a = new SerArgs();
+  a->C = c; a->nops = nops;
+  for (int o = 0; o < nops; o++) {
+    a->ops[o] = ops[o];
+    a->aux[o] = (uint64_t)(c.scalars + (ops[o].scalar >= 0 ? ops[o].scalar : 0));
+  }
+  k_serial<<<1, 1, 0, (cudaStream_t)stream>>>(*a);
+  delete a;
+  return check_launch();
+}
+
+int launch_deactivate(const DevCtx& c, const DTree& t, int, int level, const DList* lists, int, void* stream) {
+  DeArgs a;
+  a.T = t; a.C = c; a.ls = level;
+  a.drive_entries = t.driving >= 0 ? lists[t.driving].entries : nullptr;
+  a.drive_count = t.driving >= 0 ? lists[t.driving].count : nullptr;
+  for (int l = 0; l < SG_MAXL; l++) {
+    bool listed = l < t.nlev && (t.lev[l].kind == SG_POINTER ||
+                                 (t.lev[l].kind == SG_BITMASKED && !(l == t.nlev - 1)));
+    a.lent[l] = listed ? lists[l].entries : nullptr;
+    a.lcnt[l] = listed ? lists[l].count : nullptr;
+  }
+  k_deactivate<<<num_sms() * 4, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+static void dense_shifts(const DTree& t, int sh[3]) {
+  const DLevel& L = t.lev[t.nlev - 1];
+  for (int a = 0; a < 3; a++) sh[a] = L.lres[a];
+}
+
+int launch_read_field(const DevCtx&, const DTree& t, int, int slot, uint32_t* dense, void* stream) {
+  FieldIO a;
+  a.T = t; a.slot = slot; a.dense = dense; a.src = nullptr;
+  dense_shifts(t, a.sh);
+  a.total = 1ll << (a.sh[0] + a.sh[1] + a.sh[2]);
+  k_read_field<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+int launch_load_field(const DevCtx&, const DTree& t, int, int slot, const uint32_t* dense, void* stream) {
+  FieldIO a;
+  a.T = t; a.slot = slot; a.dense = nullptr; a.src = dense;
+  dense_shifts(t, a.sh);
+  a.total = 1ll << (a.sh[0] + a.sh[1] + a.sh[2]);
+  k_load_field<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+int launch_mask_scan(const DevCtx&, const DTree& t, int, int level, uint8_t* flags, void* stream) {
+  MaskScan a;
+  a.T = t; a.level = level; a.flags = flags;
+  for (int d = 0; d < 3; d++) a.sh[d] = t.lev[level].lres[d];
+  a.total = 1ll << (a.sh[0] + a.sh[1] + a.sh[2]);
+  k_mask_scan<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+int launch_list_decode(const DTree& t, int level, const DList& l, int32_t* coords, void* stream) {
+  ListDecode a{t, level, l.entries, l.count, coords};
+  k_list_decode<<<num_sms() * 4, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
+}  // namespace sg

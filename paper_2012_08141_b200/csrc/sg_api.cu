@@ -1,0 +1,761 @@
+// sg_api.cu -- the C-ABI of libsg (include/sg.h): layout derivation, device
+// memory, the task queue and the flush dispatcher.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "planner.h"
+#include "sg_internal.h"
+
+using namespace sg;
+
+static thread_local std::string g_err;
+
+static sg_status fail(sg_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                               \
+  do {                                                                            \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess) return fail(SG_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct sg_grid {
+  sg_opts opts{};
+  cudaStream_t stream = nullptr;
+  bool plan_only = false;
+  HLayout L;
+  std::vector<DTree> dtrees;
+  std::vector<std::vector<DList>> lists;   // [tree][chain position]
+  std::vector<DArray> arrays;
+  std::vector<void*> allocs;
+  DevCtx ctx{};
+  DTree* d_trees = nullptr;
+  DField* d_fields = nullptr;
+  DArray* d_arrays = nullptr;
+  int d_arrays_cap = 0;
+  // flush window
+  std::vector<PTask> eager;
+  int ncalls = 0;
+  std::vector<std::pair<const int32_t*, int64_t>> coords_seen;
+  std::unordered_map<uint64_t, Plan> cache;
+  std::vector<PlanRecord> last_plan;
+  int64_t task_counter = 0;
+  int num_sms = 148;
+
+  void* dev_alloc(size_t bytes) {
+    if (bytes == 0) bytes = 4;
+    void* p = nullptr;
+    if (opts.alloc) p = opts.alloc(opts.alloc_ctx, bytes, (void*)stream);
+    else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+    if (p) allocs.push_back(p);
+    return p;
+  }
+  ~sg_grid() {
+    for (void* p : allocs) {
+      if (opts.free) opts.free(opts.alloc_ctx, p, (void*)stream);
+      else cudaFree(p);
+    }
+  }
+};
+
+static int ilog2i(int64_t v) {
+  int r = 0;
+  while ((1ll << r) < v) r++;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Layout validation and derivation
+// ---------------------------------------------------------------------------
+static sg_status build_layout(const sg_snode_desc* d, int n, HLayout& L) {
+  if (n < 1 || !d || d[0].kind != SG_ROOT || d[0].parent != -1) return fail(SG_ERR_LAYOUT, "row 0 must be the root");
+  L.nodes.assign(d, d + n);
+  std::vector<std::vector<int>> kids(n);
+  for (int i = 1; i < n; i++) {
+    const sg_snode_desc& s = d[i];
+    if (s.kind <= SG_ROOT || s.kind > SG_PLACE) return fail(SG_ERR_LAYOUT, "bad kind at row " + std::to_string(i));
+    if (s.parent < 0 || s.parent >= i) return fail(SG_ERR_LAYOUT, "parent must precede child");
+    if (d[s.parent].kind == SG_PLACE) return fail(SG_ERR_LAYOUT, "place with children");
+    if (s.ndim < 0 || s.ndim > 3) return fail(SG_ERR_LAYOUT, "ndim out of range");
+    for (int a = 0; a < 3; a++) {
+      int e = s.extent[a];
+      if (e < 1 || (e & (e - 1))) return fail(SG_ERR_LAYOUT, "extent not a power of two");
+      if (a >= s.ndim && e != 1) return fail(SG_ERR_LAYOUT, "extent on an unused axis");
+    }
+    if (s.kind == SG_PLACE && s.dtype != SG_F32 && s.dtype != SG_I32) return fail(SG_ERR_LAYOUT, "bad dtype");
+    kids[s.parent].push_back(i);
+  }
+  L.snode_tree.assign(n, -1);
+  L.snode_pos.assign(n, -1);
+  int nscal = 0;
+  std::vector<int> place_tree(n, -1);
+  for (int c : kids[0]) {
+    HTree T;
+    int tid = (int)L.trees.size();
+    if (d[c].kind == SG_PLACE) {
+      if (d[c].ndim != 0) return fail(SG_ERR_LAYOUT, "place under the root must be 0-D");
+      T.nd = 0;
+      T.fields.push_back(c);
+      place_tree[c] = tid;
+    } else {
+      T.nd = d[c].ndim;
+      if (T.nd < 1) return fail(SG_ERR_LAYOUT, "levels need ndim >= 1");
+      int cur = c;
+      while (true) {
+        if (d[cur].ndim != T.nd) return fail(SG_ERR_LAYOUT, "axis mismatch along a chain");
+        L.snode_tree[cur] = tid;
+        L.snode_pos[cur] = (int)T.levels.size();
+        T.levels.push_back(cur);
+        if ((int)T.levels.size() > SG_MAXL) return fail(SG_ERR_LAYOUT, "chain deeper than 6 levels");
+        int structural = -1, places = 0;
+        for (int k : kids[cur]) {
+          if (d[k].kind == SG_PLACE) places++;
+          else if (structural >= 0) return fail(SG_ERR_LAYOUT, "a level with two structural children");
+          else structural = k;
+        }
+        if (structural >= 0 && places) return fail(SG_ERR_LAYOUT, "places only at the leaf level");
+        if (structural < 0) {
+          if (!places) return fail(SG_ERR_LAYOUT, "leaf level without place");
+          if (d[cur].kind == SG_POINTER) return fail(SG_ERR_LAYOUT, "a pointer level cannot be the leaf");
+          for (int k : kids[cur]) {
+            if (d[k].ndim != T.nd) return fail(SG_ERR_LAYOUT, "place ndim mismatch");
+            T.fields.push_back(k);
+            place_tree[k] = tid;
+          }
+          break;
+        }
+        cur = structural;
+      }
+      for (int k = (int)T.levels.size() - 1; k >= 0; k--) {
+        int s = T.levels[k];
+        bool sparse = d[s].kind == SG_BITMASKED || d[s].kind == SG_POINTER;
+        if (!sparse) continue;
+        if (k == (int)T.levels.size() - 1 && d[s].kind == SG_BITMASKED) { T.leaf_bitmasked = true; continue; }
+        T.driving = k;
+        break;
+      }
+    }
+    L.trees.push_back(T);
+  }
+  // fields, in order of place rows
+  for (int i = 0; i < n; i++) {
+    if (d[i].kind != SG_PLACE) continue;
+    int tid = place_tree[i];
+    if (tid < 0) return fail(SG_ERR_LAYOUT, "place not reachable from the root");
+    int fid = (int)L.field_tree.size();
+    const HTree& T = L.trees[tid];
+    int slot = 0;
+    for (size_t k = 0; k < T.fields.size(); k++) if (T.fields[k] == i) slot = (int)k;
+    L.field_tree.push_back(T.nd == 0 ? -1 : tid);
+    L.field_slot.push_back(slot);
+    L.field_dtype.push_back(d[i].dtype);
+    L.field_scalar.push_back(T.nd == 0 ? nscal++ : -1);
+    (void)fid;
+  }
+  // trees hold field ids, not place rows
+  for (HTree& T : L.trees) {
+    for (int& f : T.fields) {
+      int fid = 0;
+      for (int i = 0; i < f; i++) if (d[i].kind == SG_PLACE) fid++;
+      f = fid;
+    }
+  }
+  L.n_scalars = nscal;
+  return SG_OK;
+}
+
+static sg_status derive_tree(sg_grid* g, int tid, DTree& T) {
+  const HLayout& L = g->L;
+  const HTree& H = L.trees[tid];
+  std::memset(&T, 0, sizeof(T));
+  T.nd = H.nd;
+  T.nlev = (int)H.levels.size();
+  T.driving = H.driving;
+  T.leaf_bitmasked = H.leaf_bitmasked;
+  T.nfields = (int)H.fields.size();
+  int seg = 0;
+  for (int k = 0; k < T.nlev; k++) {
+    const sg_snode_desc& s = L.nodes[H.levels[k]];
+    DLevel& D = T.lev[k];
+    D.kind = s.kind;
+    D.seg = seg;
+    D.lE = 0;
+    for (int a = 0; a < 3; a++) { D.le[a] = ilog2i(s.extent[a]); D.lE += D.le[a]; }
+    if (s.kind == SG_POINTER) seg++;
+  }
+  T.nseg = seg + 1;
+  for (int k = 0; k < T.nlev; k++) {
+    DLevel& D = T.lev[k];
+    for (int a = 0; a < 3; a++) {
+      D.lbelow[a] = 0;
+      for (int m = k + 1; m < T.nlev; m++) D.lbelow[a] += T.lev[m].le[a];
+      D.lres[a] = 0;
+      for (int m = 0; m <= k; m++) D.lres[a] += T.lev[m].le[a];
+    }
+  }
+  for (int s = 0; s < T.nseg; s++) { T.seg[s].first = -1; T.seg[s].last = -1; }
+  for (int k = 0; k < T.nlev; k++) {
+    DSeg& S = T.seg[T.lev[k].seg];
+    if (S.first < 0) S.first = k;
+    S.last = k;
+  }
+  T.lblk = 0;
+  for (int k = T.driving + 1; k < T.nlev; k++) T.lblk += T.lev[k].lE;
+  // container layouts
+  for (int s = 0; s < T.nseg; s++) {
+    DSeg& S = T.seg[s];
+    uint64_t words = 0;
+    int ln = 0;
+    for (int k = S.first; k <= S.last; k++) {
+      DLevel& D = T.lev[k];
+      ln += D.lE;
+      D.ln = ln;
+      if (D.kind == SG_BITMASKED) {
+        D.mask_off = (uint32_t)words;
+        words += std::max<uint64_t>(1, ((1ull << ln) + 31) / 32);
+      }
+      if (D.kind == SG_POINTER) {
+        D.slot_off = (uint32_t)words;
+        words += 1ull << ln;
+      }
+    }
+    S.header_words = (uint32_t)words;
+    if (s == T.nseg - 1) {
+      T.ln_leaf = ln;
+      T.payload_off = (int32_t)((words + 31) & ~31ull);
+      words = (uint64_t)T.payload_off + (uint64_t)T.nfields << 0;
+      words = (uint64_t)T.payload_off + ((uint64_t)T.nfields << ln);
+    }
+    S.stride = (words + 63) & ~63ull;
+    if (s == 0) {
+      S.capacity = 1;
+    } else {
+      const DLevel& P = T.lev[T.seg[s - 1].last];
+      int64_t cells = 1ll << (P.lres[0] + P.lres[1] + P.lres[2]);
+      int64_t cap = cells;
+      if (g->opts.pool_capacity > 0) cap = std::min<int64_t>(cap, g->opts.pool_capacity);
+      S.capacity = (uint32_t)cap;
+    }
+    for (int k = S.first; k <= S.last; k++) {
+      if (((uint64_t)S.capacity << T.lev[k].ln) > (1ull << 32))
+        return fail(SG_ERR_LAYOUT, "list entries would overflow u32: lower opts.pool_capacity");
+    }
+  }
+  return SG_OK;
+}
+
+static sg_status alloc_tree(sg_grid* g, int tid, DTree& T) {
+  for (int s = 0; s < T.nseg; s++) {
+    DSeg& S = T.seg[s];
+    size_t bytes = (size_t)S.capacity * S.stride * 4;
+    S.base = (uint32_t*)g->dev_alloc(bytes);
+    if (!S.base) return fail(SG_ERR_CUDA, "pool allocation failed (" + std::to_string(bytes) + " bytes)");
+    CUDA_TRY(cudaMemsetAsync(S.base, 0, bytes, g->stream));
+    S.origin = (int32_t*)g->dev_alloc((size_t)S.capacity * 3 * 4);
+    S.alloc = (int32_t*)g->dev_alloc(16);
+    S.free_list = (uint32_t*)g->dev_alloc((size_t)S.capacity * 4);
+    if (!S.origin || !S.alloc || !S.free_list) return fail(SG_ERR_CUDA, "allocation failed");
+    CUDA_TRY(cudaMemsetAsync(S.origin, 0, (size_t)S.capacity * 12, g->stream));
+    CUDA_TRY(cudaMemsetAsync(S.alloc, 0, 16, g->stream));
+  }
+  (void)tid;
+  return SG_OK;
+}
+
+static uint64_t list_capacity(const sg_grid* g, const DTree& T, int k) {
+  uint64_t cap = (uint64_t)T.seg[T.lev[k].seg].capacity << T.lev[k].ln;
+  if (g->opts.list_capacity > 0) cap = std::min<uint64_t>(cap, (uint64_t)g->opts.list_capacity);
+  return std::min<uint64_t>(cap, 0xFFFFFFFFull);
+}
+
+static int parent_pos(const DTree& T, int k) {
+  for (int m = k - 1; m >= 0; m--)
+    if (T.lev[m].kind == SG_BITMASKED || T.lev[m].kind == SG_POINTER) return m;
+  return -1;
+}
+
+static sg_status alloc_list(sg_grid* g, int tid, int k) {
+  DTree& T = g->dtrees[tid];
+  DList& Ls = g->lists[tid][k];
+  if (Ls.entries) return SG_OK;
+  uint64_t cap = list_capacity(g, T, k);
+  int pk = parent_pos(T, k);
+  uint64_t pcap = pk < 0 ? 1 : list_capacity(g, T, pk);
+  int lratio;
+  if (pk < 0) lratio = T.lev[k].ln;
+  else if (T.lev[pk].seg == T.lev[k].seg) lratio = T.lev[k].ln - T.lev[pk].ln;
+  else lratio = T.lev[k].ln;
+  uint64_t cpp = lratio > 5 ? (1ull << (lratio - 5)) : 1;
+  uint64_t max_tiles = (pcap * cpp + 1023) / 1024 + 1;
+  Ls.capacity = (uint32_t)cap;
+  Ls.max_tiles = (uint32_t)std::min<uint64_t>(max_tiles, 0xFFFFFFFFull);
+  Ls.entries = (uint32_t*)g->dev_alloc(cap * 4);
+  Ls.count = (uint32_t*)g->dev_alloc(16);
+  Ls.ctl = (uint32_t*)g->dev_alloc(16);
+  Ls.status = (uint64_t*)g->dev_alloc(max_tiles * 8);
+  if (!Ls.entries || !Ls.count || !Ls.ctl || !Ls.status) return fail(SG_ERR_CUDA, "list allocation failed");
+  CUDA_TRY(cudaMemsetAsync(Ls.count, 0, 16, g->stream));
+  CUDA_TRY(cudaMemsetAsync(Ls.ctl, 0, 16, g->stream));
+  CUDA_TRY(cudaMemsetAsync(Ls.status, 0, max_tiles * 8, g->stream));
+  return SG_OK;
+}
+
+static sg_status upload_tables(sg_grid* g) {
+  CUDA_TRY(cudaMemcpyAsync(g->d_trees, g->dtrees.data(), g->dtrees.size() * sizeof(DTree), cudaMemcpyHostToDevice, g->stream));
+  return SG_OK;
+}
+
+extern "C" sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_opts* o, sg_grid** out) {
+  if (!out) return fail(SG_ERR_ARG, "out is null");
+  *out = nullptr;
+  sg_grid* g = new sg_grid();
+  if (o) g->opts = *o;
+  g->plan_only = g->opts.plan_only != 0;
+  g->stream = (cudaStream_t)g->opts.stream;
+  sg_status rc = build_layout(nodes, n, g->L);
+  if (rc) { delete g; return rc; }
+  g->dtrees.resize(g->L.trees.size());
+  g->lists.assign(g->L.trees.size(), std::vector<DList>(SG_MAXL));
+  for (size_t t = 0; t < g->L.trees.size(); t++) {
+    if (g->L.trees[t].nd == 0) continue;
+    rc = derive_tree(g, (int)t, g->dtrees[t]);
+    if (rc) { delete g; return rc; }
+  }
+  if (!g->plan_only) {
+    cudaError_t e = cudaSetDevice(g->opts.device);
+    if (e != cudaSuccess) { delete g; return fail(SG_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
+    cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->opts.device);
+    for (size_t t = 0; t < g->L.trees.size(); t++) {
+      if (g->L.trees[t].nd == 0) continue;
+      rc = alloc_tree(g, (int)t, g->dtrees[t]);
+      if (rc) { delete g; return rc; }
+      for (int s : g->L.listed_levels((int)t)) {
+        rc = alloc_list(g, (int)t, g->L.snode_pos[s]);
+        if (rc) { delete g; return rc; }
+      }
+    }
+    size_t nf = g->L.field_tree.size();
+    std::vector<DField> hf(nf);
+    for (size_t f = 0; f < nf; f++) {
+      hf[f].tree = g->L.field_tree[f];
+      hf[f].slot = g->L.field_slot[f];
+      hf[f].dtype = g->L.field_dtype[f];
+      hf[f].scalar = g->L.field_scalar[f];
+    }
+    g->d_trees = (DTree*)g->dev_alloc(std::max<size_t>(1, g->dtrees.size()) * sizeof(DTree));
+    g->d_fields = (DField*)g->dev_alloc(std::max<size_t>(1, nf) * sizeof(DField));
+    g->ctx.scalars = (uint32_t*)g->dev_alloc(std::max(1, g->L.n_scalars) * 4);
+    g->ctx.err = (uint32_t*)g->dev_alloc(16);
+    g->d_arrays_cap = 64;
+    g->d_arrays = (DArray*)g->dev_alloc(g->d_arrays_cap * sizeof(DArray));
+    if (!g->d_trees || !g->d_fields || !g->ctx.scalars || !g->ctx.err || !g->d_arrays) {
+      delete g;
+      return fail(SG_ERR_CUDA, "table allocation failed");
+    }
+    if ((rc = upload_tables(g))) { delete g; return rc; }
+    if (cudaMemcpyAsync(g->d_fields, hf.data(), nf * sizeof(DField), cudaMemcpyHostToDevice, g->stream) != cudaSuccess ||
+        cudaMemsetAsync(g->ctx.scalars, 0, std::max(1, g->L.n_scalars) * 4, g->stream) != cudaSuccess ||
+        cudaMemsetAsync(g->ctx.err, 0, 16, g->stream) != cudaSuccess ||
+        cudaStreamSynchronize(g->stream) != cudaSuccess) {
+      delete g;
+      return fail(SG_ERR_CUDA, "table upload failed");
+    }
+    g->ctx.trees = g->d_trees;
+    g->ctx.fields = g->d_fields;
+    g->ctx.arrays = g->d_arrays;
+    g->ctx.debug = g->opts.debug;
+  }
+  *out = g;
+  return SG_OK;
+}
+
+extern "C" sg_status sg_destroy(sg_grid* g) {
+  if (!g) return SG_OK;
+  if (!g->plan_only) cudaStreamSynchronize(g->stream);
+  delete g;
+  return SG_OK;
+}
+
+extern "C" sg_status sg_register_array(sg_grid* g, void* ptr, int64_t n, int32_t dtype, int32_t ncomp, int32_t* id) {
+  if (!g || !id || n < 0 || ncomp < 1) return fail(SG_ERR_ARG, "bad array");
+  if ((int)g->arrays.size() >= g->d_arrays_cap && !g->plan_only) return fail(SG_ERR_ARG, "too many arrays");
+  DArray a{ptr, n, ncomp, dtype};
+  g->arrays.push_back(a);
+  *id = (int32_t)g->arrays.size() - 1;
+  if (!g->plan_only)
+    CUDA_TRY(cudaMemcpyAsync(g->d_arrays + *id, &a, sizeof(DArray), cudaMemcpyHostToDevice, g->stream));
+  return SG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Enqueue (tasks are queued until synchronization)
+// ---------------------------------------------------------------------------
+static sg_status enqueue(sg_grid* g, const UserCall& c) {
+  std::string err;
+  size_t before = g->eager.size();
+  int rc = lower_call(g->L, c, g->ncalls, g->opts.lowering == 1, g->eager, err);
+  if (rc) { g->eager.resize(before); return fail(rc, err); }
+  for (size_t i = before; i < g->eager.size(); i++) {
+    PTask& t = g->eager[i];
+    t.pos = (int)i;
+    if (t.type == TT_ACTIVATE) {
+      int cls = -1;
+      for (size_t k = 0; k < g->coords_seen.size(); k++)
+        if (g->coords_seen[k].first == t.coords && g->coords_seen[k].second == t.n) cls = (int)k;
+      if (cls < 0) { cls = (int)g->coords_seen.size(); g->coords_seen.push_back({t.coords, t.n}); }
+      t.coords_class = cls;
+    }
+    task_meta(g->L, t);
+  }
+  g->ncalls++;
+  return SG_OK;
+}
+
+extern "C" sg_status sg_activate(sg_grid* g, int32_t field, const int32_t* coords, int64_t n) {
+  if (!g || n < 0 || (n > 0 && !coords)) return fail(SG_ERR_ARG, "bad activate arguments");
+  UserCall c;
+  c.kind = 0; c.field = field; c.coords = coords; c.n = n;
+  return enqueue(g, c);
+}
+
+extern "C" sg_status sg_listgen(sg_grid* g, int32_t snode) {
+  if (!g) return fail(SG_ERR_ARG, "null grid");
+  UserCall c;
+  c.kind = 1; c.snode = snode;
+  return enqueue(g, c);
+}
+
+extern "C" sg_status sg_struct_for(sg_grid* g, const sg_task* t) {
+  if (!g || !t) return fail(SG_ERR_ARG, "null task");
+  UserCall c;
+  c.kind = 2; c.t = *t;
+  return enqueue(g, c);
+}
+
+extern "C" sg_status sg_clear(sg_grid* g, int32_t target, int32_t mode) {
+  if (!g) return fail(SG_ERR_ARG, "null grid");
+  UserCall c;
+  c.kind = 3; c.mode = mode;
+  if (mode == SG_CLEAR_VALUES) c.field = target; else c.snode = target;
+  return enqueue(g, c);
+}
+
+// ---------------------------------------------------------------------------
+// Flush: plan (cached) and launch one kernel per group
+// ---------------------------------------------------------------------------
+static void make_op(const sg_grid* g, const PTask& t, uint32_t act, int loop_tree, DOp& o) {
+  std::memset(&o, 0, sizeof(o));
+  o.op = t.t.op;
+  o.act = act;
+  o.scalar = -1;
+  o.dt = SG_F32;
+  bool dt_set = false;
+  for (int i = 0; i < 8; i++) {
+    int f = t.t.fields[i];
+    o.f[i] = f;
+    o.a[i] = t.t.arrays[i];
+    o.p[i] = t.t.params[i];
+    o.slot[i] = -1;
+    if (f >= 0 && f < (int)g->L.field_tree.size()) {
+      o.nf = i + 1;
+      if (!dt_set) { o.dt = g->L.field_dtype[f]; dt_set = true; }
+      if (g->L.field_tree[f] == loop_tree && loop_tree >= 0) o.slot[i] = g->L.field_slot[f];
+      if (g->L.field_tree[f] < 0 && o.scalar < 0) o.scalar = g->L.field_scalar[f];
+    }
+  }
+}
+
+static int grid_hint_struct(const sg_grid* g, const DTree& T) {
+  if (T.driving < 0) return g->num_sms * 8;
+  uint64_t cap = g->lists.empty() ? 1 : 1;
+  (void)cap;
+  return g->num_sms * 8;
+}
+
+static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const std::vector<uint32_t>& acts,
+                              sg_stats& st) {
+  const PTask& t0 = g->eager[members[0]];
+  int task = (int)(g->task_counter++ & 0x7FFFFFFF);
+  int rc = 0;
+  switch (t0.type) {
+    case TT_ACTIVATE: {
+      rc = launch_activate(g->ctx, g->dtrees[t0.tree], t0.tree, t0.field, t0.coords, t0.n, task, g->stream);
+    } break;
+    case TT_LISTGEN: {
+      const DTree& T = g->dtrees[t0.tree];
+      int k = g->L.snode_pos[t0.snode];
+      if ((rc = alloc_list(g, t0.tree, k))) return rc;
+      int pk = parent_pos(T, k);
+      const DList* parent = pk >= 0 ? &g->lists[t0.tree][pk] : nullptr;
+      uint64_t ptiles = parent ? ((uint64_t)parent->capacity * (1ull << std::max(0, (pk >= 0 && T.lev[pk].seg == T.lev[k].seg ? T.lev[k].ln - T.lev[pk].ln : T.lev[k].ln) - 5)) + 1023) / 1024 : 1;
+      int hint = (int)std::min<uint64_t>(ptiles, (uint64_t)g->num_sms * 4);
+      rc = launch_listgen(g->ctx, T, t0.tree, k, pk, parent, g->lists[t0.tree][k], task, g->stream, hint);
+      st.listgen_launched++;
+    } break;
+    case TT_CLEAR_LIST: {
+      int k = g->L.snode_pos[t0.snode];
+      if ((rc = alloc_list(g, t0.tree, k))) return rc;
+      rc = launch_clear_list(g->lists[t0.tree][k], g->stream);
+      st.clear_list_launched++;
+    } break;
+    case TT_STRUCT_FOR: {
+      const DTree& T = g->dtrees[t0.tree];
+      DOp ops[SG_MAXOPS];
+      int nops = (int)members.size();
+      for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], t0.tree, ops[i]);
+      const DList* drive = T.driving >= 0 ? &g->lists[t0.tree][T.driving] : nullptr;
+      rc = launch_struct_for(g->ctx, T, t0.tree, drive, ops, nops, task, g->stream, grid_hint_struct(g, T));
+    } break;
+    case TT_RANGE_FOR: {
+      DOp ops[SG_MAXOPS];
+      int nops = (int)members.size();
+      for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], -1, ops[i]);
+      rc = launch_range_for(g->ctx, t0.n, ops, nops, task, g->stream);
+    } break;
+    case TT_SERIAL: {
+      DOp ops[SG_MAXOPS];
+      int nops = (int)members.size();
+      for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], -1, ops[i]);
+      rc = launch_serial(g->ctx, ops, nops, task, g->stream);
+    } break;
+    case TT_DEACTIVATE: {
+      const DTree& T = g->dtrees[t0.tree];
+      rc = launch_deactivate(g->ctx, T, t0.tree, g->L.snode_pos[t0.snode], g->lists[t0.tree].data(), task, g->stream);
+    } break;
+    default: rc = SG_ERR_ARG;
+  }
+  if (rc) return fail(rc, std::string("launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  st.launches++;
+  return SG_OK;
+}
+
+extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observed, int32_t n_observed, sg_stats* out) {
+  if (!g) return fail(SG_ERR_ARG, "null grid");
+  sg_stats st;
+  std::memset(&st, 0, sizeof(st));
+  auto t0 = std::chrono::steady_clock::now();
+  size_t nf = g->L.field_tree.size();
+  std::vector<char> obs(nf, 1);
+  if (observed && n_observed >= 0) {
+    std::fill(obs.begin(), obs.end(), 0);
+    for (int i = 0; i < n_observed; i++)
+      if (observed[i] >= 0 && observed[i] < (int)nf) obs[observed[i]] = 1;
+  }
+  st.tasks_lowered = (int64_t)g->eager.size();
+  g->last_plan.clear();
+  if (g->eager.empty()) {
+    if (out) *out = st;
+    return SG_OK;
+  }
+  uint64_t key = stream_hash(g->eager, passes, obs);
+  auto it = g->cache.find(key);
+  const Plan* plan;
+  if (it != g->cache.end()) {
+    st.plan_cache_hits = 1;
+    plan = &it->second;
+  } else {
+    st.plan_cache_misses = 1;
+    Plan p = optimize(g->L, g->eager, passes, obs);
+    plan = &(g->cache[key] = std::move(p));
+  }
+  st.listgens_removed = plan->stats.listgens_removed;
+  st.demotions = plan->stats.demotions;
+  st.tasks_fused = plan->stats.fused;
+  st.dead_removed = plan->stats.dead;
+  auto t1 = std::chrono::steady_clock::now();
+  st.plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
+  sg_status rc = SG_OK;
+  for (size_t gi = 0; gi < plan->groups.size(); gi++) {
+    const auto& mem = plan->groups[gi];
+    const auto& acts = plan->acts[gi];
+    for (size_t m = 0; m < mem.size(); m++) {
+      const PTask& t = g->eager[mem[m]];
+      g->last_plan.push_back({(int)gi, t.type, t.call, t.snode, acts[m], 0});
+    }
+    if (g->plan_only) {
+      const PTask& t = g->eager[mem[0]];
+      st.launches++;
+      if (t.type == TT_LISTGEN) st.listgen_launched++;
+      if (t.type == TT_CLEAR_LIST) st.clear_list_launched++;
+      continue;
+    }
+    if (!rc) rc = launch_group(g, mem, acts, st);
+  }
+  g->eager.clear();
+  g->coords_seen.clear();
+  g->ncalls = 0;
+  if (out) *out = st;
+  return rc;
+}
+
+extern "C" sg_status sg_sync(sg_grid* g) {
+  if (!g) return fail(SG_ERR_ARG, "null grid");
+  if (g->plan_only) return SG_OK;
+  CUDA_TRY(cudaStreamSynchronize(g->stream));
+  uint32_t e[2] = {0, 0};
+  CUDA_TRY(cudaMemcpy(e, g->ctx.err, 8, cudaMemcpyDeviceToHost));
+  if (e[0]) {
+    int code = (int)(int32_t)e[0];
+    const char* what = code == SG_ERR_POOL_EXHAUSTED ? "pool exhausted"
+                       : code == SG_ERR_LIST_OVERFLOW ? "list overflow"
+                       : code == SG_ERR_DEMOTION_TRAP ? "non-activating write to an inactive cell"
+                       : code == SG_ERR_RANGE ? "coordinate out of range" : "device error";
+    return fail(code, std::string("device: ") + what + " (task " + std::to_string(e[1]) + ")");
+  }
+  return SG_OK;
+}
+
+static sg_status flush_sync(sg_grid* g) {
+  if (g->plan_only) return fail(SG_ERR_STATE, "plan-only grid has no device state");
+  sg_status rc = sg_flush(g, SG_PASS_ALL, nullptr, -1, nullptr);
+  if (rc) return rc;
+  return sg_sync(g);
+}
+
+extern "C" sg_status sg_export_mask(sg_grid* g, int32_t snode, int32_t* host, int64_t cap, int64_t* count) {
+  if (!g || !count) return fail(SG_ERR_ARG, "null argument");
+  if (snode <= 0 || snode >= (int)g->L.nodes.size() || !g->L.is_sparse(snode)) return fail(SG_ERR_ARG, "bad snode");
+  sg_status rc = flush_sync(g);
+  if (rc) return rc;
+  int tid = g->L.snode_tree[snode], k = g->L.snode_pos[snode];
+  const DTree& T = g->dtrees[tid];
+  const DLevel& D = T.lev[k];
+  int lt = D.lres[0] + D.lres[1] + D.lres[2];
+  if (lt > 30) return fail(SG_ERR_ARG, "level too large to export");
+  int64_t total = 1ll << lt;
+  uint8_t* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, total));
+  int lrc = launch_mask_scan(g->ctx, T, tid, k, d, g->stream);
+  std::vector<uint8_t> h(total);
+  cudaError_t e = cudaMemcpyAsync(h.data(), d, total, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(d);
+  if (lrc || e != cudaSuccess) return fail(SG_ERR_CUDA, "mask scan failed");
+  int64_t n = 0;
+  for (int64_t i = 0; i < total; i++) {
+    if (!h[i]) continue;
+    if (n < cap && host) {
+      int64_t c[3] = {i >> (D.lres[1] + D.lres[2]), (i >> D.lres[2]) & ((1ll << D.lres[1]) - 1), i & ((1ll << D.lres[2]) - 1)};
+      for (int a = 0; a < T.nd; a++) host[n * T.nd + a] = (int32_t)c[a];
+    }
+    n++;
+  }
+  *count = n;
+  return SG_OK;
+}
+
+extern "C" sg_status sg_export_list(sg_grid* g, int32_t snode, int32_t* host, int64_t cap, int64_t* count) {
+  if (!g || !count) return fail(SG_ERR_ARG, "null argument");
+  if (snode <= 0 || snode >= (int)g->L.nodes.size() || !g->L.is_sparse(snode)) return fail(SG_ERR_ARG, "bad snode");
+  sg_status rc = flush_sync(g);
+  if (rc) return rc;
+  int tid = g->L.snode_tree[snode], k = g->L.snode_pos[snode];
+  const DList& Ls = g->lists[tid][k];
+  if (!Ls.entries) { *count = 0; return SG_OK; }
+  uint32_t n = 0;
+  CUDA_TRY(cudaMemcpy(&n, Ls.count, 4, cudaMemcpyDeviceToHost));
+  *count = n;
+  if (!host || cap <= 0 || n == 0) return SG_OK;
+  const DTree& T = g->dtrees[tid];
+  int32_t* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, (size_t)n * T.nd * 4));
+  int lrc = launch_list_decode(T, k, Ls, d, g->stream);
+  std::vector<int32_t> h((size_t)n * T.nd);
+  cudaError_t e = cudaMemcpyAsync(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(d);
+  if (lrc || e != cudaSuccess) return fail(SG_ERR_CUDA, "list decode failed");
+  int64_t m = std::min<int64_t>(cap, n);
+  std::memcpy(host, h.data(), (size_t)m * T.nd * 4);
+  return SG_OK;
+}
+
+static int64_t field_cells(const sg_grid* g, int f, const DTree** T) {
+  int tid = g->L.field_tree[f];
+  if (tid < 0) { *T = nullptr; return 1; }
+  *T = &g->dtrees[tid];
+  const DLevel& L = (*T)->lev[(*T)->nlev - 1];
+  return 1ll << (L.lres[0] + L.lres[1] + L.lres[2]);
+}
+
+extern "C" sg_status sg_read_field(sg_grid* g, int32_t f, void* host, int64_t bytes) {
+  if (!g || !host || f < 0 || f >= (int)g->L.field_tree.size()) return fail(SG_ERR_ARG, "bad field");
+  sg_status rc = flush_sync(g);
+  if (rc) return rc;
+  const DTree* T;
+  int64_t n = field_cells(g, f, &T);
+  if (bytes != n * 4) return fail(SG_ERR_ARG, "size mismatch: expected " + std::to_string(n * 4) + " bytes");
+  if (!T) {
+    CUDA_TRY(cudaMemcpy(host, g->ctx.scalars + g->L.field_scalar[f], 4, cudaMemcpyDeviceToHost));
+    return SG_OK;
+  }
+  uint32_t* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, n * 4));
+  int lrc = launch_read_field(g->ctx, *T, g->L.field_tree[f], g->L.field_slot[f], d, g->stream);
+  cudaError_t e = cudaMemcpyAsync(host, d, n * 4, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(d);
+  if (lrc || e != cudaSuccess) return fail(SG_ERR_CUDA, "read_field failed");
+  return SG_OK;
+}
+
+extern "C" sg_status sg_load_field(sg_grid* g, int32_t f, const void* host, int64_t bytes) {
+  if (!g || !host || f < 0 || f >= (int)g->L.field_tree.size()) return fail(SG_ERR_ARG, "bad field");
+  sg_status rc = flush_sync(g);
+  if (rc) return rc;
+  const DTree* T;
+  int64_t n = field_cells(g, f, &T);
+  if (bytes != n * 4) return fail(SG_ERR_ARG, "size mismatch");
+  if (!T) {
+    CUDA_TRY(cudaMemcpy(g->ctx.scalars + g->L.field_scalar[f], host, 4, cudaMemcpyHostToDevice));
+    return SG_OK;
+  }
+  uint32_t* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, n * 4));
+  cudaError_t e = cudaMemcpyAsync(d, host, n * 4, cudaMemcpyHostToDevice, g->stream);
+  int lrc = e == cudaSuccess ? launch_load_field(g->ctx, *T, g->L.field_tree[f], g->L.field_slot[f], d, g->stream) : 1;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(d);
+  if (lrc || e != cudaSuccess) return fail(SG_ERR_CUDA, "load_field failed");
+  return SG_OK;
+}
+
+extern "C" sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count) {
+  if (!g || !count) return fail(SG_ERR_ARG, "null argument");
+  *count = (int64_t)g->last_plan.size();
+  for (int64_t i = 0; i < std::min<int64_t>(cap, *count) && out; i++) {
+    const PlanRecord& r = g->last_plan[i];
+    out[i * 6 + 0] = r.group; out[i * 6 + 1] = r.type; out[i * 6 + 2] = r.call;
+    out[i * 6 + 3] = r.snode; out[i * 6 + 4] = (int32_t)r.act; out[i * 6 + 5] = r.flags;
+  }
+  return SG_OK;
+}
+
+// [0] num trees, then per tree i: [1+4i] pool base of the leaf segment, [2+4i] leaf stride words,
+// [3+4i] leaf capacity, [4+4i] payload offset words.
+extern "C" sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n) {
+  if (!g || !out) return fail(SG_ERR_ARG, "null argument");
+  int nt = (int)g->dtrees.size();
+  if (n > 0) out[0] = nt;
+  for (int i = 0; i < nt; i++) {
+    const DTree& T = g->dtrees[i];
+    int64_t v[4] = {0, 0, 0, 0};
+    if (T.nlev > 0) {
+      const DSeg& S = T.seg[T.nseg - 1];
+      v[0] = (int64_t)(uintptr_t)S.base; v[1] = (int64_t)S.stride; v[2] = S.capacity; v[3] = T.payload_off;
+    }
+    for (int k = 0; k < 4; k++) if (1 + 4 * i + k < n) out[1 + 4 * i + k] = v[k];
+  }
+  return SG_OK;
+}
+
+extern "C" const char* sg_last_error(void) { return g_err.c_str(); }

@@ -1,0 +1,307 @@
+"""Host planner tests (-m "not gpu"): plan-only grids, no device.
+
+T2 pins: the paper's printed task counts and facts (PAPER.md:316-323 6->3,
+:487-505 microbenchmarks, :346/:361 demotion), adapted to our lowering
+(SURVEY.md Appendix A).  T3 soundness on the CPU: the planner's schedule
+(what survives, in which order, with which activating flags) is replayed on
+the CPU oracle and must leave exactly the state of the eager oracle run, for
+every pass subset, on the integer fuzz corpus.  (The GPU executes the same
+schedule with fused kernels; tests/test_gpu_parity.py checks that.)
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from paper_2012_08141_b200 import sg
+
+
+def plan_counts(prog, passes="all", faithful=False):
+    g = sg.Grid(prog["desc"], plan_only=True, faithful=faithful)
+    stats, plans = [], []
+    sg.replay(g, prog, passes=passes, on_flush=lambda gr, st: (stats.append(st), plans.append(gr.last_plan())))
+    return stats, plans
+
+
+def types_of(plan):
+    return [sg.TASK_TYPES[t] for t in plan[:, 1]]
+
+
+# ---------------------------------------------------------------------------
+# Paper-printed counts
+# ---------------------------------------------------------------------------
+def fig6_program(n_kernels=2):
+    L = W.Layout()
+    lv = L.chain([("pointer", (4,)), ("dense", (2,))], [("x", "i32")])
+    calls = [W.activate(0, np.array([[1], [5]], dtype=np.int32)), W.flush()]
+    calls += [W.struct_for("INC", lv[-1], [0], [1.0]) for _ in range(n_kernels)] + [W.flush()]
+    return W.program(L, calls)
+
+
+def test_fig6_three_tasks_per_kernel_and_6_to_3():
+    # PAPER.md:316 "there are 3 tasks per such a small kernel"
+    # "we reduce the number of generated tasks from 6 to 3".
+    st, plans = plan_counts(fig6_program(1), passes=0, faithful=True)
+    assert st[1]["tasks_lowered"] == 3
+    st, plans = plan_counts(fig6_program(2), passes=0, faithful=True)
+    assert st[1]["tasks_lowered"] == 6 and st[1]["launches"] == 6
+    # Without DSE our clear-list version sits between the two listgens, so
+    # nothing is removable (reading R3: the paper's 3 keeps a clear-list task)
+    st, plans = plan_counts(fig6_program(2), passes="listgen+fusion+demotion", faithful=True)
+    assert st[1]["launches"] == 6
+    # With DSE our clear-list is dead (listgen completely overwrites List, reading R3): 6 -> 2
+    st, plans = plan_counts(fig6_program(2), passes="all", faithful=True)
+    assert st[1]["launches"] == 2
+    assert types_of(plans[1]) == ["listgen", "struct_for", "struct_for"]
+    assert len(set(plans[1][:, 0])) == 2                      # two INCs in one group
+    # folded lowering: 4 -> 2
+    st, _ = plan_counts(fig6_program(2), passes="all")
+    assert (st[1]["tasks_lowered"], st[1]["launches"]) == (4, 2)
+
+
+def dense1d(n=1024, fields=("x",), dtype="i32"):
+    L = W.Layout()
+    lv = L.chain([("dense", (n,))], [(f, dtype) for f in fields])
+    return L, lv
+
+
+def test_fill_array_10_to_1():
+    # PAPER.md:491 "only 1 task is launched in these cases instead of 10"
+    L, lv = dense1d()
+    calls = [W.struct_for("FILL", lv[-1], [0], [7.0]) for _ in range(10)] + [W.flush()]
+    st, plans = plan_counts(W.program(L, calls))
+    assert st[0]["tasks_lowered"] == 10 and st[0]["launches"] == 1
+    st, _ = plan_counts(W.program(L, calls), passes=0)
+    assert st[0]["launches"] == 10
+
+
+def test_chain_copy_fuses():
+    # PAPER.md:487 "y[i] = x[i] + 1 and z[i] = y[i] + 4 ... They are fused"
+    L, lv = dense1d(fields=("x", "y", "z"))
+    calls = [W.struct_for("ADD_CONST", lv[-1], [1, 0], [1.0]), W.struct_for("ADD_CONST", lv[-1], [2, 1], [4.0]),
+             W.flush()]
+    st, plans = plan_counts(W.program(L, calls))
+    assert st[0]["launches"] == 1 and st[0]["tasks_fused"] == 1
+
+
+def test_increments_fuse_to_one():
+    # PAPER.md:489 increments: 10 inc() kernels -> one fused task; on a 2-level sparse field
+    L = W.Layout()
+    lv = L.chain([("pointer", (8,)), ("dense", (4,))], [("x", "i32")])
+    calls = [W.activate(0, np.array([[0], [9]], dtype=np.int32)), W.flush()]
+    calls += [W.struct_for("INC", lv[-1], [0], [1.0]) for _ in range(10)] + [W.flush()]
+    st, plans = plan_counts(W.program(L, calls))
+    assert st[1]["tasks_lowered"] == 20
+    assert types_of(plans[1]) == ["listgen"] + ["struct_for"] * 10
+    assert st[1]["launches"] == 2 and st[1]["listgens_removed"] == 9
+
+
+def autodiff_program(iters=10, observed=None):
+    L = W.Layout()
+    lv = L.chain([("dense", (256,))], [("x", "f32"), ("grad", "f32")])
+    L.scalar("loss", "f32")
+    f = L.fields
+    calls = []
+    for _ in range(iters):
+        calls += [W.serial("CLEAR_SCALAR", [f["loss"]]),
+                  W.struct_for("REDUCE_SUM", lv[-1], [f["loss"], f["x"]]),
+                  W.struct_for("INC", lv[-1], [f["grad"]], [1.0])]
+    calls.append(W.flush(observed=observed))
+    return W.program(L, calls)
+
+
+def test_autodiff_dse_keeps_last_forward():
+    # "the forward tasks computing the loss function should be
+    # eliminated except for the last one, so the number of launched tasks reduces by roughly a half"
+    st, plans = plan_counts(autodiff_program())
+    eager = st[0]["tasks_lowered"]
+    assert eager == 30
+    assert st[0]["launches"] <= 0.6 * eager
+    p = plans[0]
+    reduces = [r for r in p if r[1] == 3 and r[2] % 3 == 1]
+    assert len(reduces) == 1 and reduces[0][2] == 28           # the last forward reduction survives
+    # no DSE: nothing removed
+    st2, _ = plan_counts(autodiff_program(), passes="listgen+demotion+fusion")
+    assert st2[0]["dead_removed"] == 0
+
+
+def multires_program(n=8, demote=True):
+    L = W.Layout()
+    xl = L.chain([("pointer", (4, 4)), ("dense", (4, 4))], [("x", "f32")])
+    yl = L.chain([("pointer", (4, 4)), ("dense", (2, 2))], [("y", "f32")])
+    f = L.fields
+    rng = np.random.default_rng(1)
+    cells = np.stack([rng.integers(0, 16, 12), rng.integers(0, 16, 12)], 1).astype(np.int32)
+    calls = [W.activate(f["x"], cells), W.struct_for("FILL", xl[-1], [f["x"]], [1.0]), W.flush()]
+    for _ in range(n):
+        calls += [W.struct_for("DOWNSAMPLE", xl[-1], [f["y"], f["x"]], [0.25, 0.0], [True]),
+                  W.struct_for("INC", yl[-1], [f["y"]], [1.0])]
+    calls.append(W.flush())
+    return W.program(L, calls), yl
+
+
+def test_downsample_demotion():
+    # PAPER.md:346-361 / Fig. 9 caption: with x unchanged, repeated
+    # y[i//2] += x[i]*0.25 keeps y's mask, so y's list generation is not repeated.
+    prog, yl = multires_program(8)
+    st, plans = plan_counts(prog, passes="listgen+demotion")
+    p = plans[1]
+    y_listgens = [r for r in p if r[1] == 1 and r[3] == yl[0]]
+    one, plans1 = plan_counts(multires_program(1)[0], passes="listgen+demotion")
+    y_listgens_1 = [r for r in plans1[1] if r[1] == 1 and r[3] == yl[0]]
+    assert len(y_listgens) == len(y_listgens_1) == 1
+    ds = [r for r in p if r[1] == 3 and r[2] % 2 == 0]
+    assert len(ds) == 8 and ds[0][4] == 1 and all(r[4] == 0 for r in ds[1:])   # runs 2..8 non-activating
+    # without demotion every run re-generates y's list
+    st0, plans0 = plan_counts(prog, passes="listgen")
+    assert len([r for r in plans0[1] if r[1] == 1 and r[3] == yl[0]]) == 8
+
+
+def test_deep_hierarchy_no_fusion_fewer_listgens():
+    # PAPER.md:505 "The tasks are not fusible but we can still get some
+    # performance boost by eliminating list generation tasks."
+    L = W.Layout()
+    lv = L.chain([("pointer", (4,)), ("pointer", (4,)), ("bitmasked", (4,)), ("dense", (4,))], [("x", "i32")])
+    calls = [W.activate(0, np.array([[3], [70], [200]], dtype=np.int32)), W.flush()]
+    calls += [W.struct_for("JITTER", lv[-1], [0]) for _ in range(5)] + [W.flush()]
+    st, _ = plan_counts(W.program(L, calls))
+    st0, _ = plan_counts(W.program(L, calls), passes=0)
+    assert st[1]["tasks_fused"] == 0
+    assert st[1]["listgen_launched"] < st0[1]["listgen_launched"]
+    assert (st0[1]["listgen_launched"], st[1]["listgen_launched"]) == (15, 3)
+
+
+def test_c1_c2_launch_counts():
+    # SURVEY.md Appendix A (readings R3, R5, R19): C1 8 -> 5 per step, faithful 11
+    st, _ = plan_counts(W.c1_program(steps=3))
+    assert all((s["tasks_lowered"], s["launches"]) == (8, 5) for s in st)
+    assert st[1]["plan_cache_hits"] == 1
+    st, _ = plan_counts(W.c1_program(steps=1), faithful=True)
+    assert (st[0]["tasks_lowered"], st[0]["launches"]) == (11, 5)
+    # C2: 50-iteration solve + final reduction: 161 eager -> 55
+    st, plans = plan_counts(W.c2_program())
+    assert (st[0]["tasks_lowered"], st[0]["launches"]) == (161, 55)
+    st0, _ = plan_counts(W.c2_program(), passes=0)
+    assert st0[0]["launches"] == 161
+
+
+def test_plan_is_topological_and_deterministic():
+    p1 = plan_counts(W.c2_program())[1][0]
+    p2 = plan_counts(W.c2_program())[1][0]
+    assert np.array_equal(p1, p2)
+
+
+# ---------------------------------------------------------------------------
+# T3 on the CPU: replay the planner's schedule on the oracle
+# ---------------------------------------------------------------------------
+def replay_plan_on_oracle(prog, passes):
+    """Eager oracle vs oracle executing the planner's schedule window by window."""
+    g = sg.Grid(prog["desc"], plan_only=True)
+    o = oracle.Oracle(prog["desc"])
+    window = []
+    for c in prog["calls"]:
+        if c["call"] != "flush":
+            k = c["call"]
+            if k == "activate":
+                g.activate(c["field"], c["coords"])
+            elif k == "struct_for":
+                g.struct_for(c["op"], c["snode"], c["fields"], c.get("params", []), c.get("activating", []))
+            elif k == "serial":
+                g.serial(c["op"], c["fields"], c.get("params", []))
+            elif k == "clear":
+                g.clear(c["target"], sg.CLEAR_VALUES if c["mode"] == "values" else sg.DEACTIVATE)
+            elif k == "listgen":
+                g.listgen(c["snode"])
+            window.append(c)
+            continue
+        g.flush(passes)
+        for grp, ttype, call, snode, act, _ in g.last_plan():
+            c = window[call]
+            t = sg.TASK_TYPES[ttype]
+            if t == "activate":
+                o.activate(c["field"], c["coords"])
+            elif t == "listgen":
+                o.listgen(int(snode))
+            elif t == "clear_list":
+                o.clear_list(int(snode))
+            elif t == "deactivate":
+                o.deactivate_task(int(snode))
+            elif t == "serial":
+                f = c["fields"][0] if c["call"] == "serial" else c["target"]
+                o.serial_task("CLEAR_SCALAR", [f])
+            elif t == "struct_for":
+                if c["call"] == "clear":
+                    o.struct_for_task("FILL", int(snode), [c["target"]], [0.0], 0)
+                else:
+                    o.struct_for_task(c["op"], int(snode), c["fields"], c.get("params", []), int(act))
+        window = []
+    return o
+
+
+PASS_SUBSETS = [0, 1, 2, 4, 8, 1 | 2, 1 | 4, 15]
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_schedule_soundness_on_oracle(seed):
+    prog = W.fuzz_program(seed)
+    ref = oracle.run_program(prog)
+    L = prog["layout"]
+    for passes in PASS_SUBSETS:
+        try:
+            o = replay_plan_on_oracle(prog, passes)
+        except oracle.OracleError as e:
+            raise AssertionError(f"seed {seed} passes {passes}: {e}")
+        for name, fid in L.fields.items():
+            assert np.array_equal(o.field(fid), ref.field(fid)), (seed, passes, name)
+        for s in range(1, len(L.rows)):
+            if L.rows[s][0] in (W.BITMASKED, W.POINTER):
+                assert np.array_equal(o.mask(s), ref.mask(s)), (seed, passes, s)
+
+
+def test_all_passes_never_more_launches_than_any_subset():
+    # SPEC.md:457 acceptance 10
+    for seed in range(40):
+        prog = W.fuzz_program(seed)
+        counts = {}
+        for passes in PASS_SUBSETS:
+            st, _ = plan_counts(prog, passes=passes)
+            counts[passes] = sum(s["launches"] for s in st)
+        assert counts[15] <= min(counts.values()), (seed, counts)
+        assert all(counts[p] <= counts[0] for p in counts)
+
+
+def test_layout_errors_match_spec():
+    bad = [
+        [[0, -1, 0, 1, 1, 1, 0], [3, 0, 1, 3, 1, 1, 0], [4, 1, 1, 1, 1, 1, 0]],
+        [[0, -1, 0, 1, 1, 1, 0], [1, 0, 1, 4, 1, 1, 0], [4, 1, 1, 1, 1, 1, 0], [1, 2, 1, 2, 1, 1, 0]],
+        [[0, -1, 0, 1, 1, 1, 0], [1, 0, 2, 4, 4, 1, 0], [1, 1, 1, 2, 1, 1, 0], [4, 2, 1, 1, 1, 1, 0]],
+        [[0, -1, 0, 1, 1, 1, 0], [3, 0, 1, 4, 1, 1, 0], [4, 1, 1, 1, 1, 1, 0]],   # pointer leaf
+    ]
+    for d in bad:
+        with pytest.raises(sg.SgError) as e:
+            sg.Grid(np.array(d, dtype=np.int32), plan_only=True)
+        assert e.value.kind == "LAYOUT"
+
+
+def test_bad_task_rejected():
+    L, lv = W.c1_layout()
+    g = sg.Grid(L.desc(), plan_only=True)
+    with pytest.raises(sg.SgError):
+        g.struct_for("STENCIL", lv[-1], [0, 0])          # in-place stencil would race
+    with pytest.raises(sg.SgError):
+        g.struct_for("FILL", lv[0], [0], [1.0])          # not the leaf level
+    with pytest.raises(sg.SgError):
+        g.struct_for("NOPE" if False else 99, lv[-1], [0])
+
+
+def test_library_exports_every_declared_symbol():
+    import re
+    import ctypes
+    hdr = open(sg.LIB_PATH.replace("paper_2012_08141_b200/libsg.so", "include/sg.h")).read()
+    declared = set(re.findall(r"\b(sg_[a-z_]+)\s*\(", hdr)) - {"sg_alloc_fn", "sg_free_fn"}
+    lib = ctypes.CDLL(sg.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(sg.EXPORTS)

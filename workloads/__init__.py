@@ -270,7 +270,13 @@ def fuzz_program(seed, n_ops=None, passes="all"):
     n_ops = int(rng.integers(3, 9)) if n_ops is None else n_ops
     fl = ["a", "b", "c"]
     for _ in range(n_ops):
-        r = int(rng.integers(0, 14))
+        r = int(rng.integers(0, 16))
+        if r >= 14:  # repeat the previous struct-for (demotion / listgen-removal / fusion bait)
+            prev = [c for c in calls if c["call"] == "struct_for"]
+            if prev:
+                calls.append(dict(prev[-1]))
+                continue
+            r = 1
         x, y, z = (fl[i] for i in rng.permutation(3))
         act = [bool(rng.integers(0, 2))]
         k = float(rng.integers(-3, 4))
