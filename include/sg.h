@@ -199,6 +199,15 @@ sg_status sg_load_field(sg_grid* g, int32_t field, const void* host_dense, int64
  * 6 deactivate.  call_index = index of the enqueue call within the flush window. */
 sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count);
 
+/* Launch profiling for benchmarks: when on, sg_flush records a CUDA event pair
+ * on the grid's stream around every launch group.  sg_profile_read waits for
+ * the stream and returns, per launch kind, the summed device time (ms) and the
+ * number of launches since the last read (kinds: 0 activate, 1 listgen,
+ * 2 clear_list, 3 struct_for, 4 range_for, 5 serial, 6 deactivate; struct-for
+ * launches are also accumulated under 100 + op of their first member). */
+sg_status sg_set_profiling(sg_grid* g, int32_t on);
+sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int32_t n_kinds);
+
 /* Device pointer of the payload pool / counters, for benchmarks (read-only). */
 sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
 

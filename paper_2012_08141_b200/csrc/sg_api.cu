@@ -50,6 +50,16 @@ struct sg_grid {
   std::vector<PlanRecord> last_plan;
   int64_t task_counter = 0;
   int num_sms = 148;
+  // launch profiling (benchmarks): event pairs per launch group
+  bool profiling = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) { cudaEvent_t e = event_pool.back(); event_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
 
   void* dev_alloc(size_t bytes) {
     if (bytes == 0) bytes = 4;
@@ -60,6 +70,8 @@ struct sg_grid {
     return p;
   }
   ~sg_grid() {
+    for (auto& p : prof_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
+    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     for (void* p : allocs) {
       if (opts.free) opts.free(opts.alloc_ctx, p, (void*)stream);
       else cudaFree(p);
@@ -588,7 +600,18 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
       if (t.type == TT_CLEAR_LIST) st.clear_list_launched++;
       continue;
     }
-    if (!rc) rc = launch_group(g, mem, acts, st);
+    if (!rc) {
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (g->profiling) { e0 = g->get_event(); cudaEventRecord(e0, g->stream); }
+      rc = launch_group(g, mem, acts, st);
+      if (g->profiling) {
+        e1 = g->get_event();
+        cudaEventRecord(e1, g->stream);
+        const PTask& t = g->eager[mem[0]];
+        int key = t.type == TT_STRUCT_FOR ? 100 + t.t.op : t.type;
+        g->prof_pending.push_back({key, {e0, e1}});
+      }
+    }
   }
   g->eager.clear();
   g->coords_seen.clear();
@@ -755,6 +778,32 @@ extern "C" sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n) {
     }
     for (int k = 0; k < 4; k++) if (1 + 4 * i + k < n) out[1 + 4 * i + k] = v[k];
   }
+  return SG_OK;
+}
+
+extern "C" sg_status sg_set_profiling(sg_grid* g, int32_t on) {
+  if (!g) return fail(SG_ERR_ARG, "null grid");
+  if (g->plan_only) return fail(SG_ERR_STATE, "plan-only grid");
+  g->profiling = on != 0;
+  return SG_OK;
+}
+
+extern "C" sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int32_t n_kinds) {
+  if (!g || !ms || !count) return fail(SG_ERR_ARG, "null argument");
+  CUDA_TRY(cudaStreamSynchronize(g->stream));
+  for (int i = 0; i < n_kinds; i++) { ms[i] = 0; count[i] = 0; }
+  for (auto& p : g->prof_pending) {
+    float t = 0;
+    cudaEventElapsedTime(&t, p.second.first, p.second.second);
+    int key = p.first;
+    int kinds[2] = {key >= 100 ? TT_STRUCT_FOR : key, key >= 100 ? key : -1};
+    for (int k : kinds) {
+      if (k >= 0 && k < n_kinds) { ms[k] += t; count[k]++; }
+    }
+    g->event_pool.push_back(p.second.first);
+    g->event_pool.push_back(p.second.second);
+  }
+  g->prof_pending.clear();
   return SG_OK;
 }
 

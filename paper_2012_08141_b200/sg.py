@@ -349,3 +349,24 @@ def run_program(prog, passes=None, device=0, plan_only=False, **kw):
     if not plan_only:
         g.sync()
     return g, st
+
+
+_lib.sg_set_profiling.argtypes = [_vp, ctypes.c_int32]
+_lib.sg_set_profiling.restype = ctypes.c_int32
+_lib.sg_profile_read.argtypes = [_vp, _P(ctypes.c_double), _P(ctypes.c_int64), ctypes.c_int32]
+_lib.sg_profile_read.restype = ctypes.c_int32
+EXPORTS += ["sg_set_profiling", "sg_profile_read"]
+
+PROFILE_KINDS = 128
+
+
+def set_profiling(grid, on=True):
+    _check(_lib.sg_set_profiling(grid.h, int(on)))
+
+
+def profile_read(grid):
+    """{kind: (total_ms, launches)}; kinds 0..6 task types, 100+op struct-for ops."""
+    ms = (ctypes.c_double * PROFILE_KINDS)()
+    cnt = (ctypes.c_int64 * PROFILE_KINDS)()
+    _check(_lib.sg_profile_read(grid.h, ms, cnt, PROFILE_KINDS))
+    return {k: (ms[k], cnt[k]) for k in range(PROFILE_KINDS) if cnt[k]}
