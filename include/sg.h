@@ -204,7 +204,8 @@ sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count);
  * the stream and returns, per launch kind, the summed device time (ms) and the
  * number of launches since the last read (kinds: 0 activate, 1 listgen,
  * 2 clear_list, 3 struct_for, 4 range_for, 5 serial, 6 deactivate; struct-for
- * launches are also accumulated under 100 + op of their first member). */
+ * launches are also accumulated under 100 + op of their first member, listgens
+ * under 200 + snode). */
 sg_status sg_set_profiling(sg_grid* g, int32_t on);
 sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int32_t n_kinds);
 

@@ -72,8 +72,13 @@ def lib():
         L.orc_read_field.argtypes = [vp, i32, P(ctypes.c_double), P(ctypes.c_double), i64]
         L.orc_load_field.argtypes = [vp, i32, P(ctypes.c_double), i64]
         L.orc_counters.argtypes = [vp, P(i64)]
+        L.orc_register_array.argtypes = [vp, P(ctypes.c_float), i64, i32]
+        L.orc_read_array.argtypes = [vp, i32, P(ctypes.c_double), P(ctypes.c_double), i64]
+        L.orc_load_array.argtypes = [vp, i32, P(ctypes.c_double), i64]
+        L.orc_range_for.argtypes = [vp, i32, i64, P(i32), i32, P(i32), i32, P(ctypes.c_float), i32, u32]
         for name in ("orc_activate", "orc_listgen", "orc_clear_list", "orc_struct_for", "orc_serial",
-                     "orc_deactivate", "orc_read_field", "orc_load_field", "orc_counters"):
+                     "orc_deactivate", "orc_read_field", "orc_load_field", "orc_counters", "orc_register_array",
+                     "orc_read_array", "orc_load_array", "orc_range_for"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -168,6 +173,34 @@ class Oracle:
     def deactivate_task(self, snode):
         self._check(lib().orc_deactivate(self.h, snode))
 
+    def range_for_task(self, op, n, fields, arrays, params=(), activating=0):
+        f = np.ascontiguousarray(fields, dtype=np.int32)
+        a = np.ascontiguousarray(arrays, dtype=np.int32)
+        p = np.ascontiguousarray(params if len(params) else [0.0], dtype=np.float32)
+        self._check(lib().orc_range_for(self.h, OPS[op], n, _ptr(f, ctypes.c_int32), len(f), _ptr(a, ctypes.c_int32),
+                                        len(a), _ptr(p, ctypes.c_float), len(params), activating))
+
+    # --- particle arrays (SoA: shape (ncomp, n)) ---
+    def register_array(self, arr):
+        a = np.ascontiguousarray(arr, dtype=np.float32)
+        if a.ndim == 1:
+            a = a[None]
+        rc = lib().orc_register_array(self.h, _ptr(a, ctypes.c_float), a.shape[1], a.shape[0])
+        self._check(0 if rc >= 0 else rc)
+        self.array_shapes = getattr(self, "array_shapes", []) + [a.shape]
+        return rc
+
+    def array(self, i, with_mag=False):
+        shape = self.array_shapes[i]
+        v = np.zeros(shape, dtype=np.float64)
+        m = np.zeros(shape, dtype=np.float64)
+        self._check(lib().orc_read_array(self.h, i, _ptr(v, ctypes.c_double), _ptr(m, ctypes.c_double), v.size))
+        return (v, m) if with_mag else v
+
+    def load_array(self, i, data):
+        d = np.ascontiguousarray(data, dtype=np.float64)
+        self._check(lib().orc_load_array(self.h, i, _ptr(d, ctypes.c_double), d.size))
+
     # --- lowering (readings R3, R5) ---
     def listgen_levels(self, leaf):
         """Sparse levels a struct-for over `leaf` needs lists for: every
@@ -203,6 +236,10 @@ class Oracle:
             self._count1()
         elif kind == "serial":
             self.serial_task(c["op"], c["fields"], c.get("params", []))
+            self._count1()
+        elif kind == "range_for":
+            act = sum(1 << i for i, a in enumerate(c.get("activating", [])) if a)
+            self.range_for_task(c["op"], c["n"], c["fields"], c["arrays"], c.get("params", []), act)
             self._count1()
         elif kind == "clear":
             if c["mode"] == "values":
@@ -277,6 +314,8 @@ class Oracle:
 def run_program(prog, upto=None):
     """Replay a workloads program on a fresh oracle grid (eager, unoptimized)."""
     o = Oracle(prog["desc"])
+    for name, arr in prog.get("arrays", {}).items():
+        o.register_array(arr)
     calls = prog["calls"] if upto is None else prog["calls"][:upto]
     for c in calls:
         o.call(c)

@@ -501,8 +501,161 @@ int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const 
         if (!rc) rc = atomic_add(g, f[0], c, x, act_bit(activating, 0));
       });
       break;
+    case OP_GRID_OP:
+      // MLS-MPM grid update (hu2018moving, cited at PAPER.md:444; mpm3d-like):
+      // momentum -> velocity, gravity, sticky-free boundary.  p0 dt, p1 gravity,
+      // p2 bound (cells), p3 n_grid.  Fields: f0..f2 velocity/momentum, f3 mass.
+      if (!need(4)) return fail(g, E_ARG, "GRID_OP needs 4 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        if (rc) return;
+        double m = read(g, f[3], c), mm = read_mag(g, f[3], c);
+        double v[3], mv[3];
+        for (int a = 0; a < 3; a++) { v[a] = read(g, f[a], c); mv[a] = read_mag(g, f[a], c); }
+        if (m > 0) {
+          for (int a = 0; a < 3; a++) {
+            double q = v[a] / m;
+            // propagated bound of |v/m| under relative errors of v and m
+            mv[a] = (mv[a] + std::fabs(v[a]) * (mm / m)) / m;
+            v[a] = q;
+          }
+        }
+        v[1] -= P(0) * P(1);
+        mv[1] += std::fabs(P(0) * P(1));
+        double bound = P(2), n = P(3);
+        for (int a = 0; a < D; a++) {
+          bool cond = ((double)c[a] < bound && v[a] < 0) || ((double)c[a] > n - bound && v[a] > 0);
+          if (cond) { v[a] = 0; mv[a] = 0; }
+        }
+        for (int a = 0; a < 3 && !rc; a++) rc = write(g, f[a], c, v[a], false, mv[a]);
+      });
+      break;
     default:
       return fail(g, E_ARG, "unknown struct-for op");
+  }
+  if (rc) { g->touched.clear(); return rc; }
+  return end_task(g);
+}
+
+// ---------------------------------------------------------------------------
+// Range-for: MLS-MPM particle transfers (hu2018moving, cited at PAPER.md:444;
+// the P2G scatter with atomic adds of PAPER.md:457).  Quadratic B-spline
+// weights over the 3x3x3 neighbourhood.  The index decision (base cell) is
+// made in f32 with the same operation order as the device (reading R16); the
+// rest is f64.  Arrays: a0 x (3 comps), a1 v (3), a2 C (9, row-major), a3 J (1).
+// ---------------------------------------------------------------------------
+struct Kernel {
+  int base[3];
+  double fx[3], w[3][3];
+};
+
+Kernel bspline(const float xp[3], float inv_dx) {
+  Kernel k;
+  for (int a = 0; a < 3; a++) {
+    volatile float X = xp[a] * inv_dx;          // f32 rounding, no contraction
+    volatile float Xm = X - 0.5f;
+    k.base[a] = (int)std::floor((float)Xm);
+    volatile float fx = X - (float)k.base[a];
+    k.fx[a] = (double)(float)fx;
+    double q = k.fx[a];
+    k.w[0][a] = 0.5 * (1.5 - q) * (1.5 - q);
+    k.w[1][a] = 0.75 - (q - 1.0) * (q - 1.0);
+    k.w[2][a] = 0.5 * (q - 0.5) * (q - 0.5);
+  }
+  return k;
+}
+
+double& A_(Grid* g, int arr, int comp, int64_t i) { Array& a = g->arrays[arr]; return a.val[comp * a.n + i]; }
+double& M_(Grid* g, int arr, int comp, int64_t i) { Array& a = g->arrays[arr]; return a.mag[comp * a.n + i]; }
+
+int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_t* ar, int na, const float* p,
+              int np, uint32_t activating) {
+  auto P = [&](int i) { return i < np ? (double)p[i] : 0.0; };
+  for (int i = 0; i < na; i++)
+    if (ar[i] < 0 || ar[i] >= (int)g->arrays.size()) return fail(g, E_ARG, "bad array");
+  for (int i = 0; i < nf; i++) if (!field_ok(g, f[i])) return fail(g, E_ARG, "bad field");
+  if (nf < 4 || na < 4) return fail(g, E_ARG, "MPM ops need 4 fields and 4 arrays");
+  for (int i = 0; i < 4; i++)
+    if (g->arrays[ar[i]].n < n) return fail(g, E_ARG, "array shorter than range");
+  int rc = OK;
+  const float inv_dx = (float)P(1);
+  const double dx = 1.0 / (double)inv_dx;
+  std::vector<std::pair<int, int64_t>> touched_arr;
+  switch (op) {
+    case OP_P2G: {
+      // p0 dt, p1 inv_dx, p2 p_mass, p3 p_vol, p4 E
+      const double dt = P(0), pm = P(2), pv = P(3), E = P(4);
+      for (int64_t i = 0; i < n && !rc; i++) {
+        float xp[3] = {(float)A_(g, ar[0], 0, i), (float)A_(g, ar[0], 1, i), (float)A_(g, ar[0], 2, i)};
+        Kernel k = bspline(xp, inv_dx);
+        double J = A_(g, ar[3], 0, i);
+        double stress = -dt * 4.0 * E * pv * (J - 1.0) * (double)inv_dx * (double)inv_dx;
+        double aff[3][3], v[3];
+        for (int r = 0; r < 3; r++) {
+          v[r] = A_(g, ar[1], r, i);
+          for (int c = 0; c < 3; c++) aff[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? stress : 0.0);
+        }
+        for (int a = 0; a < 3 && !rc; a++)
+          for (int b = 0; b < 3 && !rc; b++)
+            for (int c = 0; c < 3 && !rc; c++) {
+              int off[3] = {a, b, c};
+              double dpos[3], wgt = k.w[a][0] * k.w[b][1] * k.w[c][2];
+              for (int d = 0; d < 3; d++) dpos[d] = ((double)off[d] - k.fx[d]) * dx;
+              Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
+              for (int r = 0; r < 3 && !rc; r++) {
+                double mom = pm * v[r];
+                for (int d = 0; d < 3; d++) mom += aff[r][d] * dpos[d];
+                rc = atomic_add(g, f[r], node, wgt * mom, act_bit(activating, r));
+              }
+              if (!rc) rc = atomic_add(g, f[3], node, wgt * pm, act_bit(activating, 3));
+            }
+      }
+    } break;
+    case OP_G2P: {
+      // p0 dt, p1 inv_dx.  Reads grid velocity; writes v, C, x, J.
+      const double dt = P(0);
+      for (int64_t i = 0; i < n; i++) {
+        float xp[3] = {(float)A_(g, ar[0], 0, i), (float)A_(g, ar[0], 1, i), (float)A_(g, ar[0], 2, i)};
+        Kernel k = bspline(xp, inv_dx);
+        double nv[3] = {0, 0, 0}, mv[3] = {0, 0, 0}, nC[3][3] = {{0}}, mC[3][3] = {{0}};
+        for (int a = 0; a < 3; a++)
+          for (int b = 0; b < 3; b++)
+            for (int c = 0; c < 3; c++) {
+              int off[3] = {a, b, c};
+              double dpos[3], wgt = k.w[a][0] * k.w[b][1] * k.w[c][2];
+              for (int d = 0; d < 3; d++) dpos[d] = ((double)off[d] - k.fx[d]) * dx;
+              Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
+              for (int r = 0; r < 3; r++) {
+                double gv = read(g, f[r], node), gm = read_mag(g, f[r], node) + std::fabs(gv);
+                nv[r] += wgt * gv;
+                mv[r] += std::fabs(wgt) * gm;
+                for (int d = 0; d < 3; d++) {
+                  double s = 4.0 * (double)inv_dx * (double)inv_dx * wgt * dpos[d];
+                  nC[r][d] += s * gv;
+                  mC[r][d] += std::fabs(s) * gm;
+                }
+              }
+            }
+        double tr = nC[0][0] + nC[1][1] + nC[2][2];
+        double mtr = mC[0][0] + mC[1][1] + mC[2][2];
+        for (int r = 0; r < 3; r++) {
+          double x = A_(g, ar[0], r, i);
+          A_(g, ar[1], r, i) = nv[r]; M_(g, ar[1], r, i) = mv[r];
+          A_(g, ar[0], r, i) = x + dt * nv[r];
+          M_(g, ar[0], r, i) = std::fabs(x) + dt * mv[r];
+          for (int d = 0; d < 3; d++) { A_(g, ar[2], 3 * r + d, i) = nC[r][d]; M_(g, ar[2], 3 * r + d, i) = mC[r][d]; }
+        }
+        double J = A_(g, ar[3], 0, i);
+        A_(g, ar[3], 0, i) = J * (1.0 + dt * tr);
+        M_(g, ar[3], 0, i) = std::fabs(J) * (1.0 + dt * mtr);
+        touched_arr.push_back({0, i});
+      }
+      for (int r = 0; r < 4; r++) {
+        Array& a = g->arrays[ar[r]];
+        for (double& v : a.val) v = (double)(float)v;
+      }
+    } break;
+    default:
+      return fail(g, E_ARG, "unknown range-for op");
   }
   if (rc) { g->touched.clear(); return rc; }
   return end_task(g);
@@ -607,6 +760,41 @@ int32_t orc_serial(void* h, int32_t op, const int32_t* fields, int32_t nf, const
 }
 
 int32_t orc_deactivate(void* h, int32_t snode) { return deactivate((Grid*)h, snode); }
+
+// Particle arrays: the oracle keeps its own copy (f32-rounded values in f64).
+int32_t orc_register_array(void* h, const float* data, int64_t n, int32_t ncomp) {
+  Grid* g = (Grid*)h;
+  Array a;
+  a.n = n; a.ncomp = ncomp;
+  a.val.resize((size_t)n * ncomp);
+  a.mag.resize((size_t)n * ncomp);
+  for (size_t i = 0; i < a.val.size(); i++) { a.val[i] = data[i]; a.mag[i] = std::fabs((double)data[i]); }
+  g->arrays.push_back(a);
+  return (int32_t)g->arrays.size() - 1;
+}
+
+int32_t orc_read_array(void* h, int32_t id, double* out, double* mag, int64_t total) {
+  Grid* g = (Grid*)h;
+  if (id < 0 || id >= (int)g->arrays.size()) return fail(g, E_ARG, "bad array");
+  Array& a = g->arrays[id];
+  if (total != (int64_t)a.val.size()) return fail(g, E_ARG, "size mismatch");
+  for (int64_t i = 0; i < total; i++) { out[i] = a.val[i]; if (mag) mag[i] = a.mag[i]; }
+  return OK;
+}
+
+int32_t orc_load_array(void* h, int32_t id, const double* data, int64_t total) {
+  Grid* g = (Grid*)h;
+  if (id < 0 || id >= (int)g->arrays.size()) return fail(g, E_ARG, "bad array");
+  Array& a = g->arrays[id];
+  if (total != (int64_t)a.val.size()) return fail(g, E_ARG, "size mismatch");
+  for (int64_t i = 0; i < total; i++) { a.val[i] = data[i]; a.mag[i] = std::fabs(data[i]); }
+  return OK;
+}
+
+int32_t orc_range_for(void* h, int32_t op, int64_t n, const int32_t* fields, int32_t nf, const int32_t* arrays,
+                      int32_t na, const float* params, int32_t np, uint32_t activating) {
+  return range_for((Grid*)h, op, n, fields, nf, arrays, na, params, np, activating);
+}
 
 // Sorted set of active level-global cells of a sparse level.
 int64_t orc_export_mask(void* h, int32_t snode, int32_t* out, int64_t cap) {

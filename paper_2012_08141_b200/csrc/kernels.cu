@@ -19,7 +19,6 @@
 #include <stdint.h>
 #include <algorithm>
 #include "sg_internal.h"
-#include "mpm_ops.cuh"
 
 namespace sg {
 
@@ -226,6 +225,34 @@ __device__ __forceinline__ bool resolve_entry(const DTree& T, uint32_t e, uint32
   return true;
 }
 
+// Block-table row of a driving-list entry: the block and its face neighbours.
+__device__ __forceinline__ void make_block_row(const DTree& T, uint32_t e, BlockRow* out) {
+  BlockRow r;
+  uint32_t* cont = nullptr;
+  uint32_t first = 0;
+  int org[3] = {0, 0, 0};
+  bool ok = resolve_entry(T, e, cont, first, org);
+  const uint32_t* base = T.seg[T.nseg - 1].base;
+  r.blk = ok ? (uint32_t)(cont - base) + T.payload_off + first : SG_NO_BLOCK;
+  r.maskw = ok && T.leaf_bitmasked ? (uint32_t)(cont - base) + T.lev[T.nlev - 1].mask_off + (first >> 5) : 0u;
+  r.first = first;
+  r.org[0] = org[0]; r.org[1] = org[1]; r.org[2] = org[2];
+  const uint32_t lowmask = ~((1u << T.lblk) - 1u);
+#pragma unroll
+  for (int dir = 0; dir < 6; dir++) {
+    r.nbr[dir] = SG_NO_BLOCK;
+    int axis = dir >> 1;
+    if (!ok || axis >= T.nd || T.driving < 0) continue;
+    int q[3] = {org[0], org[1], org[2]};
+    q[axis] += (dir & 1) ? (1 << T.lev[T.driving].lbelow[axis]) : -1;
+    if (!in_domain(T, q)) continue;
+    uint32_t idx;
+    uint32_t* c2 = locate(T, q, idx);
+    if (c2) r.nbr[dir] = (uint32_t)(c2 - base) + T.payload_off + (idx & lowmask);
+  }
+  *out = r;
+}
+
 // ---------------------------------------------------------------------------
 // Activation
 // ---------------------------------------------------------------------------
@@ -299,7 +326,7 @@ __device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint3
 
 __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGArgs a) {
   __shared__ uint32_t s_warp[LG_TPB / 32];
-  __shared__ uint32_t s_tile, s_base, s_epoch;
+  __shared__ uint32_t s_tile, s_base, s_total, s_epoch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_epoch = ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu;
   uint32_t nparent = a.mode == 0 ? 1u : ld_volatile(a.pcount);
@@ -359,6 +386,7 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
           atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, prefix + total));
         }
         s_base = prefix;
+        s_total = total;
         if (tile == ntiles - 1) {
           uint32_t n = prefix + total;
           if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
@@ -379,6 +407,13 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
     }
     __syncthreads();
+    if (a.out.table) {
+      // block table of the driving level: one row per entry of this tile, all threads
+      const uint32_t end = min(s_base + s_total, a.out.capacity);
+      for (uint32_t i = s_base + threadIdx.x; i < end; i += LG_TPB)
+        make_block_row(a.T, a.out.entries[i], a.out.table + i);
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -394,248 +429,8 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
 
 __global__ void k_clear_list(uint32_t* count) { *count = 0; }
 
-// ---------------------------------------------------------------------------
-// Struct-for megakernel
-// ---------------------------------------------------------------------------
-struct SFArgs {
-  DTree T;
-  DevCtx C;
-  const uint32_t* entries;   // driving list (null when the tree has no driving level)
-  const uint32_t* count;
-  int nops;
-  int need_nbr;
-  int lept;                  // log2 entries per tile
-  int lchunk;                // log2 cells per tile when a block spans several tiles (else -1)
-  int task;
-  DOp ops[SG_MAXOPS];
-  uint64_t aux[SG_MAXOPS];   // 0-D target address per op
-};
-
-constexpr int SF_TPB = 256, SF_MAXE = 256;
-
-struct SFTile {
-  uint32_t* blk0[SF_MAXE];     // payload of field slot 0, first cell of the block
-  uint32_t* cont[SF_MAXE];
-  uint32_t first[SF_MAXE];
-  int org[SF_MAXE][3];
-  uint32_t* nbr[SF_MAXE][6];   // neighbour blocks (field slot 0, first cell), null = absent
-};
-
-template <typename V> __device__ __forceinline__ V ldv(const uint32_t* p);
-template <> __device__ __forceinline__ float ldv<float>(const uint32_t* p) { return __uint_as_float(*p); }
-template <> __device__ __forceinline__ int ldv<int>(const uint32_t* p) { return (int)*p; }
-__device__ __forceinline__ void stv(uint32_t* p, float v) { *p = __float_as_uint(v); }
-__device__ __forceinline__ void stv(uint32_t* p, int v) { *p = (uint32_t)v; }
-
-struct CellCtx {
-  const DTree* T;
-  const SFTile* tile;
-  int e;                 // entry slot in the tile
-  uint32_t j;            // in-block index
-  int c[3];              // leaf coords
-  uint64_t fstride;      // words between field slots
-};
-
-template <typename V>
-__device__ __forceinline__ V ld_id(const CellCtx& x, int slot) {
-  return ldv<V>(x.tile->blk0[x.e] + (uint64_t)slot * x.fstride + x.j);
-}
-template <typename V>
-__device__ __forceinline__ void st_id(const CellCtx& x, int slot, V v) {
-  stv(x.tile->blk0[x.e] + (uint64_t)slot * x.fstride + x.j, v);
-}
-
-// Neighbour value c + d*e_axis (0 when inactive / out of bound).
-template <typename V>
-__device__ __forceinline__ V ld_nbr(const CellCtx& x, int slot, int axis, int d) {
-  const DTree& T = *x.T;
-  int n[3] = {x.c[0], x.c[1], x.c[2]};
-  n[axis] += d;
-  const int bdim = T.driving < 0 ? (1 << T.lev[T.nlev - 1].lres[axis]) : (1 << T.lev[T.driving].lbelow[axis]);
-  int rel = n[axis] - x.tile->org[x.e][axis];
-  const uint32_t* base;
-  if (rel >= 0 && rel < bdim) {
-    base = x.tile->blk0[x.e];
-  } else {
-    if (T.driving < 0) return V(0);
-    base = x.tile->nbr[x.e][axis * 2 + (d > 0 ? 1 : 0)];
-    if (!base) return V(0);
-  }
-  return ldv<V>(base + (uint64_t)slot * x.fstride + inblock_idx(T, n));
-}
-
-template <typename V>
-__device__ __forceinline__ V nbr_sum(const CellCtx& x, int slot) {
-  V s = V(0);
-  for (int a = 0; a < x.T->nd; a++) s += ld_nbr<V>(x, slot, a, -1) + ld_nbr<V>(x, slot, a, +1);
-  return s;
-}
-
-template <typename V>
-__device__ __forceinline__ void apply_downsample(const SFArgs& A, const DOp& op, const CellCtx& x, V val) {
-  const DField& tf = A.C.fields[op.f[0]];
-  const DTree& T2 = A.C.trees[tf.tree];
-  int h[3] = {x.c[0] >> 1, x.c[1] >> 1, x.c[2] >> 1};
-  uint32_t idx;
-  uint32_t* cont;
-  if (op.act & 1u) {
-    cont = activate_walk(A.C, T2, h, idx, A.task);
-  } else {
-    cont = A.C.debug ? locate_active(T2, h, idx) : locate(T2, h, idx);
-    if (!cont && A.C.debug) set_err(A.C, SG_ERR_DEMOTION_TRAP, A.task);
-  }
-  if (!cont) return;
-  uint32_t* p = cont + T2.payload_off + ((uint64_t)tf.slot << T2.ln_leaf) + idx;
-  if (sizeof(V) == 4 && V(0.5) != V(0)) atomicAdd((float*)p, (float)val);
-  else atomicAdd((int*)p, (int)val);
-}
-
-template <typename V>
-__device__ __forceinline__ void apply_op(const SFArgs& A, const DOp& op, int o, const CellCtx& x, V* acc) {
-  const int D = x.T->nd;
-  switch (op.op) {
-    case SG_OP_FILL: st_id<V>(x, op.slot[0], (V)op.p[0]); break;
-    case SG_OP_ADD_CONST: st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[1]) + (V)op.p[0]); break;
-    case SG_OP_INC: st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + (V)op.p[0]); break;
-    case SG_OP_AXPY: st_id<V>(x, op.slot[0], (V)op.p[0] * ld_id<V>(x, op.slot[1]) + ld_id<V>(x, op.slot[2])); break;
-    case SG_OP_STENCIL: {
-      V s = nbr_sum<V>(x, op.slot[1]) - (V)(2 * D) * ld_id<V>(x, op.slot[1]);
-      st_id<V>(x, op.slot[0], s);
-    } break;
-    case SG_OP_JACOBI: {
-      V s = ld_id<V>(x, op.slot[2]) + nbr_sum<V>(x, op.slot[1]);
-      st_id<V>(x, op.slot[0], s / (V)(2 * D));
-    } break;
-    case SG_OP_REDUCE_SUM: acc[o] += ld_id<V>(x, op.slot[1]); break;
-    case SG_OP_DOWNSAMPLE: {
-      V v = op.slot[1] >= 0 ? ld_id<V>(x, op.slot[1]) : V(0);
-      apply_downsample<V>(A, op, x, (V)op.p[0] * v + (V)op.p[1]);
-    } break;
-    case SG_OP_JITTER:
-      if ((x.c[0] & 1) == 0) st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + ld_nbr<V>(x, op.slot[0], 0, +1));
-      break;
-    case SG_OP_GRID_OP: mpm_grid_op(op, x.c, x.tile->blk0[x.e] + x.j, x.fstride); break;
-    default: break;
-  }
-}
-
-template <typename V>
-__device__ __forceinline__ void run_cell(const SFArgs& A, const CellCtx& x, V* acc) {
-#pragma unroll
-  for (int o = 0; o < SG_MAXOPS; o++) {
-    if (o >= A.nops) break;
-    apply_op<V>(A, A.ops[o], o, x, acc);
-  }
-}
-
-template <typename V>
-__device__ void block_reduce_add(const SFArgs& A, V* acc) {
-  __shared__ V s_red[SF_TPB / 32];
-#pragma unroll
-  for (int o = 0; o < SG_MAXOPS; o++) {
-    if (o >= A.nops) break;
-    if (A.ops[o].op != SG_OP_REDUCE_SUM) continue;
-    V v = acc[o];
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      V t = V(0);
-      for (int w = 0; w < SF_TPB / 32; w++) t += s_red[w];
-      if (sizeof(V) == 4 && V(0.5) != V(0)) atomicAdd((float*)A.aux[o], (float)t);
-      else atomicAdd((int*)A.aux[o], (int)t);
-    }
-    __syncthreads();
-  }
-}
-
-template <typename V>
-__global__ void __launch_bounds__(SF_TPB) k_struct_for(const __grid_constant__ SFArgs A) {
-  __shared__ SFTile tile;
-  const DTree& T = A.T;
-  const uint32_t nent = A.entries ? ld_volatile(A.count) : 1u;
-  const int lblk = T.lblk;
-  const int ept = 1 << A.lept;
-  uint64_t ntiles;
-  int tiles_per_entry = 1;
-  if (A.lchunk >= 0) {
-    tiles_per_entry = 1 << (lblk - A.lchunk);
-    ntiles = (uint64_t)nent * tiles_per_entry;
-  } else {
-    ntiles = (nent + ept - 1) >> A.lept;
-  }
-  const uint64_t fstride = 1ull << T.ln_leaf;
-  V acc[SG_MAXOPS];
-#pragma unroll
-  for (int o = 0; o < SG_MAXOPS; o++) acc[o] = V(0);
-
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    uint32_t e0, ne;
-    uint32_t jbase = 0, tcells;
-    if (A.lchunk >= 0) {
-      e0 = (uint32_t)(t / tiles_per_entry);
-      ne = 1;
-      jbase = (uint32_t)(t % tiles_per_entry) << A.lchunk;
-      tcells = 1u << A.lchunk;
-    } else {
-      e0 = (uint32_t)(t << A.lept);
-      ne = min((uint32_t)ept, nent - e0);
-      tcells = ne << lblk;
-    }
-    // resolve the tile's entries (and neighbour blocks) into shared memory
-    for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
-      uint32_t* cont;
-      uint32_t first;
-      int org[3];
-      bool ok = resolve_entry(T, A.entries ? A.entries[e0 + i] : 0u, cont, first, org);
-      tile.cont[i] = ok ? cont : nullptr;
-      tile.blk0[i] = ok ? cont + T.payload_off + first : nullptr;
-      tile.first[i] = first;
-      tile.org[i][0] = org[0]; tile.org[i][1] = org[1]; tile.org[i][2] = org[2];
-    }
-    __syncthreads();
-    if (A.need_nbr && T.driving >= 0) {
-      const int nd2 = 2 * T.nd;
-      for (uint32_t i = threadIdx.x; i < ne * nd2; i += SF_TPB) {
-        uint32_t e = i / nd2;
-        int dir = i % nd2, axis = dir >> 1, s = (dir & 1) ? 1 : -1;
-        int q[3] = {tile.org[e][0], tile.org[e][1], tile.org[e][2]};
-        q[axis] += s > 0 ? (1 << T.lev[T.driving].lbelow[axis]) : -1;
-        uint32_t* nb = nullptr;
-        if (tile.blk0[e] && in_domain(T, q)) {
-          uint32_t idx;
-          uint32_t* c2 = locate(T, q, idx);
-          if (c2) nb = c2 + T.payload_off + (idx & ~((1u << lblk) - 1u));
-        }
-        tile.nbr[e][dir] = nb;
-      }
-      __syncthreads();
-    }
-    for (uint32_t i = threadIdx.x; i < tcells; i += SF_TPB) {
-      CellCtx x;
-      x.T = &T;
-      x.tile = &tile;
-      x.e = A.lchunk >= 0 ? 0 : (int)(i >> lblk);
-      x.j = A.lchunk >= 0 ? jbase + i : (i & ((1u << lblk) - 1u));
-      x.fstride = fstride;
-      if (!tile.blk0[x.e]) continue;
-      if (T.leaf_bitmasked) {
-        const DLevel& LL = T.lev[T.nlev - 1];
-        uint32_t li = tile.first[x.e] + x.j;
-        if (!((tile.cont[x.e][LL.mask_off + (li >> 5)] >> (li & 31)) & 1u)) continue;
-      }
-      int bc[3];
-      inblock_coords(T, x.j, bc);
-      x.c[0] = tile.org[x.e][0] + bc[0];
-      x.c[1] = tile.org[x.e][1] + bc[1];
-      x.c[2] = tile.org[x.e][2] + bc[2];
-      run_cell<V>(A, x, acc);
-    }
-    __syncthreads();
-  }
-  block_reduce_add<V>(A, acc);
-}
+#include "mpm_ops.cuh"
+#include "struct_for.cuh"
 
 // ---------------------------------------------------------------------------
 // Serial and range-for
@@ -882,6 +677,9 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   a->T = t; a->C = c; a->task = task; a->nops = nops;
   a->entries = drive ? drive->entries : nullptr;
   a->count = drive ? drive->count : nullptr;
+  a->table = drive ? drive->table : nullptr;
+  a->has_reduce = 0;
+  for (int o = 0; o < nops; o++) a->has_reduce |= ops[o].op == SG_OP_REDUCE_SUM;
   a->need_nbr = 0;
   bool i32 = false;
   for (int o = 0; o < nops; o++) {
@@ -895,18 +693,36 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   for (int o = 0; o < nops; o++)
     if (ops[o].scalar >= 0) a->aux[o] = (uint64_t)(c.scalars + ops[o].scalar);
   const int lblk = t.lblk;
-  const int TILE_LOG = 10;  // 1024 cells
-  if (lblk > TILE_LOG) { a->lchunk = TILE_LOG; a->lept = 0; }
-  else {
-    a->lchunk = -1;
-    int lept = TILE_LOG - lblk;
-    if (lept > 8) lept = 8;  // at most SF_MAXE entries
-    a->lept = lept;
+  // tile: 2048 cells (at most SF_MAXE blocks); larger blocks span several tiles
+  const int TILE_LOG = 11;
+  a->ltile = TILE_LOG;
+  a->lept = lblk >= TILE_LOG ? 0 : std::min(TILE_LOG - lblk, 8);
+  // QUAD path: the block is a single level whose fastest axis has extent >= 4
+  bool quad = false;
+  a->lb[0] = a->lb[1] = a->lb[2] = 0;
+  if (t.nlev - 1 - t.driving == 1) {
+    const DLevel& B = t.lev[t.nlev - 1];
+    for (int d = 0; d < 3; d++) a->lb[d] = B.le[d];
+    quad = B.le[t.nd - 1] >= 2;
   }
   int grid = grid_hint > 0 ? grid_hint : num_sms() * 8;
   grid = max(1, min(grid, num_sms() * 8));
-  if (i32) k_struct_for<int><<<grid, SF_TPB, 0, (cudaStream_t)stream>>>(*a);
-  else k_struct_for<float><<<grid, SF_TPB, 0, (cudaStream_t)stream>>>(*a);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nd = quad ? t.nd : 0;
+  static int pair = -1;
+  if (pair < 0) { const char* e = getenv("SG_SF_PAIR"); pair = e ? atoi(e) != 0 : 1; }
+  const bool stencil = a->need_nbr;
+#define SG_SF_LAUNCH(V)                                                                     \
+  switch (nd) {                                                                             \
+    case 1: k_struct_for<V, 1, false><<<grid, SF_TPB, 0, s>>>(*a); break;                   \
+    case 2: if (pair && stencil) k_struct_for<V, 2, true><<<grid, SF_TPB, 0, s>>>(*a);       \
+            else k_struct_for<V, 2, false><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    case 3: if (pair && stencil) k_struct_for<V, 3, true><<<grid, SF_TPB, 0, s>>>(*a);       \
+            else k_struct_for<V, 3, false><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    default: k_struct_for<V, 0, false><<<grid, SF_TPB, 0, s>>>(*a); break;                  \
+  }
+  if (i32) { SG_SF_LAUNCH(int) } else { SG_SF_LAUNCH(float) }
+#undef SG_SF_LAUNCH
   delete a;
   return check_launch();
 }

@@ -207,9 +207,19 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
     if (t.kind != SG_TASK_SERIAL || L.field_tree[t.fields[0]] >= 0) { err = "CLEAR_SCALAR is a serial op on a 0-D field"; return SG_ERR_ARG; }
     return SG_OK;
   }
-  if (t.op == SG_OP_P2G || t.op == SG_OP_G2P) {
-    if (t.kind != SG_TASK_RANGE_FOR) { err = "P2G/G2P are range-for ops"; return SG_ERR_ARG; }
-    return SG_OK;
+  if (t.op == SG_OP_P2G || t.op == SG_OP_G2P || t.op == SG_OP_GRID_OP) {
+    if (t.op != SG_OP_GRID_OP && t.kind != SG_TASK_RANGE_FOR) { err = "P2G/G2P are range-for ops"; return SG_ERR_ARG; }
+    int tree = L.field_tree[t.fields[0]];
+    if (tree < 0 || L.trees[tree].nd != 3 || L.trees[tree].driving < 0) {
+      err = "MPM grid fields must live in a 3-D sparse tree"; return SG_ERR_ARG;
+    }
+    for (int i = 0; i < 4; i++) {
+      if (L.field_tree[t.fields[i]] != tree || L.field_dtype[t.fields[i]] != SG_F32) {
+        err = "MPM grid fields must be f32 fields of one tree"; return SG_ERR_ARG;
+      }
+      if (t.op != SG_OP_GRID_OP && t.arrays[i] < 0) { err = "MPM ops need 4 particle arrays"; return SG_ERR_ARG; }
+    }
+    if (t.op != SG_OP_GRID_OP) return SG_OK;
   }
   if (!sf) { err = "op must be launched as a struct-for"; return SG_ERR_ARG; }
   if (t.snode <= 0 || t.snode >= (int)L.nodes.size() || L.nodes[t.snode].kind == SG_PLACE ||

@@ -261,6 +261,8 @@ static sg_status derive_tree(sg_grid* g, int tid, DTree& T) {
       if (((uint64_t)S.capacity << T.lev[k].ln) > (1ull << 32))
         return fail(SG_ERR_LAYOUT, "list entries would overflow u32: lower opts.pool_capacity");
     }
+    if (s == T.nseg - 1 && (uint64_t)S.capacity * S.stride >= 0xFFFFFFFFull)
+      return fail(SG_ERR_LAYOUT, "leaf pool exceeds 2^32 words (block offsets are u32): lower opts.pool_capacity");
   }
   return SG_OK;
 }
@@ -310,6 +312,10 @@ static sg_status alloc_list(sg_grid* g, int tid, int k) {
   uint64_t max_tiles = (pcap * cpp + 1023) / 1024 + 1;
   Ls.capacity = (uint32_t)cap;
   Ls.max_tiles = (uint32_t)std::min<uint64_t>(max_tiles, 0xFFFFFFFFull);
+  if (k == T.driving) {
+    Ls.table = (BlockRow*)g->dev_alloc(cap * sizeof(BlockRow));
+    if (!Ls.table) return fail(SG_ERR_CUDA, "block table allocation failed");
+  }
   Ls.entries = (uint32_t*)g->dev_alloc(cap * 4);
   Ls.count = (uint32_t*)g->dev_alloc(16);
   Ls.ctl = (uint32_t*)g->dev_alloc(16);
@@ -367,6 +373,13 @@ extern "C" sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_o
     g->d_fields = (DField*)g->dev_alloc(std::max<size_t>(1, nf) * sizeof(DField));
     g->ctx.scalars = (uint32_t*)g->dev_alloc(std::max(1, g->L.n_scalars) * 4);
     g->ctx.err = (uint32_t*)g->dev_alloc(16);
+    g->ctx.max_grid = g->num_sms * 8;
+    g->ctx.partials = (double*)g->dev_alloc((size_t)SG_MAXOPS * g->ctx.max_grid * sizeof(double));
+    g->ctx.red_done = (uint32_t*)g->dev_alloc(16);
+    if (!g->ctx.partials || !g->ctx.red_done || cudaMemsetAsync(g->ctx.red_done, 0, 16, g->stream) != cudaSuccess) {
+      delete g;
+      return fail(SG_ERR_CUDA, "reduction scratch allocation failed");
+    }
     g->d_arrays_cap = 64;
     g->d_arrays = (DArray*)g->dev_alloc(g->d_arrays_cap * sizeof(DArray));
     if (!g->d_trees || !g->d_fields || !g->ctx.scalars || !g->ctx.err || !g->d_arrays) {
@@ -608,7 +621,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         e1 = g->get_event();
         cudaEventRecord(e1, g->stream);
         const PTask& t = g->eager[mem[0]];
-        int key = t.type == TT_STRUCT_FOR ? 100 + t.t.op : t.type;
+        int key = t.type == TT_STRUCT_FOR ? 100 + t.t.op : t.type == TT_LISTGEN ? 200 + t.snode : t.type;
         g->prof_pending.push_back({key, {e0, e1}});
       }
     }
@@ -796,7 +809,7 @@ extern "C" sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int
     float t = 0;
     cudaEventElapsedTime(&t, p.second.first, p.second.second);
     int key = p.first;
-    int kinds[2] = {key >= 100 ? TT_STRUCT_FOR : key, key >= 100 ? key : -1};
+    int kinds[2] = {key >= 200 ? TT_LISTGEN : key >= 100 ? TT_STRUCT_FOR : key, key >= 100 ? key : -1};
     for (int k : kinds) {
       if (k >= 0 && k < n_kinds) { ms[k] += t; count[k]++; }
     }

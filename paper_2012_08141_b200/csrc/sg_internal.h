@@ -79,12 +79,28 @@ struct DArray {
   int32_t ncomp, dtype;
 };
 
+// Per-entry block table written by the listgen of a tree's driving level: the
+// resolved leaf block and its 2*nd face neighbours, so struct-for tiles start
+// with one coalesced load instead of a chain of tree walks.  Valid exactly as
+// long as the list is (any mask change regenerates both).
+// Offsets are u32 word offsets from the leaf segment's pool base (SG_NO_BLOCK =
+// absent), so the kernels address global memory as base + offset.
+#define SG_NO_BLOCK 0xFFFFFFFFu
+struct BlockRow {
+  uint32_t blk;        // payload of field slot 0, first cell of the block
+  uint32_t maskw;      // bitmasked leaf: word offset of the block's first mask word
+  uint32_t first;      // first leaf index of the block in its container
+  int32_t org[3];      // leaf coords of the block origin
+  uint32_t nbr[6];     // face-neighbour blocks (field slot 0, first cell)
+};
+
 // Element list of one level.
 struct DList {
   uint32_t* entries;
   uint32_t* count;     // device-side count
   uint64_t* status;    // look-back tile descriptors
   uint32_t* ctl;       // [0] tile counter, [1] done counter, [2] epoch
+  BlockRow* table;     // driving level only, else null
   uint32_t capacity;
   uint32_t max_tiles;
 };
@@ -109,6 +125,9 @@ struct DevCtx {
   DArray* arrays;      // device array
   uint32_t* scalars;   // 0-D field storage
   uint32_t* err;       // [0] code (negative sg_status as u32), [1] task id
+  double* partials;    // [SG_MAXOPS][max_grid] per-CTA reduction partials
+  uint32_t* red_done;  // CTA ticket for the last-block reduction
+  int32_t max_grid;
   int32_t debug;
 };
 

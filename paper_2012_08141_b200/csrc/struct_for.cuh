@@ -1,0 +1,521 @@
+// struct_for.cuh -- the fused struct-for megakernel (included by kernels.cu).
+//
+// One launch runs a fused group of ops (Figs. 7-8
+// "tasks that loop over the active elements of the same tensor") over the
+// element list of the tree's driving level.  Each CTA
+// iteration takes a tile of leaf blocks whose rows (block, origin, face
+// neighbours) come from the list's block table in one coalesced read.  Every
+// thread owns a fixed set of cells of the tile and runs the ops of the group on
+// them in order (op-outer, cell-inner: one tight loop per op), so an identity
+// access never leaves its thread: fused accumulations need no atomics and a
+// value written by op k is read back by op k+1 from L1 (PAPER.md:400 atomic
+// demotion and store-to-load forwarding).  The planner only fuses groups whose
+// shared fields are accessed at the identity, so no cross-thread
+// ordering is needed between ops.
+//
+// Addresses are u32 word offsets from the leaf pool base (a kernel parameter),
+// so every access is a global-space load/store.
+//
+// Two cell paths:
+//   QUAD    blocks that are one dense/bitmasked level whose fastest axis has
+//           extent >= 4 (C1, C2, C3, C5): a thread owns 4 consecutive cells of a
+//           row and moves them with 16-byte loads/stores; neighbour rows along
+//           the slower axes are whole quads, the fast-axis neighbours come from
+//           the quad itself plus two scalars.  Stencils process two quads per
+//           thread with all loads issued before any arithmetic.
+//   GENERIC any other block shape: one cell per thread, hierarchical decode.
+
+struct SFArgs {
+  DTree T;
+  DevCtx C;
+  const uint32_t* entries;   // driving list (null when the tree has no driving level)
+  const uint32_t* count;
+  const BlockRow* table;     // the list's block table
+  int has_reduce;
+  int nops;
+  int need_nbr;
+  int ltile;                 // log2 cells per tile
+  int lept;                  // log2 entries per tile (0 when a block spans tiles)
+  int task;
+  int lb[3];                 // QUAD: log2 block extent per axis
+  DOp ops[SG_MAXOPS];
+  uint64_t aux[SG_MAXOPS];   // 0-D target address per op
+};
+
+constexpr int SF_TPB = 256, SF_MAXE = 256;
+
+struct SFTile {
+  uint32_t blk[SF_MAXE];
+  uint32_t maskw[SF_MAXE];
+  uint32_t first[SF_MAXE];
+  int org[SF_MAXE][3];
+  uint32_t nbr[SF_MAXE][6];
+};
+
+template <typename V> __device__ __forceinline__ V ldv(const uint32_t* p);
+template <> __device__ __forceinline__ float ldv<float>(const uint32_t* p) { return __uint_as_float(*p); }
+template <> __device__ __forceinline__ int ldv<int>(const uint32_t* p) { return (int)*p; }
+__device__ __forceinline__ void stv(uint32_t* p, float v) { *p = __float_as_uint(v); }
+__device__ __forceinline__ void stv(uint32_t* p, int v) { *p = (uint32_t)v; }
+template <typename V> __device__ __forceinline__ bool is_float() { return false; }
+template <> __device__ __forceinline__ bool is_float<float>() { return true; }
+
+__device__ __forceinline__ void atomic_add_v(uint32_t* p, float v) { atomicAdd((float*)p, v); }
+__device__ __forceinline__ void atomic_add_v(uint32_t* p, int v) { atomicAdd((int*)p, v); }
+
+// Reductions into 0-D fields: per-thread partials -> warp (double) -> CTA
+// shared accumulator -> per-CTA partial in global memory -> the last CTA sums
+// the partials in CTA order (deterministic, f64) and adds once to the target.
+__shared__ double s_red[SG_MAXOPS];
+
+template <typename V>
+__device__ __forceinline__ void warp_add(int o, V v) {
+  double d = (double)v;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) d += __shfl_xor_sync(0xffffffffu, d, s);
+  if ((threadIdx.x & 31) == 0 && d != 0.0) atomicAdd(&s_red[o], d);
+}
+
+template <typename V>
+__device__ void finish_reductions(const SFArgs& A) {
+  __shared__ bool s_last;
+  __shared__ double s_sum[SF_TPB];
+  __syncthreads();
+  const int G = gridDim.x;
+  if (threadIdx.x < SG_MAXOPS) A.C.partials[threadIdx.x * A.C.max_grid + blockIdx.x] = s_red[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(A.C.red_done, 1u) == (uint32_t)G - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int o = 0; o < A.nops; o++) {
+    if (A.ops[o].op != SG_OP_REDUCE_SUM) continue;
+    double t = 0.0;   // fixed-order tree sum over CTAs
+    for (int b = threadIdx.x; b < G; b += SF_TPB) t += *(volatile double*)&A.C.partials[o * A.C.max_grid + b];
+    s_sum[threadIdx.x] = t;
+    __syncthreads();
+    for (int w = SF_TPB / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      uint32_t* tgt = (uint32_t*)A.aux[o];
+      V old = ldv<V>(tgt);
+      stv(tgt, (V)((double)old + s_sum[0]));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *A.C.red_done = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// scalar (one cell) helpers
+// ---------------------------------------------------------------------------
+struct CellCtx {
+  const DTree* T;
+  const SFTile* tile;
+  uint32_t* P;           // leaf pool base
+  int e;                 // entry slot in the tile
+  uint32_t j;            // in-block index
+  int c[3];              // leaf coords
+  uint64_t fstride;      // words between field slots
+};
+
+__device__ __forceinline__ uint32_t* cell_ptr(const CellCtx& x, int slot) {
+  return x.P + x.tile->blk[x.e] + (uint64_t)slot * x.fstride + x.j;
+}
+
+template <typename V>
+__device__ __forceinline__ V ld_id(const CellCtx& x, int slot) { return ldv<V>(cell_ptr(x, slot)); }
+template <typename V>
+__device__ __forceinline__ void st_id(const CellCtx& x, int slot, V v) { stv(cell_ptr(x, slot), v); }
+
+// Neighbour value c + d*e_axis (0 when inactive / out of bound).
+template <typename V>
+__device__ __forceinline__ V ld_nbr(const CellCtx& x, int slot, int axis, int d) {
+  const DTree& T = *x.T;
+  int n[3] = {x.c[0], x.c[1], x.c[2]};
+  n[axis] += d;
+  const int bdim = T.driving < 0 ? (1 << T.lev[T.nlev - 1].lres[axis]) : (1 << T.lev[T.driving].lbelow[axis]);
+  int rel = n[axis] - x.tile->org[x.e][axis];
+  uint32_t base;
+  if (rel >= 0 && rel < bdim) {
+    base = x.tile->blk[x.e];
+  } else {
+    if (T.driving < 0) return V(0);
+    base = x.tile->nbr[x.e][axis * 2 + (d > 0 ? 1 : 0)];
+    if (base == SG_NO_BLOCK) return V(0);
+  }
+  return ldv<V>(x.P + base + (uint64_t)slot * x.fstride + inblock_idx(T, n));
+}
+
+template <typename V>
+__device__ __forceinline__ V nbr_sum(const CellCtx& x, int slot) {
+  V s = V(0);
+  for (int a = 0; a < x.T->nd; a++) s += ld_nbr<V>(x, slot, a, -1) + ld_nbr<V>(x, slot, a, +1);
+  return s;
+}
+
+template <typename V>
+__device__ __noinline__ void apply_downsample(const SFArgs& A, const DOp& op, const int c[3], V val) {
+  const DField& tf = A.C.fields[op.f[0]];
+  const DTree& T2 = A.C.trees[tf.tree];
+  int h[3] = {c[0] >> 1, c[1] >> 1, c[2] >> 1};
+  uint32_t idx;
+  uint32_t* cont;
+  if (op.act & 1u) {
+    cont = activate_walk(A.C, T2, h, idx, A.task);
+  } else {
+    cont = A.C.debug ? locate_active(T2, h, idx) : locate(T2, h, idx);
+    if (!cont && A.C.debug) set_err(A.C, SG_ERR_DEMOTION_TRAP, A.task);
+  }
+  if (!cont) return;
+  atomic_add_v(cont + T2.payload_off + ((uint64_t)tf.slot << T2.ln_leaf) + idx, val);
+}
+
+// One op on one cell (GENERIC path, and the per-lane ops of the QUAD path).
+// Returns the REDUCE contribution.
+template <typename V>
+__device__ __forceinline__ V apply_cell(const SFArgs& A, const DOp& op, const CellCtx& x) {
+  const int D = x.T->nd;
+  switch (op.op) {
+    case SG_OP_FILL: st_id<V>(x, op.slot[0], (V)op.p[0]); break;
+    case SG_OP_ADD_CONST: st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[1]) + (V)op.p[0]); break;
+    case SG_OP_INC: st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + (V)op.p[0]); break;
+    case SG_OP_AXPY: st_id<V>(x, op.slot[0], (V)op.p[0] * ld_id<V>(x, op.slot[1]) + ld_id<V>(x, op.slot[2])); break;
+    case SG_OP_STENCIL:
+      st_id<V>(x, op.slot[0], nbr_sum<V>(x, op.slot[1]) - (V)(2 * D) * ld_id<V>(x, op.slot[1]));
+      break;
+    case SG_OP_JACOBI:
+      st_id<V>(x, op.slot[0], (ld_id<V>(x, op.slot[2]) + nbr_sum<V>(x, op.slot[1])) / (V)(2 * D));
+      break;
+    case SG_OP_REDUCE_SUM: return ld_id<V>(x, op.slot[1]);
+    case SG_OP_DOWNSAMPLE: {
+      V v = op.slot[1] >= 0 ? ld_id<V>(x, op.slot[1]) : V(0);
+      apply_downsample<V>(A, op, x.c, (V)op.p[0] * v + (V)op.p[1]);
+    } break;
+    case SG_OP_JITTER:
+      if ((x.c[0] & 1) == 0) st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + ld_nbr<V>(x, op.slot[0], 0, +1));
+      break;
+    case SG_OP_GRID_OP: mpm_grid_op(op, x.c, cell_ptr(x, 0), x.fstride); break;
+    default: break;
+  }
+  return V(0);
+}
+
+// ---------------------------------------------------------------------------
+// quad path
+// ---------------------------------------------------------------------------
+template <typename V>
+struct Q4 { V v[4]; };
+
+template <typename V>
+__device__ __forceinline__ Q4<V> ld4(const uint32_t* p) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  Q4<V> q;
+  if (is_float<V>()) {
+    q.v[0] = (V)__uint_as_float(u.x); q.v[1] = (V)__uint_as_float(u.y);
+    q.v[2] = (V)__uint_as_float(u.z); q.v[3] = (V)__uint_as_float(u.w);
+  } else {
+    q.v[0] = (V)(int)u.x; q.v[1] = (V)(int)u.y; q.v[2] = (V)(int)u.z; q.v[3] = (V)(int)u.w;
+  }
+  return q;
+}
+
+__device__ __forceinline__ uint32_t bits_of(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ uint32_t bits_of(int v) { return (uint32_t)v; }
+
+template <typename V>
+__device__ __forceinline__ void st4(uint32_t* p, const Q4<V>& q, uint32_t amask) {
+  if (amask == 0xFu) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(bits_of(q.v[0]), bits_of(q.v[1]), bits_of(q.v[2]), bits_of(q.v[3]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if ((amask >> k) & 1u) p[k] = bits_of(q.v[k]);
+  }
+}
+
+struct QuadCtx {
+  uint32_t off;            // word offset of lane 0 (field slot 0); SG_NO_BLOCK: skip
+  uint32_t j0;             // in-block index of lane 0
+  int r[3];                // block-relative coords of lane 0
+  int e;
+  uint32_t amask;          // active lanes
+};
+
+template <int ND>
+__device__ __forceinline__ QuadCtx quad_ctx(const SFArgs& A, const SFTile& tile, const uint32_t* P, uint32_t i,
+                                            uint32_t lq, bool chunked, uint32_t jbase) {
+  QuadCtx x;
+  x.e = chunked ? 0 : (int)(i >> lq);
+  x.j0 = chunked ? jbase + 4 * i : 4 * (i & ((1u << lq) - 1u));
+  const uint32_t b = tile.blk[x.e];
+  x.off = b == SG_NO_BLOCK ? SG_NO_BLOCK : b + x.j0;
+  x.amask = 0xFu;
+  if (b != SG_NO_BLOCK && A.T.leaf_bitmasked) {
+    uint32_t li = (tile.first[x.e] & 31u) + x.j0;
+    x.amask = (P[tile.maskw[x.e] + (li >> 5)] >> (li & 31)) & 0xFu;
+  }
+  const int lb1 = ND > 1 ? A.lb[1] : 0, lb2 = ND > 2 ? A.lb[2] : 0;
+  x.r[0] = (int)(x.j0 >> (lb1 + lb2));
+  x.r[1] = ND > 1 ? (int)((x.j0 >> lb2) & ((1u << lb1) - 1u)) : 0;
+  x.r[2] = ND > 2 ? (int)(x.j0 & ((1u << lb2) - 1u)) : 0;
+  return x;
+}
+
+// Gathers the 2*ND face-neighbour values of a quad (loads only).
+template <typename V, int ND>
+struct NbrLoads {
+  Q4<V> row[2 * (ND - 1) + 1];   // neighbour rows along the slower axes
+  V lo, hi;                      // fast-axis ends
+};
+
+template <typename V, int ND>
+__device__ __forceinline__ void nbr_load(const SFArgs& A, const SFTile& tile, const uint32_t* P, const QuadCtx& x,
+                                         uint64_t so, NbrLoads<V, ND>& L) {
+  constexpr int f = ND - 1;
+  const int Bf = 1 << A.lb[f];
+  L.lo = V(0);
+  L.hi = V(0);
+  if (x.r[f] > 0) L.lo = ldv<V>(P + so + x.off - 1);
+  else if (tile.nbr[x.e][2 * f] != SG_NO_BLOCK) L.lo = ldv<V>(P + so + tile.nbr[x.e][2 * f] + x.j0 + (Bf - 1));
+  if (x.r[f] + 4 < Bf) L.hi = ldv<V>(P + so + x.off + 4);
+  else if (tile.nbr[x.e][2 * f + 1] != SG_NO_BLOCK) L.hi = ldv<V>(P + so + tile.nbr[x.e][2 * f + 1] + x.j0 + 4 - Bf);
+#pragma unroll
+  for (int a = 0; a < f; a++) {
+    int sh = 0;
+#pragma unroll
+    for (int b = a + 1; b < ND; b++) sh += A.lb[b];
+    const int B = 1 << A.lb[a];
+    const uint32_t stride = 1u << sh;
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+      const int d = s ? 1 : -1;
+      uint32_t off;
+      if (x.r[a] + d >= 0 && x.r[a] + d < B) off = x.off + d * (int)stride;
+      else {
+        uint32_t nb = tile.nbr[x.e][2 * a + s];
+        off = nb == SG_NO_BLOCK ? SG_NO_BLOCK : nb + x.j0 - d * (int)((B - 1) * stride);
+      }
+      Q4<V>& q = L.row[2 * a + s];
+      if (off != SG_NO_BLOCK) q = ld4<V>(P + so + off);
+      else { q.v[0] = q.v[1] = q.v[2] = q.v[3] = V(0); }
+    }
+  }
+}
+
+template <typename V, int ND>
+__device__ __forceinline__ Q4<V> nbr_sum4(const NbrLoads<V, ND>& L, const Q4<V>& c) {
+  Q4<V> s;
+  s.v[0] = L.lo + c.v[1];
+  s.v[1] = c.v[0] + c.v[2];
+  s.v[2] = c.v[1] + c.v[3];
+  s.v[3] = c.v[2] + L.hi;
+#pragma unroll
+  for (int r = 0; r < 2 * (ND - 1); r++)
+#pragma unroll
+    for (int k = 0; k < 4; k++) s.v[k] += L.row[r].v[k];
+  return s;
+}
+
+template <typename V, int ND, bool PAIR>
+__device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, uint32_t* P, uint32_t nq, uint32_t lq,
+                                          bool chunked, uint32_t jbase, uint64_t fs) {
+  for (int o = 0; o < A.nops; o++) {
+    const DOp& op = A.ops[o];
+    const uint64_t s0 = (uint64_t)op.slot[0] * fs, s1 = (uint64_t)(op.slot[1] < 0 ? 0 : op.slot[1]) * fs,
+                   s2 = (uint64_t)(op.slot[2] < 0 ? 0 : op.slot[2]) * fs;
+    switch (op.op) {
+      case SG_OP_FILL: {
+        Q4<V> q;
+#pragma unroll
+        for (int k = 0; k < 4; k++) q.v[k] = (V)op.p[0];
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          if (x.off != SG_NO_BLOCK && x.amask) st4<V>(P + s0 + x.off, q, x.amask);
+        }
+      } break;
+      case SG_OP_ADD_CONST:
+      case SG_OP_INC:
+      case SG_OP_AXPY: {
+        const V p0 = (V)op.p[0];
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || !x.amask) continue;
+          Q4<V> q;
+          if (op.op == SG_OP_AXPY) {
+            Q4<V> xx = ld4<V>(P + s1 + x.off), yy = ld4<V>(P + s2 + x.off);
+#pragma unroll
+            for (int k = 0; k < 4; k++) q.v[k] = p0 * xx.v[k] + yy.v[k];
+          } else {
+            q = ld4<V>(P + (op.op == SG_OP_INC ? s0 : s1) + x.off);
+#pragma unroll
+            for (int k = 0; k < 4; k++) q.v[k] += p0;
+          }
+          st4<V>(P + s0 + x.off, q, x.amask);
+        }
+      } break;
+      case SG_OP_STENCIL:
+      case SG_OP_JACOBI: {
+        const bool jac = op.op == SG_OP_JACOBI;
+        const V inv = V(1) / (V)(2 * ND);
+        // two quads per thread per trip, every load issued before the arithmetic
+        for (uint32_t i = threadIdx.x; i < nq; i += (PAIR ? 2 : 1) * SF_TPB) {
+          const bool two = PAIR && i + SF_TPB < nq;
+          QuadCtx x0 = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          QuadCtx x1 = quad_ctx<ND>(A, tile, P, two ? i + SF_TPB : i, lq, chunked, jbase);
+          const bool ok0 = x0.off != SG_NO_BLOCK && x0.amask, ok1 = two && x1.off != SG_NO_BLOCK && x1.amask;
+          Q4<V> c0, c1, r0, r1;
+          NbrLoads<V, ND> L0, L1;
+          if (ok0) {
+            c0 = ld4<V>(P + s1 + x0.off);
+            if (jac) r0 = ld4<V>(P + s2 + x0.off);
+            nbr_load<V, ND>(A, tile, P, x0, s1, L0);
+          }
+          if (ok1) {
+            c1 = ld4<V>(P + s1 + x1.off);
+            if (jac) r1 = ld4<V>(P + s2 + x1.off);
+            nbr_load<V, ND>(A, tile, P, x1, s1, L1);
+          }
+          if (ok0) {
+            Q4<V> s = nbr_sum4<V, ND>(L0, c0);
+#pragma unroll
+            for (int k = 0; k < 4; k++) s.v[k] = jac ? (r0.v[k] + s.v[k]) * inv : s.v[k] - (V)(2 * ND) * c0.v[k];
+            st4<V>(P + s0 + x0.off, s, x0.amask);
+          }
+          if (ok1) {
+            Q4<V> s = nbr_sum4<V, ND>(L1, c1);
+#pragma unroll
+            for (int k = 0; k < 4; k++) s.v[k] = jac ? (r1.v[k] + s.v[k]) * inv : s.v[k] - (V)(2 * ND) * c1.v[k];
+            st4<V>(P + s0 + x1.off, s, x1.amask);
+          }
+        }
+      } break;
+      case SG_OP_REDUCE_SUM: {
+        V acc = V(0);
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || !x.amask) continue;
+          Q4<V> q = ld4<V>(P + s1 + x.off);
+#pragma unroll
+          for (int k = 0; k < 4; k++)
+            if ((x.amask >> k) & 1u) acc += q.v[k];
+        }
+        warp_add<V>(o, acc);
+      } break;
+      default: {
+        // per-lane ops (DOWNSAMPLE, JITTER, GRID_OP)
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK) continue;
+          for (int k = 0; k < 4; k++) {
+            if (!((x.amask >> k) & 1u)) continue;
+            CellCtx c;
+            c.T = &A.T; c.tile = &tile; c.P = P; c.e = x.e; c.j = x.j0 + k; c.fstride = fs;
+#pragma unroll
+            for (int a = 0; a < 3; a++) c.c[a] = tile.org[x.e][a] + x.r[a];
+            c.c[ND - 1] += k;
+            apply_cell<V>(A, op, c);
+          }
+        }
+      } break;
+    }
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void run_cells(const SFArgs& A, const SFTile& tile, uint32_t* P, uint32_t tcells,
+                                          bool chunked, uint32_t jbase, uint64_t fs) {
+  const DTree& T = A.T;
+  const int lblk = T.lblk;
+  for (int o = 0; o < A.nops; o++) {
+    const DOp& op = A.ops[o];
+    V acc = V(0);
+    for (uint32_t i = threadIdx.x; i < tcells; i += SF_TPB) {
+      CellCtx x;
+      x.T = &T;
+      x.tile = &tile;
+      x.P = P;
+      x.e = chunked ? 0 : (int)(i >> lblk);
+      x.j = chunked ? jbase + i : (i & ((1u << lblk) - 1u));
+      x.fstride = fs;
+      if (tile.blk[x.e] == SG_NO_BLOCK) continue;
+      if (T.leaf_bitmasked) {
+        uint32_t li = (tile.first[x.e] & 31u) + x.j;
+        if (!((P[tile.maskw[x.e] + (li >> 5)] >> (li & 31)) & 1u)) continue;
+      }
+      int bc[3];
+      inblock_coords(T, x.j, bc);
+      x.c[0] = tile.org[x.e][0] + bc[0];
+      x.c[1] = tile.org[x.e][1] + bc[1];
+      x.c[2] = tile.org[x.e][2] + bc[2];
+      acc += apply_cell<V>(A, op, x);
+    }
+    if (op.op == SG_OP_REDUCE_SUM) warp_add<V>(o, acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+// ND = 0: GENERIC cell path; 1..3: QUAD path.  PAIR: two stencil quads in
+// flight per thread (more registers, fewer resident CTAs).
+template <typename V, int ND, bool PAIR>
+__global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __grid_constant__ SFArgs A) {
+  __shared__ SFTile tile;
+  const DTree& T = A.T;
+  uint32_t* P = T.seg[T.nseg - 1].base;
+  if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
+  const uint32_t nent = A.entries ? *A.count : 1u;
+  const int lblk = T.lblk;
+  const bool chunked = lblk > A.ltile;
+  uint64_t ntiles;
+  uint32_t tiles_per_entry = 1;
+  if (chunked) {
+    tiles_per_entry = 1u << (lblk - A.ltile);
+    ntiles = (uint64_t)nent * tiles_per_entry;
+  } else {
+    ntiles = ((uint64_t)nent + (1u << A.lept) - 1) >> A.lept;
+  }
+  const uint64_t fs = 1ull << T.ln_leaf;
+
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint32_t e0, ne, jbase = 0, tcells;
+    if (chunked) {
+      e0 = (uint32_t)(t / tiles_per_entry);
+      ne = 1;
+      jbase = (uint32_t)(t % tiles_per_entry) << A.ltile;
+      tcells = 1u << A.ltile;
+    } else {
+      e0 = (uint32_t)(t << A.lept);
+      ne = min(1u << A.lept, nent - e0);
+      tcells = ne << lblk;
+    }
+    // the tile's blocks: one coalesced read of the list's block table
+    if (A.table) {
+      for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
+        const BlockRow r = A.table[e0 + i];
+        tile.blk[i] = r.blk;
+        tile.maskw[i] = r.maskw;
+        tile.first[i] = r.first;
+        tile.org[i][0] = r.org[0]; tile.org[i][1] = r.org[1]; tile.org[i][2] = r.org[2];
+#pragma unroll
+        for (int d = 0; d < 6; d++) tile.nbr[i][d] = r.nbr[d];
+      }
+    } else if (threadIdx.x == 0) {   // no driving level: the single root block
+      tile.blk[0] = (uint32_t)T.payload_off;
+      tile.maskw[0] = T.leaf_bitmasked ? T.lev[T.nlev - 1].mask_off : 0u;
+      tile.first[0] = 0;
+      tile.org[0][0] = tile.org[0][1] = tile.org[0][2] = 0;
+#pragma unroll
+      for (int d = 0; d < 6; d++) tile.nbr[0][d] = SG_NO_BLOCK;
+    }
+    __syncthreads();
+    if (ND > 0) run_quads<V, (ND > 0 ? ND : 1), PAIR>(A, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked, jbase, fs);
+    else run_cells<V>(A, tile, P, tcells, chunked, jbase, fs);
+    __syncthreads();
+  }
+  if (A.has_reduce) finish_reductions<V>(A);
+}

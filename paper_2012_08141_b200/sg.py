@@ -312,10 +312,13 @@ def replay(grid, prog, passes=None, device="cuda", upto=None, on_flush=None):
     flush's pass set when given.  Returns the list of per-flush stats."""
     import torch
     stats = []
-    arrays = {}
+    grid.tensors = {}
     for name, arr in prog.get("arrays", {}).items():
-        t = torch.as_tensor(arr).to(device).contiguous() if not grid.plan_only else arr
-        arrays[name] = grid.register_array(t, arr.shape[0]) if not grid.plan_only else len(arrays)
+        if grid.plan_only:
+            continue
+        t = torch.as_tensor(arr).to(device).contiguous()
+        grid.tensors[name] = t
+        grid.register_array(t, arr.shape[0])
     calls = prog["calls"] if upto is None else prog["calls"][:upto]
     for c in calls:
         k = c["call"]
@@ -357,7 +360,7 @@ _lib.sg_profile_read.argtypes = [_vp, _P(ctypes.c_double), _P(ctypes.c_int64), c
 _lib.sg_profile_read.restype = ctypes.c_int32
 EXPORTS += ["sg_set_profiling", "sg_profile_read"]
 
-PROFILE_KINDS = 128
+PROFILE_KINDS = 300
 
 
 def set_profiling(grid, on=True):

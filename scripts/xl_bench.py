@@ -1,0 +1,104 @@
+"""Roofline variants sized far above L2:
+
+  JAC-XL  1024^3, pointer(32^3) -> bitmasked(4^3) -> dense(8^3), block-ball R=288,
+          one JACOBI struct-for per launch (12 B algorithmic per active cell).
+  LG-XL   2048^3, pointer(64^3) -> bitmasked(32^3) leaf, 25% of pointer cells,
+          10% of their bits; one cell-level listgen of the leaf (reads the mask
+          words of every listed container + 4 B per parent entry, writes 4 B per
+          active cell + the count).
+
+Prints one JSON line per variant: achieved algorithmic GB/s per launch (CUDA
+events on the grid's stream around each launch, sg_profile_read) vs the HBM peak.
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import workloads as W  # noqa: E402
+from paper_2012_08141_b200 import sg  # noqa: E402
+
+
+def jac_xl(iters=10, radius=288.0):
+    L, lv = W.c2_layout(ptr=32)
+    f = L.fields
+    coords = W.block_ball_coords(128, 8, radius)
+    g = sg.Grid(L.desc())
+    dc = torch.as_tensor(coords).cuda()
+    calls, _ = W.c2_solve_calls(L, lv, coords, iters=0, reduce_result=False)
+    bench.enqueue_calls(g, calls, dc)
+    g.flush("all")
+    g.sync()
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sg.set_profiling(g, True)
+    src, dst = f["x0"], f["x1"]
+    for _ in range(iters):
+        flush_buf.zero_()
+        g.struct_for("JACOBI", lv[-1], [dst, src, f["b"]])
+        g.flush("all")
+        src, dst = dst, src
+    prof = sg.profile_read(g)
+    ms, n = prof[100 + sg.OPS["JACOBI"]]
+    nbytes = len(coords) * 512 * 12
+    peak, kind = bench.hbm_peak()
+    ach = nbytes / (ms / n / 1e3) / 1e9
+    return {"variant": "JAC-XL", "blocks": len(coords), "cells": len(coords) * 512, "bytes_per_launch": nbytes,
+            "avg_launch_us": ms / n * 1e3, "achieved_GBps": ach, "peak_GBps": peak, "peak_source": kind,
+            "frac": ach / peak, "launches": n}
+
+
+def lg_xl(reps=10, p_ptr=0.25, p_bit=0.10, seed=0):
+    L = W.Layout()
+    lv = L.chain([("pointer", (64,) * 3), ("bitmasked", (32,) * 3)], [("m", "f32")])
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    n_ptr = 64 ** 3
+    ptr_on = torch.randperm(n_ptr, device="cuda", generator=gen)[: int(n_ptr * p_ptr)]
+    n_act = ptr_on.numel()
+    g = sg.Grid(L.desc(), pool_capacity=n_act, list_capacity=int(n_act * 32768 * p_bit * 1.05) + 1024)
+    # 10% of the bits of each active container, activated in chunks
+    cells_per = int(32768 * p_bit)
+    total = 0
+    chunk = 4096
+    for s in range(0, n_act, chunk):
+        pc = ptr_on[s:s + chunk]
+        px, py, pz = pc // 4096, (pc // 64) % 64, pc % 64
+        loc = torch.randint(0, 32768, (pc.numel(), cells_per), device="cuda", generator=gen)
+        lx, ly, lz = loc // 1024, (loc // 32) % 32, loc % 32
+        co = torch.stack([(px[:, None] * 32 + lx), (py[:, None] * 32 + ly), (pz[:, None] * 32 + lz)], -1)
+        co = co.reshape(-1, 3).to(torch.int32).contiguous()
+        g.activate(0, co)
+        g.flush("all")
+        total += co.shape[0]
+    g.sync()
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sg.set_profiling(g, True)
+    for _ in range(reps):
+        flush_buf.zero_()
+        g.listgen(lv[-1])
+        g.flush("all")
+    prof = sg.profile_read(g)
+    g.sync()
+    ms, n = prof[200 + lv[-1]]
+    import ctypes
+    cnt = ctypes.c_int64()
+    sg._check(sg._lib.sg_export_list(g.h, lv[-1], None, 0, ctypes.byref(cnt)))
+    n_out = cnt.value
+    nbytes = n_act * 4 + n_act * 32768 // 8 + n_out * 4 + 4
+    peak, kind = bench.hbm_peak()
+    ach = nbytes / (ms / n / 1e3) / 1e9
+    return {"variant": "LG-XL", "containers": n_act, "active_cells": n_out, "activate_requests": total,
+            "bytes_per_launch": nbytes, "avg_launch_us": ms / n * 1e3, "achieved_GBps": ach, "peak_GBps": peak,
+            "peak_source": kind, "frac": ach / peak, "launches": n}
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["jac", "lg"]
+    if "jac" in which:
+        print(json.dumps(jac_xl()), flush=True)
+    if "lg" in which:
+        print(json.dumps(lg_xl()), flush=True)

@@ -1,0 +1,104 @@
+"""GPU parity of the MLS-MPM path (C3 shape) against the oracle (-m gpu).
+
+Small configs run full parity (every grid field and particle array, masks
+exact); the full 128^3 / 1M-particle config runs properties that hold at any
+size plus a single-step handoff (reading R17): the oracle's particle state is
+loaded into a fresh grid, one step runs on each side, results compared.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2012_08141_b200 import sg  # noqa: E402
+from test_gpu_parity import assert_field_close, as_set  # noqa: E402
+
+
+def gpu_run(prog, passes=None):
+    g = sg.Grid(prog["desc"])
+    stats = sg.replay(g, prog, passes=passes, device="cuda")
+    g.sync()
+    return g, g.tensors, stats
+
+
+def compare_mpm(g, arrs, o, prog, tol=1e-5):
+    L = prog["layout"]
+    for name, fid in L.fields.items():
+        want, mag = o.field(fid, with_mag=True)
+        got = g.field(fid).astype(np.float64)
+        bad = np.abs(got - want) > tol * np.maximum(np.abs(want), mag)
+        assert not bad.any(), f"grid {name}: {bad.sum()} off, worst {np.abs(got - want)[bad].max()}"
+    for s in range(1, len(L.rows)):
+        if L.rows[s][0] in (W.BITMASKED, W.POINTER):
+            assert as_set(g.mask(s)) == as_set(o.mask(s)), f"mask {s}"
+    for i, name in enumerate(prog["arrays"]):
+        want, mag = o.array(i, with_mag=True)
+        got = arrs[name].cpu().numpy().astype(np.float64)
+        bound = tol * np.maximum(np.abs(want), mag)
+        bad = np.abs(got - want) > bound
+        assert not bad.any(), f"array {name}: {bad.sum()} off, worst {np.abs(got - want)[bad].max()}"
+
+
+@pytest.mark.parametrize("passes", [0, "all"])
+def test_c3_small_one_step(passes):
+    prog = W.c3_program(n_grid=32, n_particles=4000, steps=1, seed=5, v_scale=1.0, J_jitter=0.02,
+                        lo=0.2, hi=0.7)
+    o = oracle.run_program(prog)
+    g, arrs, st = gpu_run(prog, passes)
+    compare_mpm(g, arrs, o, prog)
+    assert st[0]["tasks_lowered"] == 8
+
+
+def test_c3_small_multistep_window():
+    # 3 steps in one flush window: listgen removal across steps (G2P writes no mask).
+    # Per-step parity is test_c3_small_one_step; across steps the f32 rounding of
+    # one step feeds the next (reading R17), so the bound here is 1e-4 of M.
+    prog = W.c3_program(n_grid=32, n_particles=3000, steps=3, flush_every=3, seed=6, v_scale=0.5)
+    o = oracle.run_program(prog)
+    g, arrs, st = gpu_run(prog)
+    compare_mpm(g, arrs, o, prog, tol=1e-4)
+    assert st[0]["tasks_lowered"] == 24
+    assert st[0]["launches"] == 8 + 6 + 6
+
+
+def test_c3_full_size_properties_and_handoff():
+    n, ng = 1_000_000, 128
+    prog = W.c3_program(n_grid=ng, n_particles=n, steps=1, seed=0)
+    prm = W.mpm_params(ng)
+    g, arrs, st = gpu_run(prog)
+    L = prog["layout"]
+    f = L.fields
+    m = g.field(f["m"]).astype(np.float64)
+    np.testing.assert_allclose(m.sum(), n * prm["p_mass"], rtol=1e-4)
+    v = arrs["v"].cpu().numpy()
+    np.testing.assert_allclose(v[1], -prm["dt"] * prm["gravity"], rtol=1e-5)   # free fall from rest
+    assert np.abs(v[0]).max() < 1e-9 and np.abs(arrs["C"].cpu().numpy()).max() < 1e-4
+    # active blocks = exactly the blocks of the particles' 3x3x3 stencils
+    x = prog["arrays"]["x"]
+    X = (x * np.float32(prm["inv_dx"])).astype(np.float32)
+    base = np.floor((X - np.float32(0.5)).astype(np.float32)).astype(np.int64)
+    lo = base // 4
+    hi = (base + 2) // 4
+    blocks = set()
+    for dx in (0, 1):
+        for dy in (0, 1):
+            for dz in (0, 1):
+                sel = np.array([lo[0] + dx <= hi[0], lo[1] + dy <= hi[1], lo[2] + dz <= hi[2]]).all(0)
+                b = np.stack([lo[0] + dx, lo[1] + dy, lo[2] + dz], 1)[sel]
+                blocks.update(map(tuple, np.unique(b, axis=0).tolist()))
+    lv = [s for s in range(1, len(L.rows)) if L.rows[s][0] == W.BITMASKED][0]
+    assert as_set(g.mask(lv)) == sorted(blocks)
+    # single-step handoff on a 20k-particle subset (oracle cost bounded)
+    sub = {k: np.ascontiguousarray(a[:, :20000]) for k, a in prog["arrays"].items()}
+    sub["v"] = (np.random.default_rng(9).uniform(-1, 1, sub["v"].shape)).astype(np.float32)
+    p1 = W.c3_program(n_grid=ng, n_particles=20000, steps=1, seed=0)
+    p1["arrays"] = sub
+    o = oracle.run_program(p1)
+    g1, arrs1, _ = gpu_run(p1)
+    compare_mpm(g1, arrs1, o, p1)

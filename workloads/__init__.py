@@ -222,6 +222,58 @@ def c2_small_program(iters=6, passes="all"):
 
 
 # ----------------------------------------------------------------------------
+# C3: 3D sparse MLS-MPM (mpm3d-like), 128^3 grid, 1M particles.
+# pointer(n/16)^3 [16^3 cells each] -> bitmasked(4^3) [4^3] -> dense(4^3).
+# ----------------------------------------------------------------------------
+def c3_layout(n_grid=128):
+    L = Layout()
+    lv = L.chain([("pointer", (n_grid // 16,) * 3), ("bitmasked", (4,) * 3), ("dense", (4,) * 3)],
+                 [("vx", "f32"), ("vy", "f32"), ("vz", "f32"), ("m", "f32")])
+    return L, lv
+
+
+def mpm_params(n_grid=128, dt=1e-4, E=400.0, gravity=9.8, bound=3):
+    dx = 1.0 / n_grid
+    p_vol = (dx * 0.5) ** 3
+    p_rho = 1.0
+    return {"dt": dt, "inv_dx": float(n_grid), "p_mass": p_vol * p_rho, "p_vol": p_vol, "E": E,
+            "gravity": gravity, "bound": float(bound), "n_grid": float(n_grid)}
+
+
+def mpm_particles(n, lo=0.15, hi=0.55, seed=0, v_scale=0.0, J_jitter=0.0):
+    """SoA float32 arrays: x (3,n), v (3,n), C (9,n), J (1,n)."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(lo, hi, size=(3, n)).astype(np.float32)
+    v = (rng.uniform(-1, 1, size=(3, n)) * v_scale).astype(np.float32)
+    C = np.zeros((9, n), dtype=np.float32)
+    J = (1.0 + rng.uniform(-1, 1, size=(1, n)) * J_jitter).astype(np.float32)
+    return {"x": x, "v": v, "C": C, "J": J}
+
+
+def c3_step_calls(L, lv, n, prm):
+    f = L.fields
+    grid_f = [f["vx"], f["vy"], f["vz"], f["m"]]
+    return [deactivate(lv[0]),
+            range_for("P2G", n, grid_f, [0, 1, 2, 3],
+                      [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]], [True] * 4),
+            struct_for("GRID_OP", lv[-1], grid_f, [prm["dt"], prm["gravity"], prm["bound"], prm["n_grid"]]),
+            range_for("G2P", n, grid_f, [0, 1, 2, 3], [prm["dt"], prm["inv_dx"]])]
+
+
+def c3_program(n_grid=128, n_particles=1_000_000, steps=1, flush_every=1, seed=0, v_scale=0.0, J_jitter=0.0,
+               lo=0.15, hi=0.55, passes="all", **prm_kw):
+    L, lv = c3_layout(n_grid)
+    prm = mpm_params(n_grid, **prm_kw)
+    arrays = mpm_particles(n_particles, lo, hi, seed, v_scale, J_jitter)
+    calls = []
+    for s in range(steps):
+        calls += c3_step_calls(L, lv, n_particles, prm)
+        if (s + 1) % flush_every == 0 or s == steps - 1:
+            calls.append(flush(passes))
+    return program(L, calls, arrays=arrays, name="C3")
+
+
+# ----------------------------------------------------------------------------
 # Random integer programs (SPEC.md:386/454 fuzzer idea: seeded layouts of
 # depth <= 4, a handful of kernels, integer fields for exact comparison).
 # ----------------------------------------------------------------------------
