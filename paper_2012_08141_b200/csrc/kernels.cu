@@ -288,7 +288,7 @@ struct LGArgs {
   int task;
 };
 
-constexpr int LG_TPB = 256, LG_CPT = 4, LG_TILE = LG_TPB * LG_CPT;
+constexpr int LG_TPB = 256, LG_CPT = 4, LG_TILE = LG_TPB * LG_CPT, LG_STAGE = 4096;
 
 __device__ __forceinline__ uint32_t lg_chunk(const LGArgs& a, uint64_t chunk, uint32_t& cslot, uint32_t& first) {
   uint32_t p = (uint32_t)(chunk >> a.lcpp), sub = (uint32_t)(chunk & ((1u << a.lcpp) - 1u));
@@ -327,6 +327,7 @@ __device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint3
 __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGArgs a) {
   __shared__ uint32_t s_warp[LG_TPB / 32];
   __shared__ uint32_t s_tile, s_base, s_total, s_epoch;
+  __shared__ uint32_t s_stage[LG_STAGE];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_epoch = ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu;
   uint32_t nparent = a.mode == 0 ? 1u : ld_volatile(a.pcount);
@@ -366,25 +367,36 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
       if (lane < LG_TPB / 32) s_warp[lane] = wi - w;   // exclusive warp offsets
       uint32_t total = __shfl_sync(0xffffffffu, wi, LG_TPB / 32 - 1);
-      if (lane == 0) {
-        // single-pass decoupled look-back (deterministic order of tiles)
-        uint64_t* st = a.out.status;
-        uint32_t prefix = 0;
-        if (tile == 0) {
-          atomicExch((unsigned long long*)&st[0], (unsigned long long)lb_pack(epoch, 2u, total));
-        } else {
-          atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 1u, total));
-          int64_t j = (int64_t)tile - 1;
-          while (true) {
-            uint64_t s = ld_volatile64(&st[j]);
-            uint32_t ep = (uint32_t)(s >> 34), fl = (uint32_t)(s >> 32) & 3u;
-            if (ep != epoch || fl == 0u) { __nanosleep(8); continue; }
-            prefix += (uint32_t)s;
-            if (fl == 2u) break;
-            j--;
-          }
-          atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, prefix + total));
+      // single-pass decoupled look-back (deterministic tile order), one warp
+      // inspecting 32 predecessors per step
+      uint64_t* st = a.out.status;
+      if (lane == 0)
+        atomicExch((unsigned long long*)&st[tile],
+                   (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, total));
+      uint32_t prefix = 0;
+      int64_t j = (int64_t)tile - 1;
+      while (j >= 0) {
+        const int64_t q = j - lane;               // lane l inspects tile j-l
+        uint64_t s = 0;
+        uint32_t fl = 2u;                         // beyond tile 0: acts as an inclusive zero
+        if (q >= 0) {
+          do {
+            s = ld_volatile64(&st[q]);
+            fl = ((uint32_t)(s >> 34) == epoch) ? (uint32_t)(s >> 32) & 3u : 0u;
+          } while (fl == 0u);
         }
+        const uint32_t incl = __ballot_sync(0xffffffffu, fl == 2u);
+        const int stop = incl ? __ffs(incl) - 1 : 31;   // nearest inclusive predecessor
+        uint32_t v = (lane <= stop && q >= 0) ? (uint32_t)s : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (incl) break;
+        j -= 32;
+      }
+      if (lane == 0) {
+        if (tile != 0)
+          atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, prefix + total));
         s_base = prefix;
         s_total = total;
         if (tile == ntiles - 1) {
@@ -395,18 +407,29 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
     }
     __syncthreads();
-    uint32_t off = s_base + s_warp[warp] + (inc - cnt);
+    // stage the tile's entries in shared memory, then write them coalesced
+    const uint32_t base = s_base, total = s_total;
+    const uint32_t my0 = s_warp[warp] + (inc - cnt);
+    for (uint32_t r0 = 0; r0 < total; r0 += LG_STAGE) {
+      uint32_t off = my0;
 #pragma unroll
-    for (int k = 0; k < LG_CPT; k++) {
-      uint32_t b = bits[k];
-      while (b) {
-        int t = __ffs(b) - 1;
-        b &= b - 1;
-        if (off < a.out.capacity) a.out.entries[off] = (cs[k] << lnS) | (fs[k] + (uint32_t)t);
-        off++;
+      for (int k = 0; k < LG_CPT; k++) {
+        uint32_t b = bits[k];
+        while (b) {
+          int t = __ffs(b) - 1;
+          b &= b - 1;
+          if (off >= r0 && off < r0 + LG_STAGE) s_stage[off - r0] = (cs[k] << lnS) | (fs[k] + (uint32_t)t);
+          off++;
+        }
       }
+      __syncthreads();
+      const uint32_t n = min(total - r0, (uint32_t)LG_STAGE);
+      for (uint32_t i = threadIdx.x; i < n; i += LG_TPB) {
+        uint32_t dst = base + r0 + i;
+        if (dst < a.out.capacity) a.out.entries[dst] = s_stage[i];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (a.out.table) {
       // block table of the driving level: one row per entry of this tile, all threads
       const uint32_t end = min(s_base + s_total, a.out.capacity);
@@ -710,7 +733,9 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   cudaStream_t s = (cudaStream_t)stream;
   const int nd = quad ? t.nd : 0;
   static int pair = -1;
-  if (pair < 0) { const char* e = getenv("SG_SF_PAIR"); pair = e ? atoi(e) != 0 : 1; }
+  // measured on B200 (profiles/r01_*): one quad per thread at 6 CTAs/SM beats
+  // two quads per thread at 3 CTAs/SM (JAC-XL 2.84 vs 1.75 TB/s)
+  if (pair < 0) { const char* e = getenv("SG_SF_PAIR"); pair = e ? atoi(e) != 0 : 0; }
   const bool stencil = a->need_nbr;
 #define SG_SF_LAUNCH(V)                                                                     \
   switch (nd) {                                                                             \
