@@ -100,6 +100,11 @@ sg_status sg_destroy(sg_grid* g);
 /* Registers an external SoA particle array (ncomp components of n elements,
  * component c at dev_ptr + c*n) as a Value state usable by range-for ops. */
 sg_status sg_register_array(sg_grid* g, void* dev_ptr, int64_t n, int32_t dtype, int32_t ncomp, int32_t* id);
+/* Gives array `id` a device-resident element count (int32 at dev_count,
+ * borrowed; <= the registered n, which becomes the capacity).  Range-for tasks
+ * with range_n < 0 iterate [0, *dev_count of arrays[0]) read on the device, and
+ * the migration / halo ops (below) update it on the device. */
+sg_status sg_set_array_count(sg_grid* g, int32_t id, int32_t* dev_count);
 
 /* --- task vocabulary --------------------------------------------------------- */
 enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
@@ -117,12 +122,23 @@ enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
  *   JITTER      struct-for  f0[c] += f0[c+e0] for even c0      deep_hierarchy
  *   CLEAR_SCALAR serial     f0[] = 0
  *   P2G / GRID_OP / G2P     MLS-MPM transfer ops
+ *   ARRAY_COUNT  serial     *count(a0) = p0
+ *   HALO_PACK    struct-for blocks with origin x in [p0, p1) appended to buffer a0
+ *                           (record: 4-word header {org0,org1,org2,0} + f0..f(nf-1) payload;
+ *                           p2 = capacity in records; count = a0's device count)
+ *   HALO_UNPACK  range-for  n = capacity*cells-per-block: record cells of a0 added
+ *                           (p0 = 0) or stored (p0 = 1) into f0..; activating
+ *   G2P_MIGRATE  range-for  G2P over a0..a3 (x,v,C,J) + a4 (id) with device count, then
+ *                           stable in-place compaction of the particles whose cell x stays
+ *                           in [p2, p3); leavers appended to a5 (x < p2) / a6 (x >= p3)
+ *   MIGRATE_APPEND range-for particles of buffers a5, a6 appended to a0..a4
  * Inactive or out-of-bound reads give 0. */
 enum {
   SG_OP_FILL = 1, SG_OP_ADD_CONST = 2, SG_OP_INC = 3, SG_OP_AXPY = 4, SG_OP_STENCIL = 5,
   SG_OP_JACOBI = 6, SG_OP_REDUCE_SUM = 7, SG_OP_DOWNSAMPLE = 8, SG_OP_JITTER = 9,
-  SG_OP_CLEAR_SCALAR = 10,
-  SG_OP_P2G = 20, SG_OP_GRID_OP = 21, SG_OP_G2P = 22
+  SG_OP_CLEAR_SCALAR = 10, SG_OP_ARRAY_COUNT = 11,
+  SG_OP_P2G = 20, SG_OP_GRID_OP = 21, SG_OP_G2P = 22,
+  SG_OP_HALO_PACK = 23, SG_OP_HALO_UNPACK = 24, SG_OP_G2P_MIGRATE = 25, SG_OP_MIGRATE_APPEND = 26
 };
 
 typedef struct {

@@ -288,7 +288,7 @@ struct LGArgs {
   int task;
 };
 
-constexpr int LG_TPB = 256, LG_CPT = 4, LG_TILE = LG_TPB * LG_CPT, LG_STAGE = 4096;
+constexpr int LG_TPB = 256, LG_CPT = 8, LG_TILE = LG_TPB * LG_CPT, LG_STAGE = 8192;
 
 __device__ __forceinline__ uint32_t lg_chunk(const LGArgs& a, uint64_t chunk, uint32_t& cslot, uint32_t& first) {
   uint32_t p = (uint32_t)(chunk >> a.lcpp), sub = (uint32_t)(chunk & ((1u << a.lcpp) - 1u));
@@ -367,12 +367,35 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
       if (lane < LG_TPB / 32) s_warp[lane] = wi - w;   // exclusive warp offsets
       uint32_t total = __shfl_sync(0xffffffffu, wi, LG_TPB / 32 - 1);
+      if (lane == 0) {
+        s_total = total;
+        // publish the aggregate now, so successors can look back while we stage
+        atomicExch((unsigned long long*)&a.out.status[tile],
+                   (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, total));
+      }
+    }
+    __syncthreads();
+    // stage the tile's first LG_STAGE entries in shared memory (tile-local
+    // offsets need no prefix) while warp 0 runs the look-back
+    const uint32_t my0 = s_warp[warp] + (inc - cnt);
+    {
+      uint32_t off = my0;
+#pragma unroll
+      for (int k = 0; k < LG_CPT; k++) {
+        uint32_t b = bits[k];
+        while (b) {
+          int t = __ffs(b) - 1;
+          b &= b - 1;
+          if (off < LG_STAGE) s_stage[off] = (cs[k] << lnS) | (fs[k] + (uint32_t)t);
+          off++;
+        }
+      }
+    }
+    if (warp == 0) {
+      const uint32_t total = s_total;
       // single-pass decoupled look-back (deterministic tile order), one warp
       // inspecting 32 predecessors per step
       uint64_t* st = a.out.status;
-      if (lane == 0)
-        atomicExch((unsigned long long*)&st[tile],
-                   (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, total));
       uint32_t prefix = 0;
       int64_t j = (int64_t)tile - 1;
       while (j >= 0) {
@@ -398,7 +421,6 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
         if (tile != 0)
           atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, prefix + total));
         s_base = prefix;
-        s_total = total;
         if (tile == ntiles - 1) {
           uint32_t n = prefix + total;
           if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
@@ -407,22 +429,23 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
     }
     __syncthreads();
-    // stage the tile's entries in shared memory, then write them coalesced
+    // coalesced copy of the staged entries; dense tiles take further rounds
     const uint32_t base = s_base, total = s_total;
-    const uint32_t my0 = s_warp[warp] + (inc - cnt);
     for (uint32_t r0 = 0; r0 < total; r0 += LG_STAGE) {
-      uint32_t off = my0;
+      if (r0 > 0) {
+        uint32_t off = my0;
 #pragma unroll
-      for (int k = 0; k < LG_CPT; k++) {
-        uint32_t b = bits[k];
-        while (b) {
-          int t = __ffs(b) - 1;
-          b &= b - 1;
-          if (off >= r0 && off < r0 + LG_STAGE) s_stage[off - r0] = (cs[k] << lnS) | (fs[k] + (uint32_t)t);
-          off++;
+        for (int k = 0; k < LG_CPT; k++) {
+          uint32_t b = bits[k];
+          while (b) {
+            int t = __ffs(b) - 1;
+            b &= b - 1;
+            if (off >= r0 && off < r0 + LG_STAGE) s_stage[off - r0] = (cs[k] << lnS) | (fs[k] + (uint32_t)t);
+            off++;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
       const uint32_t n = min(total - r0, (uint32_t)LG_STAGE);
       for (uint32_t i = threadIdx.x; i < n; i += LG_TPB) {
         uint32_t dst = base + r0 + i;
@@ -454,6 +477,7 @@ __global__ void k_clear_list(uint32_t* count) { *count = 0; }
 
 #include "mpm_ops.cuh"
 #include "struct_for.cuh"
+#include "exchange_ops.cuh"
 
 // ---------------------------------------------------------------------------
 // Serial and range-for
@@ -468,24 +492,28 @@ struct SerArgs {
 __global__ void k_serial(const __grid_constant__ SerArgs A) {
   for (int o = 0; o < A.nops; o++) {
     if (A.ops[o].op == SG_OP_CLEAR_SCALAR) *(uint32_t*)A.aux[o] = 0u;
+    if (A.ops[o].op == SG_OP_ARRAY_COUNT) *A.C.arrays[A.ops[o].a[0]].dcount = (int32_t)A.ops[o].p[0];
   }
 }
 
 struct RFArgs {
   DevCtx C;
   int64_t n;
+  const int32_t* dcount;   // device extent (range_n < 0), else null
   int nops;
   int task;
   DOp ops[SG_MAXOPS];
 };
 
 __global__ void __launch_bounds__(128) k_range_for(const __grid_constant__ RFArgs A) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n = A.dcount ? (int64_t)*A.dcount : A.n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     for (int o = 0; o < A.nops; o++) {
       const DOp& op = A.ops[o];
       switch (op.op) {
         case SG_OP_P2G: mpm_p2g(A.C, op, i, A.task); break;
         case SG_OP_G2P: mpm_g2p(A.C, op, i); break;
+        case SG_OP_HALO_UNPACK: halo_unpack(A.C, op, i, A.task); break;
         default: break;
       }
     }
@@ -737,14 +765,21 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   // two quads per thread at 3 CTAs/SM (JAC-XL 2.84 vs 1.75 TB/s)
   if (pair < 0) { const char* e = getenv("SG_SF_PAIR"); pair = e ? atoi(e) != 0 : 0; }
   const bool stencil = a->need_nbr;
+  // constant-geometry instantiations for the block shapes of the configs
+  int gl = 0;
+  if (nd == 3 && a->lb[0] == 3 && a->lb[1] == 3 && a->lb[2] == 3) gl = 1;
+  else if (nd == 3 && a->lb[0] == 2 && a->lb[1] == 2 && a->lb[2] == 2) gl = 2;
+  else if (nd == 2 && a->lb[0] == 2 && a->lb[1] == 2) gl = 3;
 #define SG_SF_LAUNCH(V)                                                                     \
-  switch (nd) {                                                                             \
-    case 1: k_struct_for<V, 1, false><<<grid, SF_TPB, 0, s>>>(*a); break;                   \
-    case 2: if (pair && stencil) k_struct_for<V, 2, true><<<grid, SF_TPB, 0, s>>>(*a);       \
-            else k_struct_for<V, 2, false><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    case 3: if (pair && stencil) k_struct_for<V, 3, true><<<grid, SF_TPB, 0, s>>>(*a);       \
-            else k_struct_for<V, 3, false><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    default: k_struct_for<V, 0, false><<<grid, SF_TPB, 0, s>>>(*a); break;                  \
+  switch (nd * 10 + gl) {                                                                   \
+    case 10: k_struct_for<V, 1, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    case 20: k_struct_for<V, 2, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    case 23: k_struct_for<V, 2, false, 3><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    case 30: if (pair && stencil) k_struct_for<V, 3, true, 0><<<grid, SF_TPB, 0, s>>>(*a);   \
+             else k_struct_for<V, 3, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;           \
+    case 31: k_struct_for<V, 3, false, 1><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    case 32: k_struct_for<V, 3, false, 2><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+    default: k_struct_for<V, 0, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;               \
   }
   if (i32) { SG_SF_LAUNCH(int) } else { SG_SF_LAUNCH(float) }
 #undef SG_SF_LAUNCH
@@ -752,13 +787,29 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   return check_launch();
 }
 
-int launch_range_for(const DevCtx& c, int64_t n, const DOp* ops, int nops, int task, void* stream) {
+int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task,
+                     void* stream, const RangeScratch* rs) {
   if (n <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nops == 1 && ops[0].op == SG_OP_G2P_MIGRATE) {
+    MigArgs m;
+    m.C = c; m.op = ops[0]; m.status = rs->status; m.ctl = rs->ctl; m.task = task;
+    int grid = (int)std::min<int64_t>((n + MG_TPB - 1) / MG_TPB, (int64_t)num_sms() * 6);
+    k_g2p_migrate<<<std::max(grid, 1), MG_TPB, 0, s>>>(m);
+    return check_launch();
+  }
+  if (nops == 1 && ops[0].op == SG_OP_MIGRATE_APPEND) {
+    AppArgs m;
+    m.C = c; m.op = ops[0]; m.ctl = rs->ctl + 4;
+    int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 4);
+    k_migrate_append<<<std::max(grid, 1), 256, 0, s>>>(m);
+    return check_launch();
+  }
   RFArgs* a = new RFArgs();
-  a->C = c; a->n = n; a->nops = nops; a->task = task;
+  a->C = c; a->n = n; a->dcount = dcount; a->nops = nops; a->task = task;
   for (int o = 0; o < nops; o++) a->ops[o] = ops[o];
   int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms() * 16);
-  k_range_for<<<grid, 128, 0, (cudaStream_t)stream>>>(*a);
+  k_range_for<<<grid, 128, 0, s>>>(*a);
   delete a;
   return check_launch();
 }

@@ -86,6 +86,24 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
       for (int i = 0; i < 3; i++) F(i, R_READ, AC_DATA);
       A(0, R_RW, AC_ID); A(1, R_WRITE, AC_ID, true); A(2, R_WRITE, AC_ID, true); A(3, R_RW, AC_ID);
       break;
+    case SG_OP_ARRAY_COUNT: A(0, R_WRITE, AC_CONST); break;
+    case SG_OP_HALO_PACK:
+      for (int i = 0; i < 8 && t.fields[i] >= 0; i++) F(i, R_READ, AC_ID);
+      A(0, R_RW, AC_DATA);
+      break;
+    case SG_OP_HALO_UNPACK:
+      A(0, R_READ, AC_DATA);
+      for (int i = 0; i < 8 && t.fields[i] >= 0; i++) F(i, R_RW, AC_DATA);
+      break;
+    case SG_OP_G2P_MIGRATE:
+      for (int i = 0; i < 3; i++) F(i, R_READ, AC_DATA);
+      for (int i = 0; i < 5; i++) A(i, R_RW, AC_DATA);     // compaction moves particles
+      A(5, R_RW, AC_DATA); A(6, R_RW, AC_DATA);
+      break;
+    case SG_OP_MIGRATE_APPEND:
+      for (int i = 0; i < 5; i++) A(i, R_RW, AC_DATA);
+      A(5, R_READ, AC_DATA); A(6, R_READ, AC_DATA);
+      break;
     default: break;
   }
   return u;
@@ -96,7 +114,9 @@ static int op_min_fields(int op) {
     case SG_OP_FILL: case SG_OP_INC: case SG_OP_JITTER: case SG_OP_CLEAR_SCALAR: case SG_OP_DOWNSAMPLE: return 1;
     case SG_OP_ADD_CONST: case SG_OP_STENCIL: case SG_OP_REDUCE_SUM: return 2;
     case SG_OP_AXPY: case SG_OP_JACOBI: return 3;
-    case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: return 4;
+    case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: case SG_OP_G2P_MIGRATE: return 4;
+    case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: return 0;
+    case SG_OP_HALO_PACK: case SG_OP_HALO_UNPACK: return 1;
     default: return -1;
   }
 }
@@ -203,11 +223,38 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
     if (!valid_field(L, t.fields[i])) { err = "missing or bad field operand"; return SG_ERR_ARG; }
   }
   const bool sf = t.kind == SG_TASK_STRUCT_FOR;
+  if (t.kind == SG_TASK_RANGE_FOR && t.range_n < 0 && t.arrays[0] < 0) {
+    err = "range_n < 0 needs arrays[0] with a device count"; return SG_ERR_ARG;
+  }
+  switch (t.op) {
+    case SG_OP_ARRAY_COUNT:
+      if (t.kind != SG_TASK_SERIAL || t.arrays[0] < 0) { err = "ARRAY_COUNT is a serial op on arrays[0]"; return SG_ERR_ARG; }
+      return SG_OK;
+    case SG_OP_MIGRATE_APPEND:
+    case SG_OP_HALO_UNPACK:
+    case SG_OP_G2P_MIGRATE:
+      if (t.kind != SG_TASK_RANGE_FOR) { err = "migration / unpack ops are range-for ops"; return SG_ERR_ARG; }
+      for (int i = 0; i < (t.op == SG_OP_HALO_UNPACK ? 1 : 7); i++)
+        if (t.arrays[i] < 0) { err = "missing array operand"; return SG_ERR_ARG; }
+      if (t.op == SG_OP_HALO_UNPACK) {
+        int tree = L.field_tree[t.fields[0]];
+        if (tree < 0 || L.trees[tree].driving < 0) { err = "HALO_UNPACK fields must live in a sparse tree"; return SG_ERR_ARG; }
+        for (int i = 0; i < 8 && t.fields[i] >= 0; i++)
+          if (!valid_field(L, t.fields[i]) || L.field_tree[t.fields[i]] != tree) { err = "HALO_UNPACK fields must share a tree"; return SG_ERR_ARG; }
+        return SG_OK;
+      }
+      if (t.op == SG_OP_MIGRATE_APPEND) return SG_OK;
+      break;   // G2P_MIGRATE: grid checks below
+    case SG_OP_HALO_PACK:
+      if (!sf || t.arrays[0] < 0) { err = "HALO_PACK is a struct-for op with a buffer in arrays[0]"; return SG_ERR_ARG; }
+      break;
+    default: break;
+  }
   if (t.op == SG_OP_CLEAR_SCALAR) {
     if (t.kind != SG_TASK_SERIAL || L.field_tree[t.fields[0]] >= 0) { err = "CLEAR_SCALAR is a serial op on a 0-D field"; return SG_ERR_ARG; }
     return SG_OK;
   }
-  if (t.op == SG_OP_P2G || t.op == SG_OP_G2P || t.op == SG_OP_GRID_OP) {
+  if (t.op == SG_OP_P2G || t.op == SG_OP_G2P || t.op == SG_OP_GRID_OP || t.op == SG_OP_G2P_MIGRATE) {
     if (t.op != SG_OP_GRID_OP && t.kind != SG_TASK_RANGE_FOR) { err = "P2G/G2P are range-for ops"; return SG_ERR_ARG; }
     int tree = L.field_tree[t.fields[0]];
     if (tree < 0 || L.trees[tree].nd != 3 || L.trees[tree].driving < 0) {
@@ -552,7 +599,13 @@ static bool pass_fusion(const HLayout& L, std::vector<PTask>& seq, PlanStats& st
           }
           if (!ok) continue;
         } else if (A.type == TT_RANGE_FOR) {
-          if (A.n != B.n) continue;
+          // same range: equal host extent, or the same device-counted array
+          if (A.n != B.n || (A.n < 0 && A.t.arrays[0] != B.t.arrays[0])) continue;
+          // ops with their own kernels (scan / append / unpack) run alone
+          auto solo = [](int op) {
+            return op == SG_OP_G2P_MIGRATE || op == SG_OP_MIGRATE_APPEND || op == SG_OP_HALO_UNPACK;
+          };
+          if (solo(A.t.op) || solo(B.t.op)) continue;
         }
         // no path of length >= 2
         bool long_path = false;

@@ -50,6 +50,9 @@ struct sg_grid {
   std::vector<PlanRecord> last_plan;
   int64_t task_counter = 0;
   int num_sms = 148;
+  uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
+  uint64_t mig_tiles = 0;
+  uint32_t* mig_ctl = nullptr;
   // launch profiling (benchmarks): event pairs per launch group
   bool profiling = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -413,11 +416,19 @@ extern "C" sg_status sg_destroy(sg_grid* g) {
 extern "C" sg_status sg_register_array(sg_grid* g, void* ptr, int64_t n, int32_t dtype, int32_t ncomp, int32_t* id) {
   if (!g || !id || n < 0 || ncomp < 1) return fail(SG_ERR_ARG, "bad array");
   if ((int)g->arrays.size() >= g->d_arrays_cap && !g->plan_only) return fail(SG_ERR_ARG, "too many arrays");
-  DArray a{ptr, n, ncomp, dtype};
+  DArray a{ptr, n, ncomp, dtype, nullptr};
   g->arrays.push_back(a);
   *id = (int32_t)g->arrays.size() - 1;
   if (!g->plan_only)
     CUDA_TRY(cudaMemcpyAsync(g->d_arrays + *id, &a, sizeof(DArray), cudaMemcpyHostToDevice, g->stream));
+  return SG_OK;
+}
+
+extern "C" sg_status sg_set_array_count(sg_grid* g, int32_t id, int32_t* dev_count) {
+  if (!g || id < 0 || id >= (int)g->arrays.size()) return fail(SG_ERR_ARG, "bad array id");
+  g->arrays[id].dcount = dev_count;
+  if (!g->plan_only)
+    CUDA_TRY(cudaMemcpyAsync(g->d_arrays + id, &g->arrays[id], sizeof(DArray), cudaMemcpyHostToDevice, g->stream));
   return SG_OK;
 }
 
@@ -521,8 +532,11 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       if ((rc = alloc_list(g, t0.tree, k))) return rc;
       int pk = parent_pos(T, k);
       const DList* parent = pk >= 0 ? &g->lists[t0.tree][pk] : nullptr;
-      uint64_t ptiles = parent ? ((uint64_t)parent->capacity * (1ull << std::max(0, (pk >= 0 && T.lev[pk].seg == T.lev[k].seg ? T.lev[k].ln - T.lev[pk].ln : T.lev[k].ln) - 5)) + 1023) / 1024 : 1;
-      int hint = (int)std::min<uint64_t>(ptiles, (uint64_t)g->num_sms * 4);
+      // upper bound on the listgen's tiles: parent entries x 32-child chunks / tile
+      const int lratio = pk >= 0 && T.lev[pk].seg == T.lev[k].seg ? T.lev[k].ln - T.lev[pk].ln : T.lev[k].ln;
+      const uint64_t pcap = parent ? parent->capacity : 1;
+      const uint64_t ptiles = (pcap * (1ull << std::max(0, lratio - 5)) + 1023) / 1024;
+      int hint = (int)std::max<uint64_t>(1, std::min<uint64_t>(ptiles, (uint64_t)g->num_sms * 4));
       rc = launch_listgen(g->ctx, T, t0.tree, k, pk, parent, g->lists[t0.tree][k], task, g->stream, hint);
       st.listgen_launched++;
     } break;
@@ -544,7 +558,48 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       DOp ops[SG_MAXOPS];
       int nops = (int)members.size();
       for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], -1, ops[i]);
-      rc = launch_range_for(g->ctx, t0.n, ops, nops, task, g->stream);
+      const sg_task& tk = t0.t;
+      auto arr = [&](int slot) -> const DArray* {
+        int id = tk.arrays[slot];
+        return id >= 0 && id < (int)g->arrays.size() ? &g->arrays[id] : nullptr;
+      };
+      for (int s = 0; s < 8; s++)
+        if (tk.arrays[s] >= (int)g->arrays.size()) return fail(SG_ERR_ARG, "array id not registered");
+      int64_t n = t0.n;
+      const int32_t* dcount = nullptr;
+      if (tk.op == SG_OP_HALO_UNPACK) {
+        const DTree& T = g->dtrees[g->L.field_tree[tk.fields[0]]];
+        int nf = 0;
+        while (nf < 8 && tk.fields[nf] >= 0) nf++;
+        int64_t rec = 4 + ((int64_t)nf << T.lblk);
+        n = (arr(0)->n / rec) << T.lblk;
+        if (!arr(0)->dcount) return fail(SG_ERR_ARG, "HALO_UNPACK buffer needs a device count");
+      } else if (tk.op == SG_OP_MIGRATE_APPEND) {
+        n = (arr(5)->n + arr(6)->n) / 17;
+      } else if (n < 0) {
+        const DArray* a0 = arr(0);
+        if (!a0 || !a0->dcount) return fail(SG_ERR_ARG, "range_n < 0 needs arrays[0] with a device count");
+        n = a0->n;
+        dcount = a0->dcount;
+      }
+      if (tk.op == SG_OP_G2P_MIGRATE || tk.op == SG_OP_MIGRATE_APPEND) {
+        for (int s = 0; s < 7; s++)
+          if (!arr(s) || ((s == 0 || s >= 5) && !arr(s)->dcount)) return fail(SG_ERR_ARG, "migration arrays need device counts");
+        uint64_t tiles = (uint64_t)n / 256 + 2;
+        if (tiles > g->mig_tiles) {
+          g->mig_status = (uint64_t*)g->dev_alloc(tiles * 8);
+          if (!g->mig_status) return fail(SG_ERR_CUDA, "migration scratch allocation failed");
+          CUDA_TRY(cudaMemsetAsync(g->mig_status, 0, tiles * 8, g->stream));
+          g->mig_tiles = tiles;
+        }
+        if (!g->mig_ctl) {
+          g->mig_ctl = (uint32_t*)g->dev_alloc(64);
+          if (!g->mig_ctl) return fail(SG_ERR_CUDA, "migration scratch allocation failed");
+          CUDA_TRY(cudaMemsetAsync(g->mig_ctl, 0, 64, g->stream));
+        }
+      }
+      RangeScratch rs{g->mig_status, g->mig_ctl};
+      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs);
     } break;
     case TT_SERIAL: {
       DOp ops[SG_MAXOPS];

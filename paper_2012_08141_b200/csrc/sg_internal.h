@@ -75,8 +75,9 @@ struct DField {
 
 struct DArray {
   void* ptr;
-  int64_t n;
+  int64_t n;            // capacity (elements per component)
   int32_t ncomp, dtype;
+  int32_t* dcount;      // device-side element count, or null (= n)
 };
 
 // Per-entry block table written by the listgen of a tree's driving level: the
@@ -145,7 +146,12 @@ int launch_listgen(const DevCtx& c, const DTree& t, int tree_id, int level, int 
 int launch_clear_list(const DList& l, void* stream);
 int launch_struct_for(const DevCtx& c, const DTree& t, int tree_id, const DList* drive, const DOp* ops, int nops,
                       int task_id, void* stream, int grid_hint);
-int launch_range_for(const DevCtx& c, int64_t n, const DOp* ops, int nops, int task_id, void* stream);
+struct RangeScratch {
+  uint64_t* status;   // look-back descriptors for G2P_MIGRATE tiles
+  uint32_t* ctl;      // [0..3] migrate tile/done/epoch/count, [5] append ticket
+};
+int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task_id,
+                     void* stream, const RangeScratch* rs);
 int launch_serial(const DevCtx& c, const DOp* ops, int nops, int task_id, void* stream);
 int launch_deactivate(const DevCtx& c, const DTree& t, int tree_id, int level, const DList* lists,
                       int task_id, void* stream);

@@ -50,7 +50,29 @@ struct SFTile {
   uint32_t first[SF_MAXE];
   int org[SF_MAXE][3];
   uint32_t nbr[SF_MAXE][6];
+  int32_t slot[SF_MAXE];      // HALO_PACK: record slot of each block, -1 = not packed
+  uint32_t ne;
 };
+
+// HALO_PACK, per-tile part: blocks whose origin x lies in [p0, p1) get a record
+// slot (a0's device count) and their header; the payload is copied per cell.
+__device__ __forceinline__ void halo_pack_slots(const DevCtx& C, const DOp& op, SFTile& tile, int task) {
+  __syncthreads();
+  const DArray& B = C.arrays[op.a[0]];
+  for (uint32_t e = threadIdx.x; e < tile.ne; e += blockDim.x) {
+    int32_t s = -1;
+    if (tile.blk[e] != SG_NO_BLOCK && (float)tile.org[e][0] >= op.p[0] && (float)tile.org[e][0] < op.p[1]) {
+      s = atomicAdd(B.dcount, 1);
+      if (s >= (int32_t)op.p[2]) { set_err(C, SG_ERR_LIST_OVERFLOW, task); s = -1; }
+    }
+    tile.slot[e] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t* halo_rec(const DevCtx& C, const DOp& op, int32_t slot, uint32_t lblk, int nf) {
+  return (uint32_t*)C.arrays[op.a[0]].ptr + (uint64_t)slot * (4 + ((uint64_t)nf << lblk));
+}
 
 template <typename V> __device__ __forceinline__ V ldv(const uint32_t* p);
 template <> __device__ __forceinline__ float ldv<float>(const uint32_t* p) { return __uint_as_float(*p); }
@@ -245,9 +267,25 @@ struct QuadCtx {
   uint32_t amask;          // active lanes
 };
 
+// Block geometry of the QUAD path: log2 extents per axis.  Built once per
+// kernel from template constants (common shapes) or the launch parameters.
+struct QG {
+  int lb[3];
+};
+
+template <int GL>
+__device__ __forceinline__ QG make_qg(const SFArgs& A) {
+  QG g;
+  if (GL == 1) { g.lb[0] = 3; g.lb[1] = 3; g.lb[2] = 3; }        // 8^3 (C2, JAC-XL)
+  else if (GL == 2) { g.lb[0] = 2; g.lb[1] = 2; g.lb[2] = 2; }   // 4^3 (C3, C5)
+  else if (GL == 3) { g.lb[0] = 2; g.lb[1] = 2; g.lb[2] = 0; }   // 4x4 (C1)
+  else { g.lb[0] = A.lb[0]; g.lb[1] = A.lb[1]; g.lb[2] = A.lb[2]; }
+  return g;
+}
+
 template <int ND>
-__device__ __forceinline__ QuadCtx quad_ctx(const SFArgs& A, const SFTile& tile, const uint32_t* P, uint32_t i,
-                                            uint32_t lq, bool chunked, uint32_t jbase) {
+__device__ __forceinline__ QuadCtx quad_ctx(const SFArgs& A, const QG& g, const SFTile& tile, const uint32_t* P,
+                                            uint32_t i, uint32_t lq, bool chunked, uint32_t jbase) {
   QuadCtx x;
   x.e = chunked ? 0 : (int)(i >> lq);
   x.j0 = chunked ? jbase + 4 * i : 4 * (i & ((1u << lq) - 1u));
@@ -258,14 +296,15 @@ __device__ __forceinline__ QuadCtx quad_ctx(const SFArgs& A, const SFTile& tile,
     uint32_t li = (tile.first[x.e] & 31u) + x.j0;
     x.amask = (P[tile.maskw[x.e] + (li >> 5)] >> (li & 31)) & 0xFu;
   }
-  const int lb1 = ND > 1 ? A.lb[1] : 0, lb2 = ND > 2 ? A.lb[2] : 0;
+  const int lb1 = ND > 1 ? g.lb[1] : 0, lb2 = ND > 2 ? g.lb[2] : 0;
   x.r[0] = (int)(x.j0 >> (lb1 + lb2));
   x.r[1] = ND > 1 ? (int)((x.j0 >> lb2) & ((1u << lb1) - 1u)) : 0;
   x.r[2] = ND > 2 ? (int)(x.j0 & ((1u << lb2) - 1u)) : 0;
   return x;
 }
 
-// Gathers the 2*ND face-neighbour values of a quad (loads only).
+// Gathers the 2*ND face-neighbour values of a quad (loads only, branch-free
+// address selection: in-block row, neighbour block row, or absent).
 template <typename V, int ND>
 struct NbrLoads {
   Q4<V> row[2 * (ND - 1) + 1];   // neighbour rows along the slower axes
@@ -273,32 +312,32 @@ struct NbrLoads {
 };
 
 template <typename V, int ND>
-__device__ __forceinline__ void nbr_load(const SFArgs& A, const SFTile& tile, const uint32_t* P, const QuadCtx& x,
+__device__ __forceinline__ void nbr_load(const QG& g, const SFTile& tile, const uint32_t* P, const QuadCtx& x,
                                          uint64_t so, NbrLoads<V, ND>& L) {
   constexpr int f = ND - 1;
-  const int Bf = 1 << A.lb[f];
-  L.lo = V(0);
-  L.hi = V(0);
-  if (x.r[f] > 0) L.lo = ldv<V>(P + so + x.off - 1);
-  else if (tile.nbr[x.e][2 * f] != SG_NO_BLOCK) L.lo = ldv<V>(P + so + tile.nbr[x.e][2 * f] + x.j0 + (Bf - 1));
-  if (x.r[f] + 4 < Bf) L.hi = ldv<V>(P + so + x.off + 4);
-  else if (tile.nbr[x.e][2 * f + 1] != SG_NO_BLOCK) L.hi = ldv<V>(P + so + tile.nbr[x.e][2 * f + 1] + x.j0 + 4 - Bf);
+  const int Bf = 1 << g.lb[f];
+  {
+    const uint32_t nbl = tile.nbr[x.e][2 * f], nbh = tile.nbr[x.e][2 * f + 1];
+    const bool inl = x.r[f] > 0, inh = x.r[f] + 4 < Bf;
+    const uint32_t ol = inl ? x.off - 1 : (nbl == SG_NO_BLOCK ? SG_NO_BLOCK : nbl + x.j0 + (Bf - 1));
+    const uint32_t oh = inh ? x.off + 4 : (nbh == SG_NO_BLOCK ? SG_NO_BLOCK : nbh + x.j0 + 4 - Bf);
+    L.lo = ol != SG_NO_BLOCK ? ldv<V>(P + so + ol) : V(0);
+    L.hi = oh != SG_NO_BLOCK ? ldv<V>(P + so + oh) : V(0);
+  }
 #pragma unroll
   for (int a = 0; a < f; a++) {
     int sh = 0;
 #pragma unroll
-    for (int b = a + 1; b < ND; b++) sh += A.lb[b];
-    const int B = 1 << A.lb[a];
+    for (int b = a + 1; b < ND; b++) sh += g.lb[b];
+    const int B = 1 << g.lb[a];
     const uint32_t stride = 1u << sh;
 #pragma unroll
     for (int s = 0; s < 2; s++) {
       const int d = s ? 1 : -1;
-      uint32_t off;
-      if (x.r[a] + d >= 0 && x.r[a] + d < B) off = x.off + d * (int)stride;
-      else {
-        uint32_t nb = tile.nbr[x.e][2 * a + s];
-        off = nb == SG_NO_BLOCK ? SG_NO_BLOCK : nb + x.j0 - d * (int)((B - 1) * stride);
-      }
+      const uint32_t nb = tile.nbr[x.e][2 * a + s];
+      const bool in = (unsigned)(x.r[a] + d) < (unsigned)B;
+      const uint32_t off = in ? x.off + d * (int)stride
+                              : (nb == SG_NO_BLOCK ? SG_NO_BLOCK : nb + x.j0 - d * (int)((B - 1) * stride));
       Q4<V>& q = L.row[2 * a + s];
       if (off != SG_NO_BLOCK) q = ld4<V>(P + so + off);
       else { q.v[0] = q.v[1] = q.v[2] = q.v[3] = V(0); }
@@ -320,9 +359,10 @@ __device__ __forceinline__ Q4<V> nbr_sum4(const NbrLoads<V, ND>& L, const Q4<V>&
   return s;
 }
 
-template <typename V, int ND, bool PAIR>
+template <typename V, int ND, bool PAIR, int GL>
 __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, uint32_t* P, uint32_t nq, uint32_t lq,
                                           bool chunked, uint32_t jbase, uint64_t fs) {
+  const QG g = make_qg<GL>(A);
   for (int o = 0; o < A.nops; o++) {
     const DOp& op = A.ops[o];
     const uint64_t s0 = (uint64_t)op.slot[0] * fs, s1 = (uint64_t)(op.slot[1] < 0 ? 0 : op.slot[1]) * fs,
@@ -333,7 +373,7 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
 #pragma unroll
         for (int k = 0; k < 4; k++) q.v[k] = (V)op.p[0];
         for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
-          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
           if (x.off != SG_NO_BLOCK && x.amask) st4<V>(P + s0 + x.off, q, x.amask);
         }
       } break;
@@ -342,7 +382,7 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
       case SG_OP_AXPY: {
         const V p0 = (V)op.p[0];
         for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
-          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
           if (x.off == SG_NO_BLOCK || !x.amask) continue;
           Q4<V> q;
           if (op.op == SG_OP_AXPY) {
@@ -364,20 +404,20 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
         // two quads per thread per trip, every load issued before the arithmetic
         for (uint32_t i = threadIdx.x; i < nq; i += (PAIR ? 2 : 1) * SF_TPB) {
           const bool two = PAIR && i + SF_TPB < nq;
-          QuadCtx x0 = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
-          QuadCtx x1 = quad_ctx<ND>(A, tile, P, two ? i + SF_TPB : i, lq, chunked, jbase);
+          QuadCtx x0 = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+          QuadCtx x1 = quad_ctx<ND>(A, g, tile, P, two ? i + SF_TPB : i, lq, chunked, jbase);
           const bool ok0 = x0.off != SG_NO_BLOCK && x0.amask, ok1 = two && x1.off != SG_NO_BLOCK && x1.amask;
           Q4<V> c0, c1, r0, r1;
           NbrLoads<V, ND> L0, L1;
           if (ok0) {
             c0 = ld4<V>(P + s1 + x0.off);
             if (jac) r0 = ld4<V>(P + s2 + x0.off);
-            nbr_load<V, ND>(A, tile, P, x0, s1, L0);
+            nbr_load<V, ND>(g, tile, P, x0, s1, L0);
           }
           if (ok1) {
             c1 = ld4<V>(P + s1 + x1.off);
             if (jac) r1 = ld4<V>(P + s2 + x1.off);
-            nbr_load<V, ND>(A, tile, P, x1, s1, L1);
+            nbr_load<V, ND>(g, tile, P, x1, s1, L1);
           }
           if (ok0) {
             Q4<V> s = nbr_sum4<V, ND>(L0, c0);
@@ -396,7 +436,7 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
       case SG_OP_REDUCE_SUM: {
         V acc = V(0);
         for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
-          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
           if (x.off == SG_NO_BLOCK || !x.amask) continue;
           Q4<V> q = ld4<V>(P + s1 + x.off);
 #pragma unroll
@@ -405,10 +445,29 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
         }
         warp_add<V>(o, acc);
       } break;
+      case SG_OP_HALO_PACK: {
+        int nf = 0;
+        while (nf < 8 && op.f[nf] >= 0) nf++;
+        halo_pack_slots(A.C, op, const_cast<SFTile&>(tile), A.task);
+        const uint32_t lblk = lq + 2;
+        for (uint32_t e = threadIdx.x; e < tile.ne; e += SF_TPB)
+          if (tile.slot[e] >= 0) {
+            uint32_t* r = halo_rec(A.C, op, tile.slot[e], lblk, nf);
+            r[0] = (uint32_t)tile.org[e][0]; r[1] = (uint32_t)tile.org[e][1]; r[2] = (uint32_t)tile.org[e][2]; r[3] = 0u;
+          }
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || tile.slot[x.e] < 0) continue;
+          uint32_t* r = halo_rec(A.C, op, tile.slot[x.e], lblk, nf) + 4 + x.j0;
+          for (int k = 0; k < nf; k++)
+            *reinterpret_cast<uint4*>(r + ((uint64_t)k << lblk)) =
+                *reinterpret_cast<const uint4*>(P + (uint64_t)op.slot[k] * fs + x.off);
+        }
+      } break;
       default: {
         // per-lane ops (DOWNSAMPLE, JITTER, GRID_OP)
         for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
-          QuadCtx x = quad_ctx<ND>(A, tile, P, i, lq, chunked, jbase);
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
           if (x.off == SG_NO_BLOCK) continue;
           for (int k = 0; k < 4; k++) {
             if (!((x.amask >> k) & 1u)) continue;
@@ -433,6 +492,24 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const SFTile& tile, u
   for (int o = 0; o < A.nops; o++) {
     const DOp& op = A.ops[o];
     V acc = V(0);
+    if (op.op == SG_OP_HALO_PACK) {
+      int nf = 0;
+      while (nf < 8 && op.f[nf] >= 0) nf++;
+      halo_pack_slots(A.C, op, const_cast<SFTile&>(tile), A.task);
+      for (uint32_t e = threadIdx.x; e < tile.ne; e += SF_TPB)
+        if (tile.slot[e] >= 0) {
+          uint32_t* r = halo_rec(A.C, op, tile.slot[e], lblk, nf);
+          r[0] = (uint32_t)tile.org[e][0]; r[1] = (uint32_t)tile.org[e][1]; r[2] = (uint32_t)tile.org[e][2]; r[3] = 0u;
+        }
+      for (uint32_t i = threadIdx.x; i < tcells; i += SF_TPB) {
+        const int e = chunked ? 0 : (int)(i >> lblk);
+        const uint32_t j = chunked ? jbase + i : (i & ((1u << lblk) - 1u));
+        if (tile.blk[e] == SG_NO_BLOCK || tile.slot[e] < 0) continue;
+        uint32_t* r = halo_rec(A.C, op, tile.slot[e], lblk, nf) + 4 + j;
+        for (int k = 0; k < nf; k++) r[(uint64_t)k << lblk] = P[tile.blk[e] + (uint64_t)op.slot[k] * fs + j];
+      }
+      continue;
+    }
     for (uint32_t i = threadIdx.x; i < tcells; i += SF_TPB) {
       CellCtx x;
       x.T = &T;
@@ -462,7 +539,8 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const SFTile& tile, u
 // ---------------------------------------------------------------------------
 // ND = 0: GENERIC cell path; 1..3: QUAD path.  PAIR: two stencil quads in
 // flight per thread (more registers, fewer resident CTAs).
-template <typename V, int ND, bool PAIR>
+// GL: 0 runtime block shape, 1 = 8^3, 2 = 4^3, 3 = 4x4 (constant index math).
+template <typename V, int ND, bool PAIR, int GL>
 __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __grid_constant__ SFArgs A) {
   __shared__ SFTile tile;
   const DTree& T = A.T;
@@ -504,7 +582,9 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
 #pragma unroll
         for (int d = 0; d < 6; d++) tile.nbr[i][d] = r.nbr[d];
       }
+      if (threadIdx.x == 0) tile.ne = ne;
     } else if (threadIdx.x == 0) {   // no driving level: the single root block
+      tile.ne = 1;
       tile.blk[0] = (uint32_t)T.payload_off;
       tile.maskw[0] = T.leaf_bitmasked ? T.lev[T.nlev - 1].mask_off : 0u;
       tile.first[0] = 0;
@@ -513,7 +593,8 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
       for (int d = 0; d < 6; d++) tile.nbr[0][d] = SG_NO_BLOCK;
     }
     __syncthreads();
-    if (ND > 0) run_quads<V, (ND > 0 ? ND : 1), PAIR>(A, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked, jbase, fs);
+    if (ND > 0)
+      run_quads<V, (ND > 0 ? ND : 1), PAIR, GL>(A, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked, jbase, fs);
     else run_cells<V>(A, tile, P, tcells, chunked, jbase, fs);
     __syncthreads();
   }

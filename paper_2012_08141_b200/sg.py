@@ -25,7 +25,8 @@ ROOT, DENSE, BITMASKED, POINTER, PLACE = 0, 1, 2, 3, 4
 F32, I32 = 0, 1
 TASK_STRUCT_FOR, TASK_RANGE_FOR, TASK_SERIAL = 0, 1, 2
 OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6, "REDUCE_SUM": 7,
-       "DOWNSAMPLE": 8, "JITTER": 9, "CLEAR_SCALAR": 10, "P2G": 20, "GRID_OP": 21, "G2P": 22}
+       "DOWNSAMPLE": 8, "JITTER": 9, "CLEAR_SCALAR": 10, "ARRAY_COUNT": 11, "P2G": 20, "GRID_OP": 21, "G2P": 22,
+       "HALO_PACK": 23, "HALO_UNPACK": 24, "G2P_MIGRATE": 25, "MIGRATE_APPEND": 26}
 CLEAR_VALUES, DEACTIVATE = 0, 1
 PASS_LISTGEN_REMOVAL, PASS_ACT_DEMOTION, PASS_FUSION, PASS_DSE = 1, 2, 4, 8
 PASS_ALL = 15
@@ -358,7 +359,15 @@ _lib.sg_set_profiling.argtypes = [_vp, ctypes.c_int32]
 _lib.sg_set_profiling.restype = ctypes.c_int32
 _lib.sg_profile_read.argtypes = [_vp, _P(ctypes.c_double), _P(ctypes.c_int64), ctypes.c_int32]
 _lib.sg_profile_read.restype = ctypes.c_int32
-EXPORTS += ["sg_set_profiling", "sg_profile_read"]
+_lib.sg_set_array_count.argtypes = [_vp, ctypes.c_int32, _vp]
+_lib.sg_set_array_count.restype = ctypes.c_int32
+EXPORTS += ["sg_set_profiling", "sg_profile_read", "sg_set_array_count"]
+
+
+def set_array_count(grid, array_id, count_tensor):
+    """Attach a device int32 count (a torch tensor element) to a registered array."""
+    grid._keep.append(count_tensor)
+    _check(_lib.sg_set_array_count(grid.h, array_id, _vp(count_tensor.data_ptr())))
 
 PROFILE_KINDS = 300
 

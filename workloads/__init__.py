@@ -274,6 +274,44 @@ def c3_program(n_grid=128, n_particles=1_000_000, steps=1, flush_every=1, seed=0
 
 
 # ----------------------------------------------------------------------------
+# C5: large sparse MPM, 512^3 bound, x-slab sharded.
+# pointer(P^3) [n/P cells each] -> bitmasked((n/P/4)^3) -> dense(4^3).
+# ----------------------------------------------------------------------------
+def c5_layout(n_grid=512, ptr_cells=16):
+    L = Layout()
+    bm = n_grid // ptr_cells // 4
+    lv = L.chain([("pointer", (ptr_cells,) * 3), ("bitmasked", (bm,) * 3), ("dense", (4,) * 3)],
+                 [("vx", "f32"), ("vy", "f32"), ("vz", "f32"), ("m", "f32")])
+    return L, lv
+
+
+def c5_particles(n, n_grid=512, length=460, width=66, seed=0, shear=2.0):
+    """An x-spanning bar of length x width x width cells, uniform, with an x-velocity
+    shear v_x = shear * (y - y_c) / width so particles cross slab faces."""
+    rng = np.random.default_rng(seed)
+    dx = 1.0 / n_grid
+    c = n_grid / 2.0
+    lo = np.array([c - length / 2.0, c - width / 2.0, c - width / 2.0]) * dx
+    ext = np.array([length, width, width]) * dx
+    x = (lo[:, None] + rng.random((3, n)) * ext[:, None]).astype(np.float32)
+    v = np.zeros((3, n), dtype=np.float32)
+    v[0] = (shear * (x[1] - 0.5) / (width * dx)).astype(np.float32)
+    return {"x": x, "v": v, "C": np.zeros((9, n), dtype=np.float32), "J": np.ones((1, n), dtype=np.float32)}
+
+
+def c5_program(n_grid=512, ptr_cells=16, n_particles=16_000_000, steps=1, seed=0, **kw):
+    """The unpartitioned C5 problem as a plain program (oracle / 1-GPU reference)."""
+    L, lv = c5_layout(n_grid, ptr_cells)
+    prm = mpm_params(n_grid)
+    arrays = c5_particles(n_particles, n_grid, seed=seed, **kw)
+    calls = []
+    for _ in range(steps):
+        calls += c3_step_calls(L, lv, n_particles, prm)
+        calls.append(flush())
+    return program(L, calls, arrays=arrays, name="C5")
+
+
+# ----------------------------------------------------------------------------
 # Random integer programs (SPEC.md:386/454 fuzzer idea: seeded layouts of
 # depth <= 4, a handful of kernels, integer fields for exact comparison).
 # ----------------------------------------------------------------------------
