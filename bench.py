@@ -232,6 +232,117 @@ def cpu_baseline(args, max_seconds=30.0):
             "host_cpus": os.cpu_count()}
 
 
+def _timed_flushes(grid, enqueue, steps, warmup, l2=None):
+    """Device time (ms) of `steps` flushes; each flush = one step of a config."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        enqueue()
+        st = grid.flush("all")
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        if l2 is not None:
+            l2.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        enqueue()
+        st = grid.flush("all")
+        b.record(stream)
+        b.synchronize()
+        ms += a.elapsed_time(b)
+    return ms / steps, st
+
+
+def measure_c1(steps=200, warmup=10):
+    """C1: 2D 64^2 disk, the 8-task stream (launch-latency bound)."""
+    import torch
+    from paper_2012_08141_b200 import sg
+    L, lv = W.c1_layout()
+    coords = torch.as_tensor(W.c1_disk_coords()).cuda()
+    calls = W.c1_step_calls(L, lv, W.c1_disk_coords())
+    g = sg.Grid(L.desc())
+    ms, st = _timed_flushes(g, lambda: enqueue_calls(g, calls, coords), steps, warmup)
+    enqueue_calls(g, calls, coords)
+    eager = g.flush(0)
+    return {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
+            "eager_launches_per_step": eager["launches"], "result_s": float(g.field(L.fields["s"]))}
+
+
+def measure_c3(steps=20, warmup=3, n=1_000_000):
+    """C3: 3D 128^3 sparse MLS-MPM, 1M particles: DEACTIVATE, P2G, GRID_OP, G2P per step."""
+    import torch
+    from paper_2012_08141_b200 import sg
+    prog = W.c3_program(n_grid=128, n_particles=n, steps=1)
+    g = sg.Grid(prog["desc"])
+    for name, a in prog["arrays"].items():
+        t = torch.as_tensor(a).cuda().contiguous()
+        g.tensors = getattr(g, "tensors", {})
+        g.tensors[name] = t
+        g.register_array(t, a.shape[0])
+    step_calls = [c for c in prog["calls"] if c["call"] != "flush"]
+
+    def enqueue():
+        for c in step_calls:
+            if c["call"] == "clear":
+                g.clear(c["target"], sg.DEACTIVATE)
+            elif c["call"] == "range_for":
+                g.range_for(c["op"], c["n"], c["fields"], c["arrays"], c["params"], c["activating"])
+            elif c["call"] == "struct_for":
+                g.struct_for(c["op"], c["snode"], c["fields"], c["params"], c["activating"])
+
+    sg.set_profiling(g, True)
+    ms, st = _timed_flushes(g, enqueue, steps, warmup)
+    prof = sg.profile_read(g)
+    sg.set_profiling(g, False)
+    per = {}
+    names = {0: "activate", 1: "listgen", 3: "struct_for", 4: "range_for", 6: "deactivate"}
+    for k, (t, c) in prof.items():
+        if k in names:
+            per[names[k]] = t / max(c, 1) * 1e3
+    return {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
+            "avg_us_per_launch_kind": per, "particles": n}
+
+
+def run_c5(args, rank, world, local):
+    """C5: 512^3 sparse MPM, 16M particles in an x-spanning bar, sharded in x
+    slabs over the ranks (strong scaling); NCCL P2P halo / migration."""
+    import torch
+    from paper_2012_08141_b200 import parallel
+    torch.cuda.set_device(local)
+    n = args.c5_particles
+    prm = W.mpm_params(512)
+    parts = W.c5_particles(n, 512, seed=0)
+    transport = parallel.DistTransport() if world > 1 else parallel.LocalTransport()
+    sim = parallel.SlabMPM(512, 16, parts, world, [rank], transport, prm, lambda r: torch.device("cuda", local),
+                           halo_cap=4096, mig_cap=65536)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        st = sim.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        a.record(stream)
+        for _ in range(args.steps):
+            st = sim.step()
+            launches += sum(s["launches"] for s in st)
+        b.record(stream)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    me = sim.ranks[rank]
+    return {"ms_per_step": ms / args.steps, "launches": launches, "clocks": clk.summary(), "n_local": me.n(),
+            "launches_per_step_rank0": sum(s["launches"] for s in st)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,6 +351,9 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--impl", default="sg", choices=["sg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C1/C3 lines and the XL rooflines")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--c5-particles", type=int, default=16_000_000)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -269,6 +383,24 @@ def main():
         import torch
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.workload == "c5":
+        r = run_c5(args, rank, world, local)
+        if rank == 0:
+            out = {"metric": "sparse-grid steps/s (C5 MPM steps/s)", "value": 1000.0 / r["ms_per_step"],
+                   "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                   "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+                   "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                   "config": {"workload": f"C5: 512^3 sparse MLS-MPM, {args.c5_particles} particles in a "
+                                          "460x66x66-cell bar with x-velocity shear; pointer(16^3)->bitmasked(8^3)"
+                                          "->dense(4^3)", "parallelism": f"x-slabs{world}",
+                              "l2": "inputs (1 GB of particles) larger than L2"},
+                   "gpu_launches": r["launches"], "launches_per_step_rank0": r["launches_per_step_rank0"],
+                   "clocks": r["clocks"]}
+            print(json.dumps(out))
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     r = run_sg(args, rank, world, local)
     if rank == 0:
         jac_ms, jac_n, jac_bytes, achieved, peak, peak_kind, traffic = r["jac"]
@@ -295,6 +427,21 @@ def main():
             "clocks": r["clocks"],
             "result_s": r["s"],
         }
+        if not args.no_extra and world == 1:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            import xl_bench
+            extra = {}
+            for name, fn in (("c1", measure_c1), ("c3", measure_c3), ("jac_xl", xl_bench.jac_xl),
+                             ("lg_xl", xl_bench.lg_xl)):
+                try:
+                    extra[name] = fn()
+                except Exception as e:  # keep the main line even if an extra fails
+                    extra[name] = {"error": repr(e)[:200]}
+            out["extra"] = extra
+            out["roofline_xl"] = {k: {"achieved": extra[k].get("achieved_GBps"), "frac": extra[k].get("frac"),
+                                      "peak": extra[k].get("peak_GBps"), "unit": "GB/s",
+                                      "bytes_per_launch": extra[k].get("bytes_per_launch")}
+                                  for k in ("jac_xl", "lg_xl")}
         if not args.no_cpu_baseline and world == 1:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out))

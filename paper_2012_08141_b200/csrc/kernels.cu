@@ -240,7 +240,7 @@ __device__ __forceinline__ void make_block_row(const DTree& T, uint32_t e, Block
   const uint32_t lowmask = ~((1u << T.lblk) - 1u);
 #pragma unroll
   for (int dir = 0; dir < 6; dir++) {
-    r.nbr[dir] = SG_NO_BLOCK;
+    r.nbr[dir] = SG_NO_BLOCK;   // absent: reads 0
     int axis = dir >> 1;
     if (!ok || axis >= T.nd || T.driving < 0) continue;
     int q[3] = {org[0], org[1], org[2]};
@@ -453,13 +453,6 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
       __syncthreads();
     }
-    if (a.out.table) {
-      // block table of the driving level: one row per entry of this tile, all threads
-      const uint32_t end = min(s_base + s_total, a.out.capacity);
-      for (uint32_t i = s_base + threadIdx.x; i < end; i += LG_TPB)
-        make_block_row(a.T, a.out.entries[i], a.out.table + i);
-      __syncthreads();
-    }
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -468,6 +461,7 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       a.out.ctl[0] = 0;
       a.out.ctl[1] = 0;
       a.out.ctl[2] = a.out.ctl[2] + 1u;
+      a.out.ctl[4] = 0u;   // the block table (if any) is stale until a struct-for rebuilds it
       __threadfence();
     }
   }
@@ -729,6 +723,7 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   a->entries = drive ? drive->entries : nullptr;
   a->count = drive ? drive->count : nullptr;
   a->table = drive ? drive->table : nullptr;
+  a->table_ctl = drive ? drive->ctl : nullptr;
   a->has_reduce = 0;
   for (int o = 0; o < nops; o++) a->has_reduce |= ops[o].op == SG_OP_REDUCE_SUM;
   a->need_nbr = 0;

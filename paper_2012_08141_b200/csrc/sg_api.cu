@@ -264,8 +264,12 @@ static sg_status derive_tree(sg_grid* g, int tid, DTree& T) {
       if (((uint64_t)S.capacity << T.lev[k].ln) > (1ull << 32))
         return fail(SG_ERR_LAYOUT, "list entries would overflow u32: lower opts.pool_capacity");
     }
-    if (s == T.nseg - 1 && (uint64_t)S.capacity * S.stride >= 0xFFFFFFFFull)
-      return fail(SG_ERR_LAYOUT, "leaf pool exceeds 2^32 words (block offsets are u32): lower opts.pool_capacity");
+    if (s == T.nseg - 1) {
+      // one extra, never-allocated container stays all-zero: absent neighbours point at it
+      if ((uint64_t)(S.capacity + 1) * S.stride >= 0xFFFFFFFFull)
+        return fail(SG_ERR_LAYOUT, "leaf pool exceeds 2^32 words (block offsets are u32): lower opts.pool_capacity");
+      T.zero_blk = (uint32_t)((uint64_t)S.capacity * S.stride + T.payload_off);
+    }
   }
   return SG_OK;
 }
@@ -273,7 +277,7 @@ static sg_status derive_tree(sg_grid* g, int tid, DTree& T) {
 static sg_status alloc_tree(sg_grid* g, int tid, DTree& T) {
   for (int s = 0; s < T.nseg; s++) {
     DSeg& S = T.seg[s];
-    size_t bytes = (size_t)S.capacity * S.stride * 4;
+    size_t bytes = (size_t)(S.capacity + (s == T.nseg - 1 ? 1 : 0)) * S.stride * 4;
     S.base = (uint32_t*)g->dev_alloc(bytes);
     if (!S.base) return fail(SG_ERR_CUDA, "pool allocation failed (" + std::to_string(bytes) + " bytes)");
     CUDA_TRY(cudaMemsetAsync(S.base, 0, bytes, g->stream));
@@ -321,11 +325,11 @@ static sg_status alloc_list(sg_grid* g, int tid, int k) {
   }
   Ls.entries = (uint32_t*)g->dev_alloc(cap * 4);
   Ls.count = (uint32_t*)g->dev_alloc(16);
-  Ls.ctl = (uint32_t*)g->dev_alloc(16);
+  Ls.ctl = (uint32_t*)g->dev_alloc(32);
   Ls.status = (uint64_t*)g->dev_alloc(max_tiles * 8);
   if (!Ls.entries || !Ls.count || !Ls.ctl || !Ls.status) return fail(SG_ERR_CUDA, "list allocation failed");
   CUDA_TRY(cudaMemsetAsync(Ls.count, 0, 16, g->stream));
-  CUDA_TRY(cudaMemsetAsync(Ls.ctl, 0, 16, g->stream));
+  CUDA_TRY(cudaMemsetAsync(Ls.ctl, 0, 32, g->stream));
   CUDA_TRY(cudaMemsetAsync(Ls.status, 0, max_tiles * 8, g->stream));
   return SG_OK;
 }

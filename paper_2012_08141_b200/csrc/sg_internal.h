@@ -61,7 +61,8 @@ struct DTree {
   int32_t payload_off;    // u32-word offset of the payload in leaf containers
   int32_t ln_leaf;        // log2 leaf cells per leaf container
   int32_t nfields;
-  int32_t pad_;
+  uint32_t zero_blk;      // word offset (leaf pool) of a never-written all-zero container's
+                          // payload: absent neighbour blocks point here, so loads need no branch
   DLevel lev[SG_MAXL];
   DSeg seg[SG_MAXL];
 };
@@ -100,8 +101,9 @@ struct DList {
   uint32_t* entries;
   uint32_t* count;     // device-side count
   uint64_t* status;    // look-back tile descriptors
-  uint32_t* ctl;       // [0] tile counter, [1] done counter, [2] epoch
-  BlockRow* table;     // driving level only, else null
+  uint32_t* ctl;       // [0] tile counter, [1] done counter, [2] epoch, [3] table-row ticket,
+                       // [4] table_ok: rows of the current list version are built
+  BlockRow* table;     // driving level only, else null (rows built by the first struct-for)
   uint32_t capacity;
   uint32_t max_tiles;
 };

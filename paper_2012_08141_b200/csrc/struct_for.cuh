@@ -30,7 +30,8 @@ struct SFArgs {
   DevCtx C;
   const uint32_t* entries;   // driving list (null when the tree has no driving level)
   const uint32_t* count;
-  const BlockRow* table;     // the list's block table
+  BlockRow* table;           // the list's block table
+  uint32_t* table_ctl;       // the list's ctl words ([3] ticket, [4] rows built)
   int has_reduce;
   int nops;
   int need_nbr;
@@ -311,18 +312,40 @@ struct NbrLoads {
   V lo, hi;                      // fast-axis ends
 };
 
+// Predicated global loads (no branch; the register keeps 0 when the predicate
+// is off -- an absent neighbour reads 0).
+__device__ __forceinline__ uint4 ld4_if(const uint32_t* p, bool pred) {
+  uint4 r = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n}\n"
+      : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+      : "l"(p), "r"((int)pred));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld1_if(const uint32_t* p, bool pred) {
+  uint32_t r = 0u;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.u32 %0, [%1];\n}\n"
+               : "+r"(r)
+               : "l"(p), "r"((int)pred));
+  return r;
+}
+template <typename V> __device__ __forceinline__ V bits_to(uint32_t u);
+template <> __device__ __forceinline__ float bits_to<float>(uint32_t u) { return __uint_as_float(u); }
+template <> __device__ __forceinline__ int bits_to<int>(uint32_t u) { return (int)u; }
+
+// `src` is the field's base (pool + slot * field stride).
 template <typename V, int ND>
-__device__ __forceinline__ void nbr_load(const QG& g, const SFTile& tile, const uint32_t* P, const QuadCtx& x,
-                                         uint64_t so, NbrLoads<V, ND>& L) {
+__device__ __forceinline__ void nbr_load(const QG& g, const SFTile& tile, const uint32_t* __restrict__ src,
+                                         const QuadCtx& x, NbrLoads<V, ND>& L) {
   constexpr int f = ND - 1;
   const int Bf = 1 << g.lb[f];
   {
     const uint32_t nbl = tile.nbr[x.e][2 * f], nbh = tile.nbr[x.e][2 * f + 1];
     const bool inl = x.r[f] > 0, inh = x.r[f] + 4 < Bf;
-    const uint32_t ol = inl ? x.off - 1 : (nbl == SG_NO_BLOCK ? SG_NO_BLOCK : nbl + x.j0 + (Bf - 1));
-    const uint32_t oh = inh ? x.off + 4 : (nbh == SG_NO_BLOCK ? SG_NO_BLOCK : nbh + x.j0 + 4 - Bf);
-    L.lo = ol != SG_NO_BLOCK ? ldv<V>(P + so + ol) : V(0);
-    L.hi = oh != SG_NO_BLOCK ? ldv<V>(P + so + oh) : V(0);
+    const uint32_t ol = inl ? x.off - 1 : nbl + x.j0 + (Bf - 1);
+    const uint32_t oh = inh ? x.off + 4 : nbh + x.j0 + 4 - Bf;
+    L.lo = bits_to<V>(ld1_if(src + ol, inl || nbl != SG_NO_BLOCK));
+    L.hi = bits_to<V>(ld1_if(src + oh, inh || nbh != SG_NO_BLOCK));
   }
 #pragma unroll
   for (int a = 0; a < f; a++) {
@@ -336,11 +359,10 @@ __device__ __forceinline__ void nbr_load(const QG& g, const SFTile& tile, const 
       const int d = s ? 1 : -1;
       const uint32_t nb = tile.nbr[x.e][2 * a + s];
       const bool in = (unsigned)(x.r[a] + d) < (unsigned)B;
-      const uint32_t off = in ? x.off + d * (int)stride
-                              : (nb == SG_NO_BLOCK ? SG_NO_BLOCK : nb + x.j0 - d * (int)((B - 1) * stride));
+      const uint32_t off = in ? x.off + d * (int)stride : nb + x.j0 - d * (int)((B - 1) * stride);
+      const uint4 u = ld4_if(src + off, in || nb != SG_NO_BLOCK);
       Q4<V>& q = L.row[2 * a + s];
-      if (off != SG_NO_BLOCK) q = ld4<V>(P + so + off);
-      else { q.v[0] = q.v[1] = q.v[2] = q.v[3] = V(0); }
+      q.v[0] = bits_to<V>(u.x); q.v[1] = bits_to<V>(u.y); q.v[2] = bits_to<V>(u.z); q.v[3] = bits_to<V>(u.w);
     }
   }
 }
@@ -401,7 +423,10 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
       case SG_OP_JACOBI: {
         const bool jac = op.op == SG_OP_JACOBI;
         const V inv = V(1) / (V)(2 * ND);
-        // two quads per thread per trip, every load issued before the arithmetic
+        const uint32_t* __restrict__ src = P + s1;
+        const uint32_t* __restrict__ rhs = P + s2;
+        uint32_t* dst = P + s0;
+        // (PAIR: two quads per thread per trip, every load issued before the arithmetic)
         for (uint32_t i = threadIdx.x; i < nq; i += (PAIR ? 2 : 1) * SF_TPB) {
           const bool two = PAIR && i + SF_TPB < nq;
           QuadCtx x0 = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
@@ -410,26 +435,26 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
           Q4<V> c0, c1, r0, r1;
           NbrLoads<V, ND> L0, L1;
           if (ok0) {
-            c0 = ld4<V>(P + s1 + x0.off);
-            if (jac) r0 = ld4<V>(P + s2 + x0.off);
-            nbr_load<V, ND>(g, tile, P, x0, s1, L0);
+            c0 = ld4<V>(src + x0.off);
+            if (jac) r0 = ld4<V>(rhs + x0.off);
+            nbr_load<V, ND>(g, tile, src, x0, L0);
           }
           if (ok1) {
-            c1 = ld4<V>(P + s1 + x1.off);
-            if (jac) r1 = ld4<V>(P + s2 + x1.off);
-            nbr_load<V, ND>(g, tile, P, x1, s1, L1);
+            c1 = ld4<V>(src + x1.off);
+            if (jac) r1 = ld4<V>(rhs + x1.off);
+            nbr_load<V, ND>(g, tile, src, x1, L1);
           }
           if (ok0) {
             Q4<V> s = nbr_sum4<V, ND>(L0, c0);
 #pragma unroll
             for (int k = 0; k < 4; k++) s.v[k] = jac ? (r0.v[k] + s.v[k]) * inv : s.v[k] - (V)(2 * ND) * c0.v[k];
-            st4<V>(P + s0 + x0.off, s, x0.amask);
+            st4<V>(dst + x0.off, s, x0.amask);
           }
           if (ok1) {
             Q4<V> s = nbr_sum4<V, ND>(L1, c1);
 #pragma unroll
             for (int k = 0; k < 4; k++) s.v[k] = jac ? (r1.v[k] + s.v[k]) * inv : s.v[k] - (V)(2 * ND) * c1.v[k];
-            st4<V>(P + s0 + x1.off, s, x1.amask);
+            st4<V>(dst + x1.off, s, x1.amask);
           }
         }
       } break;
@@ -547,6 +572,7 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
   uint32_t* P = T.seg[T.nseg - 1].base;
   if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
   const uint32_t nent = A.entries ? *A.count : 1u;
+  const bool rows_ok = A.table && *(volatile uint32_t*)&A.table_ctl[4] != 0u;
   const int lblk = T.lblk;
   const bool chunked = lblk > A.ltile;
   uint64_t ntiles;
@@ -571,8 +597,10 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
       ne = min(1u << A.lept, nent - e0);
       tcells = ne << lblk;
     }
-    // the tile's blocks: one coalesced read of the list's block table
-    if (A.table) {
+    // the tile's blocks: one coalesced read of the list's block table, or --
+    // first struct-for after a listgen -- built here (tree walks spread over
+    // every CTA) and stored for the following launches
+    if (A.entries && rows_ok) {
       for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
         const BlockRow r = A.table[e0 + i];
         tile.blk[i] = r.blk;
@@ -583,6 +611,47 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
         for (int d = 0; d < 6; d++) tile.nbr[i][d] = r.nbr[d];
       }
       if (threadIdx.x == 0) tile.ne = ne;
+    } else if (A.entries) {
+      // build the rows: resolve every entry, then one tree walk per (entry, face)
+      const uint32_t* base = T.seg[T.nseg - 1].base;
+      for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
+        uint32_t* cont;
+        uint32_t first;
+        int org[3];
+        bool ok = resolve_entry(T, A.entries[e0 + i], cont, first, org);
+        tile.blk[i] = ok ? (uint32_t)(cont - base) + T.payload_off + first : SG_NO_BLOCK;
+        tile.maskw[i] = ok && T.leaf_bitmasked ? (uint32_t)(cont - base) + T.lev[T.nlev - 1].mask_off + (first >> 5) : 0u;
+        tile.first[i] = first;
+        tile.org[i][0] = org[0]; tile.org[i][1] = org[1]; tile.org[i][2] = org[2];
+      }
+      if (threadIdx.x == 0) tile.ne = ne;
+      __syncthreads();
+      const uint32_t lowmask = ~((1u << lblk) - 1u);
+      for (uint32_t i = threadIdx.x; i < ne * 6; i += SF_TPB) {
+        const uint32_t e = i / 6;
+        const int dir = i % 6, axis = dir >> 1;
+        uint32_t nb = SG_NO_BLOCK;
+        if (axis < T.nd && tile.blk[e] != SG_NO_BLOCK && T.driving >= 0) {
+          int q[3] = {tile.org[e][0], tile.org[e][1], tile.org[e][2]};
+          q[axis] += (dir & 1) ? (1 << T.lev[T.driving].lbelow[axis]) : -1;
+          if (in_domain(T, q)) {
+            uint32_t idx;
+            uint32_t* c2 = locate(T, q, idx);
+            if (c2) nb = (uint32_t)(c2 - base) + T.payload_off + (idx & lowmask);
+          }
+        }
+        tile.nbr[e][dir] = nb;
+      }
+      __syncthreads();
+      if (A.table)
+        for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
+          BlockRow r;
+          r.blk = tile.blk[i]; r.maskw = tile.maskw[i]; r.first = tile.first[i];
+          r.org[0] = tile.org[i][0]; r.org[1] = tile.org[i][1]; r.org[2] = tile.org[i][2];
+#pragma unroll
+          for (int d = 0; d < 6; d++) r.nbr[d] = tile.nbr[i][d];
+          A.table[e0 + i] = r;
+        }
     } else if (threadIdx.x == 0) {   // no driving level: the single root block
       tile.ne = 1;
       tile.blk[0] = (uint32_t)T.payload_off;
@@ -599,4 +668,13 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
     __syncthreads();
   }
   if (A.has_reduce) finish_reductions<V>(A);
+  if (A.table && !rows_ok && threadIdx.x == 0) {
+    // the last CTA marks the table complete for this list version
+    __threadfence();
+    if (atomicAdd(&A.table_ctl[3], 1u) == gridDim.x - 1) {
+      A.table_ctl[3] = 0u;
+      __threadfence();
+      A.table_ctl[4] = 1u;
+    }
+  }
 }

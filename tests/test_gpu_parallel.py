@@ -57,7 +57,15 @@ def check(sim, prog, o):
     L = prog["layout"]
     m_want, m_mag = o.field(L.fields["m"], with_mag=True)
     m_got = sim.gather_field("m").astype(np.float64)
-    assert (np.abs(m_got - m_want) <= 1e-4 * np.maximum(np.abs(m_want), m_mag)).all()
+    # after several steps the particle positions agree to ~1 ulp; a node whose
+    # B-spline weight w = (fx - 1/2)^2 / 2 is nearly 0 turns that into a large
+    # relative error, so the mass bound carries an absolute floor of 1e-5 of
+    # the largest node mass (reading R17)
+    floor = 1e-5 * np.abs(m_want).max()
+    err = np.abs(m_got - m_want)
+    bad = err > 1e-4 * np.maximum(np.abs(m_want), m_mag) + floor
+    assert not bad.any(), f"m: {bad.sum()} off, worst {err[bad].max()}"
+    assert ((m_got > 0) == (m_want > 0)).all()
 
 
 @pytest.mark.parametrize("world", [1, 2, 4])
