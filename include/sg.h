@@ -175,7 +175,14 @@ enum {
   SG_PASS_ACT_DEMOTION = 2,      /* section 6.3 */
   SG_PASS_FUSION = 4,            /* section 6.4 */
   SG_PASS_DSE = 8,               /* section 6.5 */
-  SG_PASS_ALL = 15
+  SG_PASS_ALL = 15,
+  /* Beyond the paper: after the four passes, adjacent
+   * struct-for groups over the same list version (with independent tasks
+   * hoisted out of the way) become the phases of ONE persistent cooperative
+   * launch with a grid-wide barrier between phases -- legal for the dependent
+   * stencil chains the paper's rule cannot fuse.  Reported
+   * separately from SG_PASS_ALL. */
+  SG_PASS_CHAIN = 16
 };
 
 typedef struct {
@@ -190,6 +197,8 @@ typedef struct {
   int64_t plan_cache_hits;
   int64_t plan_cache_misses;
   double plan_us;               /* host planning time of this flush */
+  int64_t tasks_chained;        /* SG_PASS_CHAIN: struct-for groups merged into chains */
+  int64_t launches_chained;     /* SG_PASS_CHAIN: cooperative chain launches */
 } sg_stats;
 
 /* Optimize and launch the queue.  passes = 0 launches one kernel per lowered

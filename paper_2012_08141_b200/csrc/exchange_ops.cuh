@@ -45,6 +45,7 @@ __device__ void halo_unpack(const DevCtx& C, const DOp& op, int64_t i, int task)
 // overwrite unread data), leavers are appended to the left / right buffers.
 // ---------------------------------------------------------------------------
 struct MigArgs {
+  DTree T;                // the grid tree (by value: constant bank)
   DevCtx C;
   DOp op;
   uint64_t* status;       // look-back descriptors (one per tile)
@@ -76,12 +77,7 @@ __global__ void __launch_bounds__(MG_TPB) k_g2p_migrate(const __grid_constant__ 
   const uint32_t ntiles = (n + MG_TPB - 1) / MG_TPB;
   const float dt = op.p[0], inv_dx = op.p[1], lo = op.p[2], hi = op.p[3];
   const float dx = 1.0f / inv_dx;
-  const DField& F0 = C.fields[op.f[0]];
-  const DTree& T = C.trees[F0.tree];
-  const uint64_t fs = 1ull << T.ln_leaf;
-  int sl[3];
-#pragma unroll
-  for (int r = 0; r < 3; r++) sl[r] = C.fields[op.f[r]].slot;
+  const DTree& T = A.T;
   __syncthreads();
   const uint32_t epoch = s_epoch;
   while (true) {
@@ -99,28 +95,7 @@ __global__ void __launch_bounds__(MG_TPB) k_g2p_migrate(const __grid_constant__ 
       J = jj[i];
       pid = id[i];
       MpmKernel k = mpm_bspline(xp, inv_dx);
-      MpmBlocks B;
-      mpm_blocks<false>(C, T, k.base, B, 0);
-      const float s4 = 4.0f * inv_dx * inv_dx;
-#pragma unroll
-      for (int a = 0; a < 3; a++)
-#pragma unroll
-        for (int b = 0; b < 3; b++)
-#pragma unroll
-          for (int c = 0; c < 3; c++) {
-            const float wgt = k.w[a][0] * k.w[b][1] * k.w[c][2];
-            const float dpos[3] = {((float)a - k.fx[0]) * dx, ((float)b - k.fx[1]) * dx, ((float)c - k.fx[2]) * dx};
-            int nn[3] = {k.base[0] + a, k.base[1] + b, k.base[2] + c};
-            const uint32_t* p = mpm_node(T, B, nn);
-            if (!p) continue;
-#pragma unroll
-            for (int r = 0; r < 3; r++) {
-              float g = __uint_as_float(p[sl[r] * fs]);
-              nv[r] += wgt * g;
-#pragma unroll
-              for (int d = 0; d < 3; d++) nC[r][d] += s4 * wgt * g * dpos[d];
-            }
-          }
+      mpm_gather<0>(C, T, op, k, dx, inv_dx, nv, nC);
       J = J * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
 #pragma unroll
       for (int r = 0; r < 3; r++) xp[r] = xp[r] + dt * nv[r];

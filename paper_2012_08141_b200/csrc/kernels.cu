@@ -15,10 +15,13 @@
 //   k_serial / k_range_for, export helpers.
 // No host synchronization anywhere on the hot path: list counts are read on
 // the device and every kernel grid-strides over them.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <algorithm>
 #include "sg_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace sg {
 
@@ -505,8 +508,8 @@ __global__ void __launch_bounds__(128) k_range_for(const __grid_constant__ RFArg
     for (int o = 0; o < A.nops; o++) {
       const DOp& op = A.ops[o];
       switch (op.op) {
-        case SG_OP_P2G: mpm_p2g(A.C, op, i, A.task); break;
-        case SG_OP_G2P: mpm_g2p(A.C, op, i); break;
+        case SG_OP_P2G: mpm_p2g<0>(A.C, A.C.trees[A.C.fields[op.f[0]].tree], op, i, A.task); break;
+        case SG_OP_G2P: mpm_g2p<0>(A.C, A.C.trees[A.C.fields[op.f[0]].tree], op, i); break;
         case SG_OP_HALO_UNPACK: halo_unpack(A.C, op, i, A.task); break;
         default: break;
       }
@@ -716,8 +719,27 @@ int launch_clear_list(const DList& l, void* stream) {
 
 static int ilog2(uint64_t v) { int r = 0; while ((1ull << r) < v) r++; return r; }
 
+template <typename V, int ND, bool PAIR, int GL>
+static void sf_dispatch(SFArgs* a, int grid, cudaStream_t s, const DOp* optab, const int* phase_end, int nphases) {
+  if (nphases <= 1) {
+    k_struct_for<V, ND, PAIR, GL><<<grid, SF_TPB, 0, s>>>(*a);
+    return;
+  }
+  // cooperative launch: every CTA resident (grid-wide barriers between phases)
+  auto kern = k_struct_chain<V, ND, PAIR, GL>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SF_TPB, 0) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+  }
+  int g = std::max(1, std::min(grid, per_sm * num_sms()));
+  void* args[] = {(void*)a, (void*)&optab, (void*)&phase_end, (void*)&nphases};
+  cudaLaunchCooperativeKernel((const void*)kern, dim3(g), dim3(SF_TPB), args, 0, s);
+}
+
 int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, const DOp* ops, int nops,
-                      int task, void* stream, int grid_hint) {
+                      int task, void* stream, int grid_hint, const DOp* dev_optab, const int* dev_phase_end,
+                      int nphases, int chain_needs_nbr) {
   SFArgs* a = new SFArgs();
   a->T = t; a->C = c; a->task = task; a->nops = nops;
   a->entries = drive ? drive->entries : nullptr;
@@ -734,6 +756,7 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
     if (op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER) a->need_nbr = 1;
     a->aux[o] = 0;
   }
+  if (chain_needs_nbr) a->need_nbr = 1;
   // dtype of the group (validated uniform by the host)
   i32 = ops[0].dt == SG_I32;
   for (int o = 0; o < nops; o++)
@@ -765,16 +788,16 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   if (nd == 3 && a->lb[0] == 3 && a->lb[1] == 3 && a->lb[2] == 3) gl = 1;
   else if (nd == 3 && a->lb[0] == 2 && a->lb[1] == 2 && a->lb[2] == 2) gl = 2;
   else if (nd == 2 && a->lb[0] == 2 && a->lb[1] == 2) gl = 3;
-#define SG_SF_LAUNCH(V)                                                                     \
-  switch (nd * 10 + gl) {                                                                   \
-    case 10: k_struct_for<V, 1, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    case 20: k_struct_for<V, 2, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    case 23: k_struct_for<V, 2, false, 3><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    case 30: if (pair && stencil) k_struct_for<V, 3, true, 0><<<grid, SF_TPB, 0, s>>>(*a);   \
-             else k_struct_for<V, 3, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;           \
-    case 31: k_struct_for<V, 3, false, 1><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    case 32: k_struct_for<V, 3, false, 2><<<grid, SF_TPB, 0, s>>>(*a); break;               \
-    default: k_struct_for<V, 0, false, 0><<<grid, SF_TPB, 0, s>>>(*a); break;               \
+#define SG_SF_LAUNCH(V)                                                                           \
+  switch (nd * 10 + gl) {                                                                         \
+    case 10: sf_dispatch<V, 1, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
+    case 20: sf_dispatch<V, 2, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
+    case 23: sf_dispatch<V, 2, false, 3>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
+    case 30: if (pair && stencil) sf_dispatch<V, 3, true, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); \
+             else sf_dispatch<V, 3, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;          \
+    case 31: sf_dispatch<V, 3, false, 1>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
+    case 32: sf_dispatch<V, 3, false, 2>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
+    default: sf_dispatch<V, 0, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
   }
   if (i32) { SG_SF_LAUNCH(int) } else { SG_SF_LAUNCH(float) }
 #undef SG_SF_LAUNCH
@@ -783,12 +806,28 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
 }
 
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task,
-                     void* stream, const RangeScratch* rs) {
+                     void* stream, const RangeScratch* rs, const DTree* grid_tree) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  if (nops == 1 && grid_tree && (ops[0].op == SG_OP_P2G || ops[0].op == SG_OP_G2P)) {
+    MpmArgs m;
+    m.T = *grid_tree; m.C = c; m.op = ops[0]; m.n = n; m.dcount = dcount; m.task = task;
+    const bool lb2 = grid_tree->lev[grid_tree->driving].lbelow[0] == 2 && grid_tree->lev[grid_tree->driving].lbelow[1] == 2 &&
+                     grid_tree->lev[grid_tree->driving].lbelow[2] == 2 && grid_tree->lblk == 6;
+    int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms() * 16);
+    if (ops[0].op == SG_OP_P2G) {
+      if (lb2) k_p2g<2><<<grid, 128, 0, s>>>(m);
+      else k_p2g<0><<<grid, 128, 0, s>>>(m);
+    } else {
+      if (lb2) k_g2p<2><<<grid, 128, 0, s>>>(m);
+      else k_g2p<0><<<grid, 128, 0, s>>>(m);
+    }
+    return check_launch();
+  }
   if (nops == 1 && ops[0].op == SG_OP_G2P_MIGRATE) {
     MigArgs m;
     m.C = c; m.op = ops[0]; m.status = rs->status; m.ctl = rs->ctl; m.task = task;
+    m.T = *grid_tree;
     int grid = (int)std::min<int64_t>((n + MG_TPB - 1) / MG_TPB, (int64_t)num_sms() * 6);
     k_g2p_migrate<<<std::max(grid, 1), MG_TPB, 0, s>>>(m);
     return check_launch();

@@ -689,6 +689,77 @@ static bool pass_dse(std::vector<PTask>& seq, const std::vector<char>& observed,
   return changed;
 }
 
+// Beyond the paper (SG_PASS_CHAIN): adjacent struct-for groups over the same
+// list version become phases of one cooperative launch (grid barrier between
+// phases).  Tasks in between that do not depend on the chain so far are
+// hoisted before it; a reduction may only end a chain.
+static void pass_chain(const HLayout& L, std::vector<PTask>& seq, const std::vector<PTask>& eager, PlanStats& st) {
+  Graph G = build_graph(seq);
+  const int n = G.n;
+  std::vector<char> used(n, 0);
+  std::vector<PTask> out;
+  auto list_ver = [&](int i, int64_t& lv, int64_t& mv) {
+    const HTree& T = L.trees[seq[i].tree];
+    lv = -7; mv = -7;
+    if (T.driving >= 0) {
+      int64_t s = skey(ST_LIST, T.levels[T.driving]);
+      lv = G.in_ver[i].count(s) ? G.in_ver[i].at(s) : -3;
+    }
+    if (T.leaf_bitmasked) {
+      int64_t s = skey(ST_MASK, T.levels.back());
+      mv = G.in_ver[i].count(s) ? G.in_ver[i].at(s) : -3;
+    }
+  };
+  auto group_reduces = [&](const PTask& t) {
+    for (int m : t.members) if (eager[m].t.op == SG_OP_REDUCE_SUM) return true;
+    return false;
+  };
+  for (int i = 0; i < n; i++) {
+    if (used[i]) continue;
+    const PTask& A = seq[i];
+    if (A.type != TT_STRUCT_FOR) { out.push_back(A); used[i] = 1; continue; }
+    int64_t alv, amv;
+    list_ver(i, alv, amv);
+    std::vector<int> chain{i}, hoist;
+    std::vector<char> in_chain(n, 0);
+    in_chain[i] = 1;
+    bool reduce_seen = group_reduces(A);
+    for (int j = i + 1; j < n && !reduce_seen; j++) {
+      if (used[j]) continue;
+      const PTask& X = seq[j];
+      if (X.type == TT_STRUCT_FOR && X.tree == A.tree && X.snode == A.snode &&
+          task_dtype(L, X) == task_dtype(L, A)) {
+        int64_t xlv, xmv;
+        list_ver(j, xlv, xmv);
+        if (xlv == alv && xmv == amv) {
+          chain.push_back(j);
+          in_chain[j] = 1;
+          reduce_seen = group_reduces(X);
+          continue;
+        }
+      }
+      bool dep = false;
+      for (int p : G.pred[j]) if (in_chain[p]) { dep = true; break; }
+      if (dep) break;
+      hoist.push_back(j);
+    }
+    if (chain.size() < 2) { out.push_back(A); used[i] = 1; continue; }
+    for (int h : hoist) { out.push_back(seq[h]); used[h] = 1; }
+    PTask F = seq[chain[0]];
+    F.phase_end = {(int)F.members.size()};
+    for (size_t c = 1; c < chain.size(); c++) {
+      const PTask& X = seq[chain[c]];
+      F.members.insert(F.members.end(), X.members.begin(), X.members.end());
+      F.member_act.insert(F.member_act.end(), X.member_act.begin(), X.member_act.end());
+      F.phase_end.push_back((int)F.members.size());
+    }
+    for (int c : chain) used[c] = 1;
+    st.chained += (int64_t)chain.size() - 1;
+    out.push_back(F);
+  }
+  seq.swap(out);
+}
+
 Plan optimize(const HLayout& L, const std::vector<PTask>& eager, uint32_t passes,
               const std::vector<char>& observed) {
   std::vector<PTask> seq = eager;
@@ -712,10 +783,12 @@ Plan optimize(const HLayout& L, const std::vector<PTask>& eager, uint32_t passes
       if (passes & SG_PASS_DSE) ch |= pass_dse(seq, observed, P.stats);
       if (!ch) break;
     }
+    if (passes & SG_PASS_CHAIN) pass_chain(L, seq, eager, P.stats);
   }
   for (const PTask& t : seq) {
     P.groups.push_back(t.members);
     P.acts.push_back(t.member_act);
+    P.phase_ends.push_back(t.phase_end.empty() ? std::vector<int>{(int)t.members.size()} : t.phase_end);
   }
   return P;
 }

@@ -64,18 +64,20 @@ struct PTask {
   int pos = 0;            // index in the eager lowered sequence
   std::vector<int> members;   // eager positions of the fused member tasks (in order)
   std::vector<uint32_t> member_act;
+  std::vector<int> phase_end; // SG_PASS_CHAIN: cumulative member counts at phase ends
   std::vector<Use> in, out;
 };
 
 struct PlanRecord { int group, type, call, snode; uint32_t act; int flags; };
 
 struct PlanStats {
-  int64_t listgens_removed = 0, demotions = 0, fused = 0, dead = 0;
+  int64_t listgens_removed = 0, demotions = 0, fused = 0, dead = 0, chained = 0;
 };
 
 struct Plan {
   std::vector<std::vector<int>> groups;        // eager positions per launch group
   std::vector<std::vector<uint32_t>> acts;     // effective act bits per member
+  std::vector<std::vector<int>> phase_ends;    // per group: cumulative member counts (1 entry unless chained)
   PlanStats stats;
 };
 

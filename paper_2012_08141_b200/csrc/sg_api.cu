@@ -50,6 +50,9 @@ struct sg_grid {
   std::vector<PlanRecord> last_plan;
   int64_t task_counter = 0;
   int num_sms = 148;
+  char* chain_buf = nullptr;        // SG_PASS_CHAIN op tables
+  size_t chain_bytes = 0;
+  std::vector<char> chain_host;
   uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
   uint64_t mig_tiles = 0;
   uint32_t* mig_ctl = nullptr;
@@ -508,7 +511,8 @@ static void make_op(const sg_grid* g, const PTask& t, uint32_t act, int loop_tre
     if (f >= 0 && f < (int)g->L.field_tree.size()) {
       o.nf = i + 1;
       if (!dt_set) { o.dt = g->L.field_dtype[f]; dt_set = true; }
-      if (g->L.field_tree[f] == loop_tree && loop_tree >= 0) o.slot[i] = g->L.field_slot[f];
+      // struct-for: slot in the iterated tree; range-for / serial: slot in the field's own tree
+      if (g->L.field_tree[f] >= 0 && (loop_tree < 0 || g->L.field_tree[f] == loop_tree)) o.slot[i] = g->L.field_slot[f];
       if (g->L.field_tree[f] < 0 && o.scalar < 0) o.scalar = g->L.field_scalar[f];
     }
   }
@@ -522,7 +526,7 @@ static int grid_hint_struct(const sg_grid* g, const DTree& T) {
 }
 
 static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const std::vector<uint32_t>& acts,
-                              sg_stats& st) {
+                              const std::vector<int>& phase_end, sg_stats& st) {
   const PTask& t0 = g->eager[members[0]];
   int task = (int)(g->task_counter++ & 0x7FFFFFFF);
   int rc = 0;
@@ -552,11 +556,39 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
     } break;
     case TT_STRUCT_FOR: {
       const DTree& T = g->dtrees[t0.tree];
-      DOp ops[SG_MAXOPS];
-      int nops = (int)members.size();
-      for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], t0.tree, ops[i]);
       const DList* drive = T.driving >= 0 ? &g->lists[t0.tree][T.driving] : nullptr;
-      rc = launch_struct_for(g->ctx, T, t0.tree, drive, ops, nops, task, g->stream, grid_hint_struct(g, T));
+      const int nops = (int)members.size();
+      if (phase_end.size() <= 1) {
+        DOp ops[SG_MAXOPS];
+        for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], t0.tree, ops[i]);
+        rc = launch_struct_for(g->ctx, T, t0.tree, drive, ops, nops, task, g->stream, grid_hint_struct(g, T),
+                               nullptr, nullptr, 1, 0);
+      } else {
+        // chain (SG_PASS_CHAIN): whole op table + phase ends to the device
+        std::vector<DOp> all(nops);
+        int nbr = 0;
+        for (int i = 0; i < nops; i++) {
+          make_op(g, g->eager[members[i]], acts[i], t0.tree, all[i]);
+          int op = all[i].op;
+          nbr |= op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER;
+        }
+        const size_t bytes = nops * sizeof(DOp) + phase_end.size() * sizeof(int) + 64;
+        if (bytes > g->chain_bytes) {
+          g->chain_buf = (char*)g->dev_alloc(std::max<size_t>(bytes, 64 * 1024));
+          if (!g->chain_buf) return fail(SG_ERR_CUDA, "chain op table allocation failed");
+          g->chain_bytes = std::max<size_t>(bytes, 64 * 1024);
+        }
+        // the host staging copy must stay valid until the async copy ran: one buffer per grid
+        g->chain_host.resize(bytes);
+        std::memcpy(g->chain_host.data(), all.data(), nops * sizeof(DOp));
+        std::memcpy(g->chain_host.data() + nops * sizeof(DOp), phase_end.data(), phase_end.size() * sizeof(int));
+        CUDA_TRY(cudaMemcpyAsync(g->chain_buf, g->chain_host.data(), bytes - 64, cudaMemcpyHostToDevice, g->stream));
+        const int last0 = phase_end[phase_end.size() - 2], nlast = nops - last0;
+        rc = launch_struct_for(g->ctx, T, t0.tree, drive, all.data() + last0, nlast, task, g->stream,
+                               grid_hint_struct(g, T), (const DOp*)g->chain_buf,
+                               (const int*)(g->chain_buf + nops * sizeof(DOp)), (int)phase_end.size(), nbr);
+        st.launches_chained++;
+      }
     } break;
     case TT_RANGE_FOR: {
       DOp ops[SG_MAXOPS];
@@ -603,7 +635,10 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
         }
       }
       RangeScratch rs{g->mig_status, g->mig_ctl};
-      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs);
+      const DTree* gt = nullptr;
+      if (tk.fields[0] >= 0 && tk.fields[0] < (int)g->L.field_tree.size() && g->L.field_tree[tk.fields[0]] >= 0)
+        gt = &g->dtrees[g->L.field_tree[tk.fields[0]]];
+      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt);
     } break;
     case TT_SERIAL: {
       DOp ops[SG_MAXOPS];
@@ -655,6 +690,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
   st.demotions = plan->stats.demotions;
   st.tasks_fused = plan->stats.fused;
   st.dead_removed = plan->stats.dead;
+  st.tasks_chained = plan->stats.chained;
   auto t1 = std::chrono::steady_clock::now();
   st.plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
   sg_status rc = SG_OK;
@@ -675,7 +711,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
     if (!rc) {
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (g->profiling) { e0 = g->get_event(); cudaEventRecord(e0, g->stream); }
-      rc = launch_group(g, mem, acts, st);
+      rc = launch_group(g, mem, acts, plan->phase_ends[gi], st);
       if (g->profiling) {
         e1 = g->get_event();
         cudaEventRecord(e1, g->stream);

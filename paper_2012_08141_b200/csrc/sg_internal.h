@@ -146,14 +146,17 @@ int launch_activate(const DevCtx& c, const DTree& t, int tree_id, int field, con
 int launch_listgen(const DevCtx& c, const DTree& t, int tree_id, int level, int parent_level,
                    const DList* parent, const DList& out, int task_id, void* stream, int grid_hint);
 int launch_clear_list(const DList& l, void* stream);
+// nphases > 1: a chain (SG_PASS_CHAIN) -- `ops` are the LAST phase's ops (reductions),
+// the whole op table and the phase ends are in device memory.
 int launch_struct_for(const DevCtx& c, const DTree& t, int tree_id, const DList* drive, const DOp* ops, int nops,
-                      int task_id, void* stream, int grid_hint);
+                      int task_id, void* stream, int grid_hint, const DOp* dev_optab, const int* dev_phase_end,
+                      int nphases, int chain_needs_nbr);
 struct RangeScratch {
   uint64_t* status;   // look-back descriptors for G2P_MIGRATE tiles
   uint32_t* ctl;      // [0..3] migrate tile/done/epoch/count, [5] append ticket
 };
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task_id,
-                     void* stream, const RangeScratch* rs);
+                     void* stream, const RangeScratch* rs, const DTree* grid_tree);
 int launch_serial(const DevCtx& c, const DOp* ops, int nops, int task_id, void* stream);
 int launch_deactivate(const DevCtx& c, const DTree& t, int tree_id, int level, const DList* lists,
                       int task_id, void* stream);

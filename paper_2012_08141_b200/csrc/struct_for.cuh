@@ -100,7 +100,7 @@ __device__ __forceinline__ void warp_add(int o, V v) {
 }
 
 template <typename V>
-__device__ void finish_reductions(const SFArgs& A) {
+__device__ void finish_reductions(const SFArgs& A, const DOp* ops, int nops) {
   __shared__ bool s_last;
   __shared__ double s_sum[SF_TPB];
   __syncthreads();
@@ -112,8 +112,8 @@ __device__ void finish_reductions(const SFArgs& A) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int o = 0; o < A.nops; o++) {
-    if (A.ops[o].op != SG_OP_REDUCE_SUM) continue;
+  for (int o = 0; o < nops; o++) {
+    if (ops[o].op != SG_OP_REDUCE_SUM) continue;
     double t = 0.0;   // fixed-order tree sum over CTAs
     for (int b = threadIdx.x; b < G; b += SF_TPB) t += *(volatile double*)&A.C.partials[o * A.C.max_grid + b];
     s_sum[threadIdx.x] = t;
@@ -382,11 +382,11 @@ __device__ __forceinline__ Q4<V> nbr_sum4(const NbrLoads<V, ND>& L, const Q4<V>&
 }
 
 template <typename V, int ND, bool PAIR, int GL>
-__device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, uint32_t* P, uint32_t nq, uint32_t lq,
-                                          bool chunked, uint32_t jbase, uint64_t fs) {
+__device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int nops, const SFTile& tile, uint32_t* P,
+                                          uint32_t nq, uint32_t lq, bool chunked, uint32_t jbase, uint64_t fs) {
   const QG g = make_qg<GL>(A);
-  for (int o = 0; o < A.nops; o++) {
-    const DOp& op = A.ops[o];
+  for (int o = 0; o < nops; o++) {
+    const DOp& op = ops[o];
     const uint64_t s0 = (uint64_t)op.slot[0] * fs, s1 = (uint64_t)(op.slot[1] < 0 ? 0 : op.slot[1]) * fs,
                    s2 = (uint64_t)(op.slot[2] < 0 ? 0 : op.slot[2]) * fs;
     switch (op.op) {
@@ -510,12 +510,12 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const SFTile& tile, u
 }
 
 template <typename V>
-__device__ __forceinline__ void run_cells(const SFArgs& A, const SFTile& tile, uint32_t* P, uint32_t tcells,
-                                          bool chunked, uint32_t jbase, uint64_t fs) {
+__device__ __forceinline__ void run_cells(const SFArgs& A, const DOp* ops, int nops, const SFTile& tile, uint32_t* P,
+                                          uint32_t tcells, bool chunked, uint32_t jbase, uint64_t fs) {
   const DTree& T = A.T;
   const int lblk = T.lblk;
-  for (int o = 0; o < A.nops; o++) {
-    const DOp& op = A.ops[o];
+  for (int o = 0; o < nops; o++) {
+    const DOp& op = ops[o];
     V acc = V(0);
     if (op.op == SG_OP_HALO_PACK) {
       int nf = 0;
@@ -560,19 +560,14 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const SFTile& tile, u
 }
 
 // ---------------------------------------------------------------------------
-// the kernel
+// the kernels
 // ---------------------------------------------------------------------------
-// ND = 0: GENERIC cell path; 1..3: QUAD path.  PAIR: two stencil quads in
-// flight per thread (more registers, fewer resident CTAs).
-// GL: 0 runtime block shape, 1 = 8^3, 2 = 4^3, 3 = 4x4 (constant index math).
+// One pass over every tile of the list with the given op list.
 template <typename V, int ND, bool PAIR, int GL>
-__global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __grid_constant__ SFArgs A) {
-  __shared__ SFTile tile;
+__device__ __forceinline__ void sf_tiles(const SFArgs& A, const DOp* ops, int nops, SFTile& tile, bool rows_ok) {
   const DTree& T = A.T;
   uint32_t* P = T.seg[T.nseg - 1].base;
-  if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
   const uint32_t nent = A.entries ? *A.count : 1u;
-  const bool rows_ok = A.table && *(volatile uint32_t*)&A.table_ctl[4] != 0u;
   const int lblk = T.lblk;
   const bool chunked = lblk > A.ltile;
   uint64_t ntiles;
@@ -663,13 +658,16 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
     }
     __syncthreads();
     if (ND > 0)
-      run_quads<V, (ND > 0 ? ND : 1), PAIR, GL>(A, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked, jbase, fs);
-    else run_cells<V>(A, tile, P, tcells, chunked, jbase, fs);
+      run_quads<V, (ND > 0 ? ND : 1), PAIR, GL>(A, ops, nops, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked,
+                                                jbase, fs);
+    else run_cells<V>(A, ops, nops, tile, P, tcells, chunked, jbase, fs);
     __syncthreads();
   }
-  if (A.has_reduce) finish_reductions<V>(A);
+}
+
+// Marks the block table built (last CTA) when this launch built it.
+__device__ __forceinline__ void sf_mark_table(const SFArgs& A, bool rows_ok) {
   if (A.table && !rows_ok && threadIdx.x == 0) {
-    // the last CTA marks the table complete for this list version
     __threadfence();
     if (atomicAdd(&A.table_ctl[3], 1u) == gridDim.x - 1) {
       A.table_ctl[3] = 0u;
@@ -677,4 +675,51 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
       A.table_ctl[4] = 1u;
     }
   }
+}
+
+// ND = 0: GENERIC cell path; 1..3: QUAD path.  PAIR: two stencil quads in
+// flight per thread (more registers, fewer resident CTAs).
+// GL: 0 runtime block shape, 1 = 8^3, 2 = 4^3, 3 = 4x4 (constant index math).
+template <typename V, int ND, bool PAIR, int GL>
+__global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __grid_constant__ SFArgs A) {
+  __shared__ SFTile tile;
+  if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
+  const bool rows_ok = A.table && *(volatile uint32_t*)&A.table_ctl[4] != 0u;
+  sf_tiles<V, ND, PAIR, GL>(A, A.ops, A.nops, tile, rows_ok);
+  if (A.has_reduce) finish_reductions<V>(A, A.ops, A.nops);
+  sf_mark_table(A, rows_ok);
+}
+
+// Beyond the paper (SG_PASS_CHAIN): a chain of struct-for phases
+// over one list in ONE cooperative launch; phase p+1 starts after a grid-wide
+// barrier, so dependent stencils (Jacobi sweeps) chain without a kernel
+// boundary.  Op table and phase ends come from device memory; reductions are
+// allowed in the last phase only (their aux / s_red slots are that phase's).
+template <typename V, int ND, bool PAIR, int GL>
+__global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5)
+    k_struct_chain(const __grid_constant__ SFArgs A, const DOp* __restrict__ optab, const int* __restrict__ phase_end,
+                   int nphases) {
+  __shared__ SFTile tile;
+  __shared__ DOp s_ops[SG_MAXOPS];
+  cg::grid_group grid = cg::this_grid();
+  if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
+  const bool rows_ok0 = A.table && *(volatile uint32_t*)&A.table_ctl[4] != 0u;
+  int begin = 0;
+  int last_n = 0;
+  for (int p = 0; p < nphases; p++) {
+    const int end = phase_end[p], n = end - begin;
+    for (int i = threadIdx.x; i < n * (int)(sizeof(DOp) / 4); i += SF_TPB)
+      reinterpret_cast<uint32_t*>(s_ops)[i] = reinterpret_cast<const uint32_t*>(optab + begin)[i];
+    __syncthreads();
+    // rows built by phase 0 are visible to the later phases after the barrier
+    sf_tiles<V, ND, PAIR, GL>(A, s_ops, n, tile, rows_ok0 || p > 0);
+    last_n = n;
+    begin = end;
+    if (p + 1 < nphases) {
+      __threadfence();
+      grid.sync();
+    }
+  }
+  if (A.has_reduce) finish_reductions<V>(A, s_ops, last_n);
+  sf_mark_table(A, rows_ok0);
 }

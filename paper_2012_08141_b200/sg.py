@@ -30,7 +30,8 @@ OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6
 CLEAR_VALUES, DEACTIVATE = 0, 1
 PASS_LISTGEN_REMOVAL, PASS_ACT_DEMOTION, PASS_FUSION, PASS_DSE = 1, 2, 4, 8
 PASS_ALL = 15
-PASS_NAMES = {"none": 0, "all": 15, "listgen": 1, "demotion": 2, "fusion": 4, "dse": 8}
+PASS_CHAIN = 16
+PASS_NAMES = {"none": 0, "all": 15, "listgen": 1, "demotion": 2, "fusion": 4, "dse": 8, "chain": 16}
 ERRORS = {0: "OK", -1: "ARG", -2: "LAYOUT", -3: "RANGE", -4: "CUDA", -5: "NCCL", -6: "DEMOTION_TRAP",
           -7: "OVERFLOW", -8: "POOL_EXHAUSTED", -9: "LIST_OVERFLOW", -10: "STATE"}
 TASK_TYPES = ["activate", "listgen", "clear_list", "struct_for", "range_for", "serial", "deactivate"]
@@ -62,7 +63,7 @@ class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "tasks_lowered", "launches", "listgen_launched", "clear_list_launched", "listgens_removed",
         "demotions", "tasks_fused", "dead_removed", "plan_cache_hits", "plan_cache_misses")] + [
-        ("plan_us", ctypes.c_double)]
+        ("plan_us", ctypes.c_double), ("tasks_chained", ctypes.c_int64), ("launches_chained", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
