@@ -254,6 +254,36 @@ def _timed_flushes(grid, enqueue, steps, warmup, l2=None):
     return ms / steps, st
 
 
+def measure_c2_chain(steps=20, warmup=5):
+    """Beyond the paper (SG_PASS_CHAIN): the same C2 solve with the
+    dependent Jacobi sweeps chained in one cooperative launch."""
+    import torch
+    from paper_2012_08141_b200 import sg
+    L, lv, coords, calls, result = c2_setup(50)
+    g = sg.Grid(L.desc())
+    dc = torch.as_tensor(coords).cuda()
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        enqueue_calls(g, calls, dc)
+        g.flush("all+chain")
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        l2.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        enqueue_calls(g, calls, dc)
+        st = g.flush("all+chain")
+        b.record(stream)
+        b.synchronize()
+        ms += a.elapsed_time(b)
+    ms /= steps
+    return {"solves_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
+            "tasks_chained": st["tasks_chained"], "result_s": float(g.field(L.fields["s"])),
+            "note": "beyond the paper: dependent stencils chained with grid-wide barriers"}
+
+
 def measure_c1(steps=200, warmup=10):
     """C1: 2D 64^2 disk, the 8-task stream (launch-latency bound)."""
     import torch
@@ -431,8 +461,8 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "scripts"))
             import xl_bench
             extra = {}
-            for name, fn in (("c1", measure_c1), ("c3", measure_c3), ("jac_xl", xl_bench.jac_xl),
-                             ("lg_xl", xl_bench.lg_xl)):
+            for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3),
+                             ("jac_xl", xl_bench.jac_xl), ("lg_xl", xl_bench.lg_xl)):
                 try:
                     extra[name] = fn()
                 except Exception as e:  # keep the main line even if an extra fails

@@ -285,6 +285,7 @@ struct LGArgs {
   DevCtx C;
   int ls, lp, mode;     // mode 0: root parent, 1: parent in same segment, 2: parent pointer of previous segment
   int lratio, lcpp, nbits;
+  int fast8;            // bitmasked level with >= 8 aligned word-chunks per parent entry
   const uint32_t* pentries;
   const uint32_t* pcount;
   DList out;
@@ -346,11 +347,50 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
     if (tile >= ntiles) break;
     uint32_t bits[LG_CPT], cs[LG_CPT], fs[LG_CPT];
     uint32_t cnt = 0;
+    const uint64_t ch0 = (uint64_t)tile * LG_TILE + threadIdx.x * LG_CPT;
+    if (a.fast8 && ch0 + LG_CPT <= nchunks) {
+      // bitmasked level, >= 8 word-chunks per parent entry: the thread's 8 chunks
+      // share one parent, so decode it once and fetch the 8 mask words with two
+      // 16-byte loads
+      uint32_t c0, f0;
+      const uint32_t p = (uint32_t)(ch0 >> a.lcpp), sub = (uint32_t)(ch0 & ((1u << a.lcpp) - 1u));
+      const DLevel& S = a.T.lev[a.ls];
+      const DLevel& P = a.T.lev[a.lp < 0 ? 0 : a.lp];
+      const uint32_t* cont = nullptr;
+      if (a.mode == 0) {
+        c0 = 0; f0 = sub * 32u; cont = a.T.seg[0].base;
+      } else {
+        const uint32_t e = a.pentries[p];
+        const uint32_t ps = e >> P.ln, pidx = e & ((1u << P.ln) - 1u);
+        if (a.mode == 1) {
+          c0 = ps; f0 = (pidx << a.lratio) + sub * 32u; cont = cont_ptr(a.T, S.seg, ps);
+        } else {
+          const uint32_t v = cont_ptr(a.T, P.seg, ps)[P.slot_off + pidx];
+          const bool ok = v != SG_SLOT_NULL && v != SG_SLOT_BUSY;
+          c0 = ok ? v - 1u : 0u; f0 = sub * 32u; cont = ok ? cont_ptr(a.T, S.seg, c0) : nullptr;
+        }
+      }
+      uint4 w0 = make_uint4(0u, 0u, 0u, 0u), w1 = w0;
+      if (cont) {
+        const uint4* q = reinterpret_cast<const uint4*>(cont + S.mask_off + (f0 >> 5));
+        w0 = q[0];
+        w1 = q[1];
+      }
+      bits[0] = w0.x; bits[1] = w0.y; bits[2] = w0.z; bits[3] = w0.w;
+      bits[4] = w1.x; bits[5] = w1.y; bits[6] = w1.z; bits[7] = w1.w;
 #pragma unroll
-    for (int k = 0; k < LG_CPT; k++) {
-      uint64_t ch = (uint64_t)tile * LG_TILE + threadIdx.x * LG_CPT + k;
-      bits[k] = ch < nchunks ? lg_chunk(a, ch, cs[k], fs[k]) : 0u;
-      cnt += __popc(bits[k]);
+      for (int k = 0; k < LG_CPT; k++) {
+        cs[k] = c0;
+        fs[k] = f0 + 32u * k;
+        cnt += __popc(bits[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < LG_CPT; k++) {
+        uint64_t ch = ch0 + k;
+        bits[k] = ch < nchunks ? lg_chunk(a, ch, cs[k], fs[k]) : 0u;
+        cnt += __popc(bits[k]);
+      }
     }
     // block exclusive scan
     uint32_t inc = cnt;
@@ -704,6 +744,9 @@ int launch_listgen(const DevCtx& c, const DTree& t, int, int level, int parent_l
   a.lratio = lratio;
   a.lcpp = lratio > 5 ? lratio - 5 : 0;
   a.nbits = lratio >= 5 ? 32 : (1 << lratio);
+  // 8 chunks of one parent are 8 consecutive mask words, 16-byte aligned when the
+  // level's mask region is (mask_off % 4 == 0) -- see derive_tree
+  a.fast8 = S.kind == SG_BITMASKED && a.lcpp >= 3 && (S.mask_off % 4) == 0;
   a.pentries = parent ? parent->entries : nullptr;
   a.pcount = parent ? parent->count : nullptr;
   int grid = grid_hint > 0 ? grid_hint : 1;
@@ -765,7 +808,7 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   // tile: 2048 cells (at most SF_MAXE blocks); larger blocks span several tiles
   const int TILE_LOG = 11;
   a->ltile = TILE_LOG;
-  a->lept = lblk >= TILE_LOG ? 0 : std::min(TILE_LOG - lblk, 8);
+  a->lept = 8;   // entries per tile chosen on the device (<= 256), see sf_tiles
   // QUAD path: the block is a single level whose fastest axis has extent >= 4
   bool quad = false;
   a->lb[0] = a->lb[1] = a->lb[2] = 0;
@@ -774,8 +817,10 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
     for (int d = 0; d < 3; d++) a->lb[d] = B.le[d];
     quad = B.le[t.nd - 1] >= 2;
   }
-  int grid = grid_hint > 0 ? grid_hint : num_sms() * 8;
-  grid = max(1, min(grid, num_sms() * 8));
+  // one resident wave: 5 CTAs per SM (__launch_bounds__(SF_TPB, 5)); tiles are
+  // sized on the device so every CTA gets an equal share
+  (void)grid_hint;
+  int grid = num_sms() * 5;
   cudaStream_t s = (cudaStream_t)stream;
   const int nd = quad ? t.nd : 0;
   static int pair = -1;

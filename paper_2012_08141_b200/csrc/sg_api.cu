@@ -238,6 +238,7 @@ static sg_status derive_tree(sg_grid* g, int tid, DTree& T) {
       ln += D.lE;
       D.ln = ln;
       if (D.kind == SG_BITMASKED) {
+        words = (words + 3) & ~3ull;   // 16-byte aligned mask regions (vector loads in listgen)
         D.mask_off = (uint32_t)words;
         words += std::max<uint64_t>(1, ((1ull << ln) + 31) / 32);
       }

@@ -564,19 +564,26 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const DOp* ops, int n
 // ---------------------------------------------------------------------------
 // One pass over every tile of the list with the given op list.
 template <typename V, int ND, bool PAIR, int GL>
-__device__ __forceinline__ void sf_tiles(const SFArgs& A, const DOp* ops, int nops, SFTile& tile, bool rows_ok) {
+__device__ __forceinline__ void sf_tiles(const SFArgs& A, const DOp* ops, int nops, SFTile& tile, bool rows_ok,
+                                         bool tile_cached = false) {
   const DTree& T = A.T;
   uint32_t* P = T.seg[T.nseg - 1].base;
   const uint32_t nent = A.entries ? *A.count : 1u;
   const int lblk = T.lblk;
   const bool chunked = lblk > A.ltile;
   uint64_t ntiles;
-  uint32_t tiles_per_entry = 1;
+  uint32_t tiles_per_entry = 1, ept = 1;
   if (chunked) {
     tiles_per_entry = 1u << (lblk - A.ltile);
     ntiles = (uint64_t)nent * tiles_per_entry;
   } else {
-    ntiles = ((uint64_t)nent + (1u << A.lept) - 1) >> A.lept;
+    // entries per tile from the device-side count: k equal waves of tiles over
+    // the resident grid (no wave-quantization tail), at most SF_MAXE and at
+    // most 2^lept entries per tile
+    const uint32_t G = gridDim.x, cap = min((uint32_t)SF_MAXE, 1u << A.lept);
+    const uint32_t k = max(1u, (nent + cap * G - 1) / (cap * G));
+    ept = max(1u, (nent + k * G - 1) / (k * G));
+    ntiles = ((uint64_t)nent + ept - 1) / ept;
   }
   const uint64_t fs = 1ull << T.ln_leaf;
 
@@ -588,14 +595,17 @@ __device__ __forceinline__ void sf_tiles(const SFArgs& A, const DOp* ops, int no
       jbase = (uint32_t)(t % tiles_per_entry) << A.ltile;
       tcells = 1u << A.ltile;
     } else {
-      e0 = (uint32_t)(t << A.lept);
-      ne = min(1u << A.lept, nent - e0);
+      e0 = (uint32_t)t * ept;
+      ne = min(ept, nent - e0);
       tcells = ne << lblk;
     }
     // the tile's blocks: one coalesced read of the list's block table, or --
     // first struct-for after a listgen -- built here (tree walks spread over
-    // every CTA) and stored for the following launches
-    if (A.entries && rows_ok) {
+    // every CTA) and stored for the following launches.  In a chain whose
+    // tiles all fit in one wave, every phase reuses the CTA's tile as loaded.
+    if (tile_cached && ntiles <= gridDim.x) {
+      // shared memory already holds tile t == blockIdx.x from the previous phase
+    } else if (A.entries && rows_ok) {
       for (uint32_t i = threadIdx.x; i < ne; i += SF_TPB) {
         const BlockRow r = A.table[e0 + i];
         tile.blk[i] = r.blk;
@@ -712,7 +722,7 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5)
       reinterpret_cast<uint32_t*>(s_ops)[i] = reinterpret_cast<const uint32_t*>(optab + begin)[i];
     __syncthreads();
     // rows built by phase 0 are visible to the later phases after the barrier
-    sf_tiles<V, ND, PAIR, GL>(A, s_ops, n, tile, rows_ok0 || p > 0);
+    sf_tiles<V, ND, PAIR, GL>(A, s_ops, n, tile, rows_ok0 || p > 0, p > 0);
     last_n = n;
     begin = end;
     if (p + 1 < nphases) {

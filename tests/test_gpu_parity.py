@@ -61,7 +61,7 @@ def test_c1(passes, dtype, disk):
     assert st[0]["launches"] == (8 if passes == 0 else 5)
 
 
-@pytest.mark.parametrize("passes", [0, "all"])
+@pytest.mark.parametrize("passes", [0, "all", "all+chain"])
 def test_c2_small(passes):
     prog = W.c2_small_program(iters=6)
     g, st = sg.run_program(prog, passes=passes)
@@ -85,7 +85,7 @@ def test_c2_small_lists_and_fig_counts():
 def test_fuzz_programs(seed):
     prog = W.fuzz_program(seed)
     o = oracle.run_program(prog)
-    for passes in (0, "all", "listgen+demotion", "fusion+dse"):
+    for passes in (0, "all", "listgen+demotion", "fusion+dse", "all+chain"):
         g, _ = sg.run_program(prog, passes=passes, debug=True)
         compare(g, o, prog)
         g.close()

@@ -187,6 +187,29 @@ def test_c1_c2_launch_counts():
     assert st0[0]["launches"] == 161
 
 
+def test_chain_pass_beyond_paper():
+    # SG_PASS_CHAIN (beyond PAPER.md:367-368): the 50 dependent
+    # JACOBI sweeps become phases of one cooperative launch; the independent
+    # scalar clear is hoisted in front of the chain.
+    st, plans = plan_counts(W.c2_program(), passes="all+chain")
+    assert st[0]["launches"] == 5 and st[0]["tasks_chained"] == 50
+    assert types_of(plans[0])[:4] == ["activate", "listgen", "listgen", "serial"]
+    assert len(set(plans[0][4:, 0])) == 1           # one group holds every struct-for
+    # without the flag nothing changes
+    st2, _ = plan_counts(W.c2_program(), passes="all")
+    assert st2[0]["launches"] == 55 and st2[0]["tasks_chained"] == 0
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_chain_schedule_soundness_on_oracle(seed):
+    prog = W.fuzz_program(seed)
+    ref = oracle.run_program(prog)
+    o = replay_plan_on_oracle(prog, 15 | 16)
+    L = prog["layout"]
+    for name, fid in L.fields.items():
+        assert np.array_equal(o.field(fid), ref.field(fid)), (seed, name)
+
+
 def test_plan_is_topological_and_deterministic():
     p1 = plan_counts(W.c2_program())[1][0]
     p2 = plan_counts(W.c2_program())[1][0]
