@@ -58,7 +58,8 @@ enum {
   OP_FILL = 1, OP_ADD_CONST = 2, OP_INC = 3, OP_AXPY = 4, OP_STENCIL = 5,
   OP_JACOBI = 6, OP_REDUCE_SUM = 7, OP_DOWNSAMPLE = 8, OP_JITTER = 9,
   OP_CLEAR_SCALAR = 10,
-  OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22
+  OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22,
+  OP_GRID_OP_SPLIT = 27, OP_LOSS_MEAN = 28, OP_ADJ_INIT = 29, OP_G2P_ADJ = 30, OP_P2G_ADJ = 31
 };
 
 typedef std::array<int64_t, 3> Coord;
@@ -97,6 +98,7 @@ struct Grid {
   std::map<int, std::vector<Coord>> lists;   // level -> last generated list
   std::map<int, int64_t> allocated, freed;   // pointer level -> counters
   int64_t tasks = 0, listgens = 0;
+  bool exact = false;   // f64 storage (no f32 rounding): finite-difference pins of the adjoints
   std::string err;
   // per-task bookkeeping: cells whose value must be rounded to storage type
   std::set<std::pair<int, Coord>> touched;
@@ -291,7 +293,7 @@ int end_task(Grid* g) {
     if (it == fl.val.end()) continue;
     double v = it->second;
     if (fl.dtype == T_F32) {
-      it->second = (double)(float)v;
+      if (!g->exact) it->second = (double)(float)v;
     } else {
       if (v != std::floor(v) || v > 2147483647.0 || v < -2147483648.0) {
         g->touched.clear();
@@ -409,6 +411,9 @@ int field_ok(Grid* g, int f) { return f >= 0 && f < (int)g->fields.size(); }
 // race-free by construction, so sequential order equals any parallel order up
 // to float reassociation.
 // ---------------------------------------------------------------------------
+void grid_update(double p[3], double m, const int node[3], double dt, double grav, double bound, double ng, int D,
+                 double u[3], double mask[3]);
+
 int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const float* p, int np,
                uint32_t activating) {
   if (leaf_snode <= 0 || leaf_snode >= (int)g->nodes.size()) return fail(g, E_ARG, "bad snode");
@@ -529,6 +534,26 @@ int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const 
         for (int a = 0; a < 3 && !rc; a++) rc = write(g, f[a], c, v[a], false, mv[a]);
       });
       break;
+    case OP_GRID_OP_SPLIT:
+      // Grid update with separate output (C4 keeps the momentum for the
+      // adjoint): f0..f2 momentum, f3 mass (read), f4..f6 velocity (written).
+      // p0 dt, p1 gravity, p2 bound, p3 n_grid.
+      if (!need(7)) return fail(g, E_ARG, "GRID_OP_SPLIT needs 7 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        if (rc) return;
+        double pp[3], u[3], mask[3];
+        for (int r = 0; r < 3; r++) pp[r] = read(g, f[r], c);
+        const double m = read(g, f[3], c), mm = read_mag(g, f[3], c);
+        int nd[3] = {(int)c[0], (int)c[1], (int)c[2]};
+        grid_update(pp, m, nd, P(0), P(1), P(2), P(3), D, u, mask);
+        for (int r = 0; r < 3 && !rc; r++) {
+          double mp = read_mag(g, f[r], c);
+          double mu = m > 0 ? (mp + std::fabs(pp[r]) * (mm / m)) / m : mp;
+          if (r == 1) mu += std::fabs(P(0) * P(1));
+          rc = write(g, f[4 + r], c, u[r], false, mask[r] * mu);
+        }
+      });
+      break;
     default:
       return fail(g, E_ARG, "unknown struct-for op");
   }
@@ -545,24 +570,43 @@ int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const 
 // ---------------------------------------------------------------------------
 struct Kernel {
   int base[3];
-  double fx[3], w[3][3];
+  double fx[3], w[3][3], dw[3][3];
 };
 
-Kernel bspline(const float xp[3], float inv_dx) {
+Kernel bspline(const float xp[3], float inv_dx, const double* x64 = nullptr) {
   Kernel k;
   for (int a = 0; a < 3; a++) {
     volatile float X = xp[a] * inv_dx;          // f32 rounding, no contraction
     volatile float Xm = X - 0.5f;
     k.base[a] = (int)std::floor((float)Xm);
     volatile float fx = X - (float)k.base[a];
-    k.fx[a] = (double)(float)fx;
+    // exact mode (f64 storage, finite-difference pins): same base, f64 fraction
+    k.fx[a] = x64 ? x64[a] * (double)inv_dx - (double)k.base[a] : (double)(float)fx;
     double q = k.fx[a];
     k.w[0][a] = 0.5 * (1.5 - q) * (1.5 - q);
     k.w[1][a] = 0.75 - (q - 1.0) * (q - 1.0);
     k.w[2][a] = 0.5 * (q - 0.5) * (q - 0.5);
+    // d w / d fx
+    k.dw[0][a] = q - 1.5;
+    k.dw[1][a] = -2.0 * (q - 1.0);
+    k.dw[2][a] = q - 0.5;
   }
   return k;
 }
+
+// Grid velocity after the grid update (mpm3d grid op, reading R28), from the
+// pre-update momentum p and mass m of a node; mask[r] = 0 where the wall
+// condition zeroed component r.
+void grid_update(double p[3], double m, const int node[3], double dt, double grav, double bound, double ng, int D,
+                 double u[3], double mask[3]) {
+  for (int r = 0; r < 3; r++) u[r] = m > 0 ? p[r] / m : p[r];
+  u[1] -= dt * grav;
+  for (int r = 0; r < 3; r++) {
+    mask[r] = 1.0;
+    if (r < D && ((node[r] < bound && u[r] < 0) || (node[r] > ng - bound && u[r] > 0))) { u[r] = 0.0; mask[r] = 0.0; }
+  }
+}
+
 
 double& A_(Grid* g, int arr, int comp, int64_t i) { Array& a = g->arrays[arr]; return a.val[comp * a.n + i]; }
 double& M_(Grid* g, int arr, int comp, int64_t i) { Array& a = g->arrays[arr]; return a.mag[comp * a.n + i]; }
@@ -572,23 +616,39 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
   auto P = [&](int i) { return i < np ? (double)p[i] : 0.0; };
   for (int i = 0; i < na; i++)
     if (ar[i] < 0 || ar[i] >= (int)g->arrays.size()) return fail(g, E_ARG, "bad array");
-  for (int i = 0; i < nf; i++) if (!field_ok(g, f[i])) return fail(g, E_ARG, "bad field");
-  if (nf < 4 || na < 4) return fail(g, E_ARG, "MPM ops need 4 fields and 4 arrays");
-  for (int i = 0; i < 4; i++)
+  for (int i = 0; i < nf; i++) if (f[i] >= 0 && !field_ok(g, f[i])) return fail(g, E_ARG, "bad field");
+  for (int i = 0; i < na; i++)
     if (g->arrays[ar[i]].n < n) return fail(g, E_ARG, "array shorter than range");
   int rc = OK;
   const float inv_dx = (float)P(1);
-  const double dx = 1.0 / (double)inv_dx;
-  std::vector<std::pair<int, int64_t>> touched_arr;
+  const double dx = 1.0 / (double)inv_dx, idx = (double)inv_dx, s4 = 4.0 * idx * idx;
+  auto kernel_of = [&](int arr, int64_t i) {
+    float xp[3] = {(float)A_(g, arr, 0, i), (float)A_(g, arr, 1, i), (float)A_(g, arr, 2, i)};
+    double x64[3] = {A_(g, arr, 0, i), A_(g, arr, 1, i), A_(g, arr, 2, i)};
+    return bspline(xp, inv_dx, g->exact ? x64 : nullptr);
+  };
+  // node weight, its gradient d W / d x, and dpos for offset (a, b, c)
+  auto node_w = [&](const Kernel& k, int a, int b, int c, double& W, double gW[3], double dpos[3]) {
+    int off[3] = {a, b, c};
+    W = k.w[a][0] * k.w[b][1] * k.w[c][2];
+    gW[0] = idx * k.dw[a][0] * k.w[b][1] * k.w[c][2];
+    gW[1] = idx * k.w[a][0] * k.dw[b][1] * k.w[c][2];
+    gW[2] = idx * k.w[a][0] * k.w[b][1] * k.dw[c][2];
+    for (int d = 0; d < 3; d++) dpos[d] = ((double)off[d] - k.fx[d]) * dx;
+  };
+  auto round_arrays = [&](std::initializer_list<int> ids) {
+    if (g->exact) return;
+    for (int id : ids) for (double& v : g->arrays[id].val) v = (double)(float)v;
+  };
   switch (op) {
     case OP_P2G: {
       // p0 dt, p1 inv_dx, p2 p_mass, p3 p_vol, p4 E
+      if (nf < 4 || na < 4) return fail(g, E_ARG, "P2G needs 4 fields and 4 arrays");
       const double dt = P(0), pm = P(2), pv = P(3), E = P(4);
       for (int64_t i = 0; i < n && !rc; i++) {
-        float xp[3] = {(float)A_(g, ar[0], 0, i), (float)A_(g, ar[0], 1, i), (float)A_(g, ar[0], 2, i)};
-        Kernel k = bspline(xp, inv_dx);
+        Kernel k = kernel_of(ar[0], i);
         double J = A_(g, ar[3], 0, i);
-        double stress = -dt * 4.0 * E * pv * (J - 1.0) * (double)inv_dx * (double)inv_dx;
+        double stress = -dt * 4.0 * E * pv * (J - 1.0) * idx * idx;
         double aff[3][3], v[3];
         for (int r = 0; r < 3; r++) {
           v[r] = A_(g, ar[1], r, i);
@@ -597,39 +657,39 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
         for (int a = 0; a < 3 && !rc; a++)
           for (int b = 0; b < 3 && !rc; b++)
             for (int c = 0; c < 3 && !rc; c++) {
-              int off[3] = {a, b, c};
-              double dpos[3], wgt = k.w[a][0] * k.w[b][1] * k.w[c][2];
-              for (int d = 0; d < 3; d++) dpos[d] = ((double)off[d] - k.fx[d]) * dx;
+              double W, gW[3], dpos[3];
+              node_w(k, a, b, c, W, gW, dpos);
               Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
               for (int r = 0; r < 3 && !rc; r++) {
                 double mom = pm * v[r];
                 for (int d = 0; d < 3; d++) mom += aff[r][d] * dpos[d];
-                rc = atomic_add(g, f[r], node, wgt * mom, act_bit(activating, r));
+                rc = atomic_add(g, f[r], node, W * mom, act_bit(activating, r));
               }
-              if (!rc) rc = atomic_add(g, f[3], node, wgt * pm, act_bit(activating, 3));
+              if (!rc) rc = atomic_add(g, f[3], node, W * pm, act_bit(activating, 3));
             }
       }
     } break;
     case OP_G2P: {
-      // p0 dt, p1 inv_dx.  Reads grid velocity; writes v, C, x, J.
+      // p0 dt, p1 inv_dx.  Reads grid velocity f0..f2 at the particle state a0..a3
+      // and writes the new state to a4..a7 (in place when a4 is absent).
+      if (nf < 3 || na < 4) return fail(g, E_ARG, "G2P needs 3 fields and 4 arrays");
       const double dt = P(0);
+      const int o0 = na >= 8 ? 4 : 0;
       for (int64_t i = 0; i < n; i++) {
-        float xp[3] = {(float)A_(g, ar[0], 0, i), (float)A_(g, ar[0], 1, i), (float)A_(g, ar[0], 2, i)};
-        Kernel k = bspline(xp, inv_dx);
+        Kernel k = kernel_of(ar[0], i);
         double nv[3] = {0, 0, 0}, mv[3] = {0, 0, 0}, nC[3][3] = {{0}}, mC[3][3] = {{0}};
         for (int a = 0; a < 3; a++)
           for (int b = 0; b < 3; b++)
             for (int c = 0; c < 3; c++) {
-              int off[3] = {a, b, c};
-              double dpos[3], wgt = k.w[a][0] * k.w[b][1] * k.w[c][2];
-              for (int d = 0; d < 3; d++) dpos[d] = ((double)off[d] - k.fx[d]) * dx;
+              double W, gW[3], dpos[3];
+              node_w(k, a, b, c, W, gW, dpos);
               Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
               for (int r = 0; r < 3; r++) {
                 double gv = read(g, f[r], node), gm = read_mag(g, f[r], node) + std::fabs(gv);
-                nv[r] += wgt * gv;
-                mv[r] += std::fabs(wgt) * gm;
+                nv[r] += W * gv;
+                mv[r] += std::fabs(W) * gm;
                 for (int d = 0; d < 3; d++) {
-                  double s = 4.0 * (double)inv_dx * (double)inv_dx * wgt * dpos[d];
+                  double s = s4 * W * dpos[d];
                   nC[r][d] += s * gv;
                   mC[r][d] += std::fabs(s) * gm;
                 }
@@ -637,22 +697,175 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
             }
         double tr = nC[0][0] + nC[1][1] + nC[2][2];
         double mtr = mC[0][0] + mC[1][1] + mC[2][2];
+        const double J = A_(g, ar[3], 0, i);
         for (int r = 0; r < 3; r++) {
           double x = A_(g, ar[0], r, i);
-          A_(g, ar[1], r, i) = nv[r]; M_(g, ar[1], r, i) = mv[r];
-          A_(g, ar[0], r, i) = x + dt * nv[r];
-          M_(g, ar[0], r, i) = std::fabs(x) + dt * mv[r];
-          for (int d = 0; d < 3; d++) { A_(g, ar[2], 3 * r + d, i) = nC[r][d]; M_(g, ar[2], 3 * r + d, i) = mC[r][d]; }
+          A_(g, ar[o0 + 1], r, i) = nv[r]; M_(g, ar[o0 + 1], r, i) = mv[r];
+          A_(g, ar[o0 + 0], r, i) = x + dt * nv[r];
+          M_(g, ar[o0 + 0], r, i) = std::fabs(x) + dt * mv[r];
+          for (int d = 0; d < 3; d++) {
+            A_(g, ar[o0 + 2], 3 * r + d, i) = nC[r][d]; M_(g, ar[o0 + 2], 3 * r + d, i) = mC[r][d];
+          }
         }
-        double J = A_(g, ar[3], 0, i);
-        A_(g, ar[3], 0, i) = J * (1.0 + dt * tr);
-        M_(g, ar[3], 0, i) = std::fabs(J) * (1.0 + dt * mtr);
-        touched_arr.push_back({0, i});
+        A_(g, ar[o0 + 3], 0, i) = J * (1.0 + dt * tr);
+        M_(g, ar[o0 + 3], 0, i) = std::fabs(J) * (1.0 + dt * mtr);
       }
-      for (int r = 0; r < 4; r++) {
-        Array& a = g->arrays[ar[r]];
-        for (double& v : a.val) v = (double)(float)v;
+      round_arrays({ar[o0], ar[o0 + 1], ar[o0 + 2], ar[o0 + 3]});
+    } break;
+    case OP_LOSS_MEAN: {
+      // f0 (0-D) += p1 * sum_i a0[p0][i]   (loss = mean x of the particles, C4)
+      if (nf < 1 || na < 1) return fail(g, E_ARG, "LOSS_MEAN needs a field and an array");
+      const int comp = (int)P(0);
+      for (int64_t i = 0; i < n && !rc; i++)
+        rc = atomic_add(g, f[0], Coord{0, 0, 0}, P(1) * A_(g, ar[0], comp, i), false);
+    } break;
+    case OP_ADJ_INIT: {
+      // adjoint of the last state: a0[p0] = p1 (d loss / d x_T), everything else 0
+      if (na < 4) return fail(g, E_ARG, "ADJ_INIT needs 4 arrays");
+      for (int k = 0; k < 4; k++) {
+        Array& a = g->arrays[ar[k]];
+        for (int c = 0; c < a.ncomp; c++)
+          for (int64_t i = 0; i < n; i++) {
+            A_(g, ar[k], c, i) = (k == 0 && c == (int)P(0)) ? P(1) : 0.0;
+            M_(g, ar[k], c, i) = std::fabs(A_(g, ar[k], c, i));
+          }
       }
+    } break;
+    case OP_G2P_ADJ: {
+      // Adjoint of GRID_OP (folded) and G2P for step s.  p0 dt, p1 inv_dx,
+      // p2 gravity, p3 bound, p4 n_grid.  Fields: f0..f2 grid momentum p, f3
+      // mass m (forward, read), f4..f6 adjoint of p, f7 adjoint of m (scattered,
+      // activating).  Arrays: a0 x_s, a1 J_s, a2..a5 adjoints (x, v, C, J) of
+      // state s+1, a6 adjoint of x_s (written), a7 adjoint of J_s (written).
+      if (nf < 8 || na < 8) return fail(g, E_ARG, "G2P_ADJ needs 8 fields and 8 arrays");
+      const double dt = P(0), grav = P(2), bound = P(3), ng = P(4);
+      const int D = 3;
+      for (int64_t i = 0; i < n && !rc; i++) {
+        Kernel k = kernel_of(ar[0], i);
+        const double J = A_(g, ar[1], 0, i);
+        double xb1[3], vb1[3], Cb1[3][3];
+        for (int r = 0; r < 3; r++) {
+          xb1[r] = A_(g, ar[2], r, i);
+          vb1[r] = A_(g, ar[3], r, i);
+          for (int d = 0; d < 3; d++) Cb1[r][d] = A_(g, ar[4], 3 * r + d, i);
+        }
+        const double Jb1 = A_(g, ar[5], 0, i);
+        // forward grid velocities of the 27 nodes and the new C (for tr C')
+        double u[27][3], mask[27][3], pn[27][3], mn[27];
+        double nC[3][3] = {{0}};
+        for (int a = 0, q = 0; a < 3; a++)
+          for (int b = 0; b < 3; b++)
+            for (int c = 0; c < 3; c++, q++) {
+              double W, gW[3], dpos[3];
+              node_w(k, a, b, c, W, gW, dpos);
+              Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
+              int nd[3] = {(int)node[0], (int)node[1], (int)node[2]};
+              for (int r = 0; r < 3; r++) pn[q][r] = read(g, f[r], node);
+              mn[q] = read(g, f[3], node);
+              grid_update(pn[q], mn[q], nd, dt, grav, bound, ng, D, u[q], mask[q]);
+              for (int r = 0; r < 3; r++)
+                for (int d = 0; d < 3; d++) nC[r][d] += s4 * W * u[q][r] * dpos[d];
+            }
+        double vt[3], Ct[3][3];
+        for (int r = 0; r < 3; r++) {
+          vt[r] = vb1[r] + dt * xb1[r];
+          for (int d = 0; d < 3; d++) Ct[r][d] = Cb1[r][d] + (r == d ? Jb1 * J * dt : 0.0);
+        }
+        const double trC = nC[0][0] + nC[1][1] + nC[2][2];
+        double Jb = Jb1 * (1.0 + dt * trC), mJ = std::fabs(Jb);
+        double xb[3] = {xb1[0], xb1[1], xb1[2]}, mx[3] = {std::fabs(xb1[0]), std::fabs(xb1[1]), std::fabs(xb1[2])};
+        for (int a = 0, q = 0; a < 3 && !rc; a++)
+          for (int b = 0; b < 3 && !rc; b++)
+            for (int c = 0; c < 3 && !rc; c++, q++) {
+              double W, gW[3], dpos[3];
+              node_w(k, a, b, c, W, gW, dpos);
+              Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
+              double gbar[3], Wbar = 0.0, dposbar[3] = {0, 0, 0};
+              for (int r = 0; r < 3; r++) {
+                double ct = 0.0;
+                for (int d = 0; d < 3; d++) ct += Ct[r][d] * dpos[d];
+                gbar[r] = W * vt[r] + s4 * W * ct;
+                Wbar += u[q][r] * vt[r] + s4 * u[q][r] * ct;
+                for (int d = 0; d < 3; d++) dposbar[d] += s4 * W * Ct[r][d] * u[q][r];
+              }
+              for (int d = 0; d < 3; d++) {
+                xb[d] += Wbar * gW[d] - dposbar[d];
+                mx[d] += std::fabs(Wbar * gW[d]) + std::fabs(dposbar[d]);
+              }
+              // GRID_OP adjoint: u = mask * (p / m - dt g e_y)
+              double ub[3], pb[3], mb = 0.0;
+              for (int r = 0; r < 3; r++) ub[r] = gbar[r] * mask[q][r];
+              for (int r = 0; r < 3; r++) {
+                pb[r] = mn[q] > 0 ? ub[r] / mn[q] : ub[r];
+                if (mn[q] > 0) mb -= ub[r] * pn[q][r] / (mn[q] * mn[q]);
+              }
+              for (int r = 0; r < 3 && !rc; r++) rc = atomic_add(g, f[4 + r], node, pb[r], act_bit(activating, 4 + r));
+              if (!rc) rc = atomic_add(g, f[7], node, mb, act_bit(activating, 7));
+            }
+        for (int d = 0; d < 3; d++) { A_(g, ar[6], d, i) = xb[d]; M_(g, ar[6], d, i) = mx[d]; }
+        A_(g, ar[7], 0, i) = Jb;
+        M_(g, ar[7], 0, i) = mJ;
+      }
+      round_arrays({ar[6], ar[7]});
+    } break;
+    case OP_P2G_ADJ: {
+      // Adjoint of P2G for step s.  p0 dt, p1 inv_dx, p2 p_mass, p3 p_vol, p4 E.
+      // Fields f0..f2 adjoint of grid momentum, f3 adjoint of mass (gathered).
+      // Arrays a0..a3 state s (x, v, C, J); a4 adjoint x_s (+=), a5 adjoint v_s,
+      // a6 adjoint C_s (written), a7 adjoint J_s (+=).
+      if (nf < 4 || na < 8) return fail(g, E_ARG, "P2G_ADJ needs 4 fields and 8 arrays");
+      const double dt = P(0), pm = P(2), pv = P(3), E = P(4);
+      const double kJ = -dt * 4.0 * E * pv * idx * idx;
+      for (int64_t i = 0; i < n; i++) {
+        Kernel k = kernel_of(ar[0], i);
+        const double J = A_(g, ar[3], 0, i);
+        double v[3], A[3][3];
+        for (int r = 0; r < 3; r++) {
+          v[r] = A_(g, ar[1], r, i);
+          for (int c = 0; c < 3; c++) A[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? kJ * (J - 1.0) : 0.0);
+        }
+        double vb[3] = {0, 0, 0}, Ab[3][3] = {{0}}, xb[3] = {0, 0, 0}, mx[3] = {0, 0, 0}, mv[3] = {0, 0, 0};
+        for (int a = 0; a < 3; a++)
+          for (int b = 0; b < 3; b++)
+            for (int c = 0; c < 3; c++) {
+              double W, gW[3], dpos[3];
+              node_w(k, a, b, c, W, gW, dpos);
+              Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
+              double pb[3];
+              for (int r = 0; r < 3; r++) pb[r] = read(g, f[r], node);
+              const double mb = read(g, f[3], node);
+              double Wbar = mb * pm, dposbar[3] = {0, 0, 0};
+              for (int r = 0; r < 3; r++) {
+                double mom = pm * v[r];
+                for (int d = 0; d < 3; d++) mom += A[r][d] * dpos[d];
+                Wbar += pb[r] * mom;
+                vb[r] += W * pm * pb[r];
+                mv[r] += std::fabs(W * pm * pb[r]);
+                for (int d = 0; d < 3; d++) {
+                  Ab[r][d] += W * pb[r] * dpos[d];
+                  dposbar[d] += W * pb[r] * A[r][d];
+                }
+              }
+              for (int d = 0; d < 3; d++) {
+                xb[d] += Wbar * gW[d] - dposbar[d];
+                mx[d] += std::fabs(Wbar * gW[d]) + std::fabs(dposbar[d]);
+              }
+            }
+        for (int d = 0; d < 3; d++) {
+          A_(g, ar[4], d, i) += xb[d];
+          M_(g, ar[4], d, i) += mx[d];
+          A_(g, ar[5], d, i) = vb[d];
+          M_(g, ar[5], d, i) = mv[d];
+          for (int c = 0; c < 3; c++) {
+            A_(g, ar[6], 3 * d + c, i) = pm * Ab[d][c];
+            M_(g, ar[6], 3 * d + c, i) = std::fabs(pm * Ab[d][c]) + 1e-30;
+          }
+        }
+        const double trA = Ab[0][0] + Ab[1][1] + Ab[2][2];
+        A_(g, ar[7], 0, i) += kJ * trA;
+        M_(g, ar[7], 0, i) += std::fabs(kJ * trA);
+      }
+      round_arrays({ar[4], ar[5], ar[6], ar[7]});
     } break;
     default:
       return fail(g, E_ARG, "unknown range-for op");
@@ -721,6 +934,9 @@ void orc_destroy(void* h) { delete (Grid*)h; }
 const char* orc_error(void* h) { return ((Grid*)h)->err.c_str(); }
 
 int32_t orc_num_fields(void* h) { return (int32_t)((Grid*)h)->fields.size(); }
+
+// f64 storage (no f32 rounding): for the finite-difference pins of the adjoints.
+void orc_set_exact(void* h, int32_t on) { ((Grid*)h)->exact = on != 0; }
 
 int32_t orc_activate(void* h, int32_t field, const int32_t* coords, int64_t n) {
   Grid* g = (Grid*)h;
