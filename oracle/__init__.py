@@ -29,7 +29,8 @@ ROOT, DENSE, BITMASKED, POINTER, PLACE = 0, 1, 2, 3, 4
 # The oracle's own op ids (must match the enum in sg_oracle.cpp).
 OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6,
        "REDUCE_SUM": 7, "DOWNSAMPLE": 8, "JITTER": 9, "CLEAR_SCALAR": 10,
-       "P2G": 20, "GRID_OP": 21, "G2P": 22}
+       "P2G": 20, "GRID_OP": 21, "G2P": 22,
+       "LOSS_MEAN": 27, "ADJ_INIT": 28, "G2P_ADJ": 29, "P2G_ADJ": 30}
 
 ERRORS = {-1: "ARG", -2: "LAYOUT", -3: "RANGE", -6: "DEMOTION_TRAP", -7: "OVERFLOW"}
 
@@ -75,6 +76,7 @@ def lib():
         L.orc_register_array.argtypes = [vp, P(ctypes.c_float), i64, i32]
         L.orc_read_array.argtypes = [vp, i32, P(ctypes.c_double), P(ctypes.c_double), i64]
         L.orc_load_array.argtypes = [vp, i32, P(ctypes.c_double), i64]
+        L.orc_set_exact.argtypes = [vp, i32]
         L.orc_range_for.argtypes = [vp, i32, i64, P(i32), i32, P(i32), i32, P(ctypes.c_float), i32, u32]
         for name in ("orc_activate", "orc_listgen", "orc_clear_list", "orc_struct_for", "orc_serial",
                      "orc_deactivate", "orc_read_field", "orc_load_field", "orc_counters", "orc_register_array",
@@ -179,6 +181,10 @@ class Oracle:
         p = np.ascontiguousarray(params if len(params) else [0.0], dtype=np.float32)
         self._check(lib().orc_range_for(self.h, OPS[op], n, _ptr(f, ctypes.c_int32), len(f), _ptr(a, ctypes.c_int32),
                                         len(a), _ptr(p, ctypes.c_float), len(params), activating))
+
+    def set_exact(self, on=True):
+        """f64 storage (no f32 rounding of fields/arrays): finite-difference pins."""
+        lib().orc_set_exact(self.h, 1 if on else 0)
 
     # --- particle arrays (SoA: shape (ncomp, n)) ---
     def register_array(self, arr):

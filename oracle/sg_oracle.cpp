@@ -59,7 +59,7 @@ enum {
   OP_JACOBI = 6, OP_REDUCE_SUM = 7, OP_DOWNSAMPLE = 8, OP_JITTER = 9,
   OP_CLEAR_SCALAR = 10,
   OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22,
-  OP_GRID_OP_SPLIT = 27, OP_LOSS_MEAN = 28, OP_ADJ_INIT = 29, OP_G2P_ADJ = 30, OP_P2G_ADJ = 31
+  OP_LOSS_MEAN = 27, OP_ADJ_INIT = 28, OP_G2P_ADJ = 29, OP_P2G_ADJ = 30
 };
 
 typedef std::array<int64_t, 3> Coord;
@@ -532,26 +532,6 @@ int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const 
           if (cond) { v[a] = 0; mv[a] = 0; }
         }
         for (int a = 0; a < 3 && !rc; a++) rc = write(g, f[a], c, v[a], false, mv[a]);
-      });
-      break;
-    case OP_GRID_OP_SPLIT:
-      // Grid update with separate output (C4 keeps the momentum for the
-      // adjoint): f0..f2 momentum, f3 mass (read), f4..f6 velocity (written).
-      // p0 dt, p1 gravity, p2 bound, p3 n_grid.
-      if (!need(7)) return fail(g, E_ARG, "GRID_OP_SPLIT needs 7 fields");
-      for_struct(g, t, [&](const Coord& c) {
-        if (rc) return;
-        double pp[3], u[3], mask[3];
-        for (int r = 0; r < 3; r++) pp[r] = read(g, f[r], c);
-        const double m = read(g, f[3], c), mm = read_mag(g, f[3], c);
-        int nd[3] = {(int)c[0], (int)c[1], (int)c[2]};
-        grid_update(pp, m, nd, P(0), P(1), P(2), P(3), D, u, mask);
-        for (int r = 0; r < 3 && !rc; r++) {
-          double mp = read_mag(g, f[r], c);
-          double mu = m > 0 ? (mp + std::fabs(pp[r]) * (mm / m)) / m : mp;
-          if (r == 1) mu += std::fabs(P(0) * P(1));
-          rc = write(g, f[4 + r], c, u[r], false, mask[r] * mu);
-        }
       });
       break;
     default:

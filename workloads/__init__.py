@@ -274,6 +274,114 @@ def c3_program(n_grid=128, n_particles=1_000_000, steps=1, flush_every=1, seed=0
 
 
 # ----------------------------------------------------------------------------
+# C4: differentiable MPM (diffmpm-like; "global
+# fields as checkpoints", PAPER.md:375-377 gradient clears).  Forward T
+# substeps keep every particle state (the checkpoints); the backward pass
+# recomputes each substep's grid (P2G) and runs the hand-written adjoints
+# G2P_ADJ (grid-op adjoint folded in) and P2G_ADJ, scattering grid adjoints
+# into a second tree of the same shape (activating).
+# ----------------------------------------------------------------------------
+def c4_layout(n_grid=64):
+    L = Layout()
+    lv = L.chain([("pointer", (n_grid // 16,) * 3), ("bitmasked", (4,) * 3), ("dense", (4,) * 3)],
+                 [("px", "f32"), ("py", "f32"), ("pz", "f32"), ("m", "f32")])
+    lg = L.chain([("pointer", (n_grid // 16,) * 3), ("bitmasked", (4,) * 3), ("dense", (4,) * 3)],
+                 [("gpx", "f32"), ("gpy", "f32"), ("gpz", "f32"), ("gm", "f32")])
+    L.scalar("loss")
+    return L, lv, lg
+
+
+def c4_particles(n, n_grid=64, side=23, center=(0.5, 0.4, 0.5), seed=0, v_scale=0.5, C_scale=1.0, J_jitter=0.02):
+    """A cube of `side` cells (about 8 particles per cell at n = 100K) with a
+    random initial velocity, affine C and J, so every adjoint term is nonzero."""
+    rng = np.random.default_rng(seed)
+    half = side / (2.0 * n_grid)
+    c = np.asarray(center, dtype=np.float64)[:, None]
+    x = (c - half + rng.random((3, n)) * 2 * half).astype(np.float32)
+    v = (rng.uniform(-1, 1, (3, n)) * v_scale).astype(np.float32)
+    C = (rng.uniform(-1, 1, (9, n)) * C_scale).astype(np.float32)
+    J = (1.0 + rng.uniform(-1, 1, (1, n)) * J_jitter).astype(np.float32)
+    return {"x": x, "v": v, "C": C, "J": J}
+
+
+def c4_arrays(n, T, n_grid=64, **kw):
+    """Array table: state s = ids 4s..4s+3 (x, v, C, J) for s = 0..T, then two
+    adjoint buffers A = 4(T+1)+0..3 and B = 4(T+1)+4..7 (same shapes)."""
+    p0 = c4_particles(n, n_grid, **kw)
+    arrays = {}
+    for s in range(T + 1):
+        for k in ("x", "v", "C", "J"):
+            arrays[f"{k}{s}"] = p0[k] if s == 0 else np.zeros_like(p0[k])
+    for b in ("A", "B"):
+        for k in ("x", "v", "C", "J"):
+            arrays[f"adj{b}_{k}"] = np.zeros_like(p0[k])
+    return arrays
+
+
+def c4_forward_calls(L, lv, lg, n, T, prm, comp=0, grad_clears=True):
+    f = L.fields
+    grid_f = [f["px"], f["py"], f["pz"], f["m"]]
+    grad_f = [f["gpx"], f["gpy"], f["gpz"], f["gm"]]
+    calls = []
+    for s in range(T):
+        st, nx = [4 * s + k for k in range(4)], [4 * (s + 1) + k for k in range(4)]
+        calls.append(deactivate(lv[0]))
+        if grad_clears:   # diffmpm's clear_grid also zeroes the grads: dead stores (PAPER.md:377)
+            calls += [clear_values(g) for g in grad_f]
+        calls.append(range_for("P2G", n, grid_f, st,
+                               [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]], [True] * 4))
+        calls.append(struct_for("GRID_OP", lv[-1], grid_f, [prm["dt"], prm["gravity"], prm["bound"], prm["n_grid"]]))
+        calls.append(range_for("G2P", n, grid_f, st + nx, [prm["dt"], prm["inv_dx"]]))
+    calls.append(serial("CLEAR_SCALAR", [f["loss"]]))
+    calls.append(range_for("LOSS_MEAN", n, [f["loss"]], [4 * T], [comp, 1.0 / n]))
+    return calls
+
+
+def c4_backward_calls(L, lv, lg, n, T, prm, comp=0):
+    f = L.fields
+    grid_f = [f["px"], f["py"], f["pz"], f["m"]]
+    grad_f = [f["gpx"], f["gpy"], f["gpz"], f["gm"]]
+    A = [4 * (T + 1) + k for k in range(4)]
+    B = [4 * (T + 1) + 4 + k for k in range(4)]
+    calls = [range_for("ADJ_INIT", n, [], A, [comp, 1.0 / n])]
+    for j, s in enumerate(reversed(range(T))):
+        adj1, adj0 = (A, B) if j % 2 == 0 else (B, A)
+        st = [4 * s + k for k in range(4)]
+        calls.append(deactivate(lv[0]))
+        calls.append(range_for("P2G", n, grid_f, st,
+                               [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]], [True] * 4))
+        calls.append(deactivate(lg[0]))
+        calls.append(range_for("G2P_ADJ", n, grid_f + grad_f, [st[0], st[3]] + adj1 + [adj0[0], adj0[3]],
+                               [prm["dt"], prm["inv_dx"], prm["gravity"], prm["bound"], prm["n_grid"]],
+                               [False] * 4 + [True] * 4))
+        calls.append(range_for("P2G_ADJ", n, grad_f, st + adj0,
+                               [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]]))
+    return calls
+
+
+def c4_result_arrays(T):
+    """Array ids holding d loss / d (x0, v0, C0, J0) after the backward pass."""
+    A = [4 * (T + 1) + k for k in range(4)]
+    B = [4 * (T + 1) + 4 + k for k in range(4)]
+    return B if T % 2 == 1 else A
+
+
+def c4_program(n_grid=64, n_particles=100_000, T=64, seed=0, passes="all", comp=0, grad_clears=True,
+               observed=None, dt=2e-4, **kw):
+    L, lv, lg = c4_layout(n_grid)
+    prm = mpm_params(n_grid, dt=dt)
+    arrays = c4_arrays(n_particles, T, n_grid, seed=seed, **kw)
+    calls = c4_forward_calls(L, lv, lg, n_particles, T, prm, comp, grad_clears)
+    calls += c4_backward_calls(L, lv, lg, n_particles, T, prm, comp)
+    calls.append(flush(passes, observed))
+    prog = program(L, calls, arrays=arrays, name="C4")
+    prog["params"] = prm
+    prog["T"] = T
+    prog["result_arrays"] = c4_result_arrays(T)
+    return prog
+
+
+# ----------------------------------------------------------------------------
 # C5: large sparse MPM, 512^3 bound, x-slab sharded.
 # pointer(P^3) [n/P cells each] -> bitmasked((n/P/4)^3) -> dense(4^3).
 # ----------------------------------------------------------------------------
