@@ -334,6 +334,48 @@ def measure_c3(steps=20, warmup=3, n=1_000_000):
             "avg_us_per_launch_kind": per, "particles": n}
 
 
+def _enqueue_calls(g, sg, calls):
+    for c in calls:
+        k = c["call"]
+        if k == "clear":
+            g.clear(c["target"], sg.CLEAR_VALUES if c["mode"] == "values" else sg.DEACTIVATE)
+        elif k == "range_for":
+            g.range_for(c["op"], c["n"], c["fields"], c["arrays"], c["params"], c["activating"])
+        elif k == "struct_for":
+            g.struct_for(c["op"], c["snode"], c["fields"], c["params"], c["activating"])
+        elif k == "serial":
+            g.serial(c["op"], c["fields"], c["params"])
+
+
+def measure_c4(steps=5, warmup=3, n=100_000, T=64):
+    """C4: differentiable MPM, 64^3, 100K particles, T = 64 substeps: one
+    forward (checkpointing every substep's particle state) plus the backward
+    pass (recomputed P2G, G2P_ADJ, P2G_ADJ per substep) = one iteration."""
+    import torch
+    from paper_2012_08141_b200 import sg
+    prog = W.c4_program(n_grid=64, n_particles=n, T=T)
+    g = sg.Grid(prog["desc"])
+    g.tensors = {}
+    for name, a in prog["arrays"].items():
+        t = torch.as_tensor(a).cuda().contiguous()
+        g.tensors[name] = t
+        g.register_array(t, a.shape[0])
+    calls = [c for c in prog["calls"] if c["call"] != "flush"]
+    sg.set_profiling(g, True)
+    ms, st = _timed_flushes(g, lambda: _enqueue_calls(g, sg, calls), steps, warmup)
+    prof = sg.profile_read(g)
+    sg.set_profiling(g, False)
+    per = {}
+    names = {0: "activate", 1: "listgen", 3: "struct_for", 4: "range_for", 5: "serial", 6: "deactivate"}
+    for k, (t, c) in prof.items():
+        if k in names:
+            per[names[k]] = {"us": t / max(c, 1) * 1e3, "launches": c / max(steps, 1)}
+    loss = float(g.field(prog["layout"].fields["loss"]).reshape(-1)[0])
+    return {"iterations_per_s": 1000.0 / ms, "ms_per_iteration": ms, "launches_per_iteration": st["launches"],
+            "tasks_lowered": st["tasks_lowered"], "dead_removed": st["dead_removed"],
+            "avg_us_per_launch_kind": per, "particles": n, "substeps": T, "loss": loss}
+
+
 def run_c5(args, rank, world, local):
     """C5: 512^3 sparse MPM, 16M particles in an x-spanning bar, sharded in x
     slabs over the ranks (strong scaling); NCCL P2P halo / migration."""
@@ -461,7 +503,7 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "scripts"))
             import xl_bench
             extra = {}
-            for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3),
+            for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3), ("c4", measure_c4),
                              ("jac_xl", xl_bench.jac_xl), ("lg_xl", xl_bench.lg_xl)):
                 try:
                     extra[name] = fn()

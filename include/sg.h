@@ -132,13 +132,31 @@ enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
  *                           stable in-place compaction of the particles whose cell x stays
  *                           in [p2, p3); leavers appended to a5 (x < p2) / a6 (x >= p3)
  *   MIGRATE_APPEND range-for particles of buffers a5, a6 appended to a0..a4
+ * Differentiable MPM (C4; "kernels and their gradients", the
+ * global fields / particle states serve as checkpoints):
+ *   G2P with arrays a4..a7 set: reads state a0..a3, writes the new state to
+ *                           a4..a7 (x, v, C, J) instead of in place
+ *   LOSS_MEAN    range-for  f0[] (0-D) += p1 * sum_i a0[comp p0][i]   (deterministic
+ *                           f64 tree reduction; loss = mean x with p1 = 1/n)
+ *   ADJ_INIT     range-for  a0[comp p0][i] = p1; every other entry of a0..a3 = 0
+ *   G2P_ADJ      range-for  adjoint of GRID_OP (folded) + G2P of one substep.
+ *                           f0..f3 grid momentum / mass from P2G (read), f4..f7 their
+ *                           adjoints in a second tree (scattered with atomics,
+ *                           activating); a0 x_s, a1 J_s, a2..a5 adjoint of state s+1
+ *                           (x, v, C, J), writes a6 = adjoint x_s, a7 = adjoint J_s;
+ *                           p0 dt, p1 inv_dx, p2 gravity, p3 bound, p4 n_grid
+ *   P2G_ADJ      range-for  adjoint of P2G: gathers f0..f3 (grid adjoints); a0..a3
+ *                           state s; a4 adjoint x_s (+=), a5 adjoint v_s (=), a6
+ *                           adjoint C_s (=), a7 adjoint J_s (+=); p0 dt, p1 inv_dx,
+ *                           p2 p_mass, p3 p_vol, p4 E
  * Inactive or out-of-bound reads give 0. */
 enum {
   SG_OP_FILL = 1, SG_OP_ADD_CONST = 2, SG_OP_INC = 3, SG_OP_AXPY = 4, SG_OP_STENCIL = 5,
   SG_OP_JACOBI = 6, SG_OP_REDUCE_SUM = 7, SG_OP_DOWNSAMPLE = 8, SG_OP_JITTER = 9,
   SG_OP_CLEAR_SCALAR = 10, SG_OP_ARRAY_COUNT = 11,
   SG_OP_P2G = 20, SG_OP_GRID_OP = 21, SG_OP_G2P = 22,
-  SG_OP_HALO_PACK = 23, SG_OP_HALO_UNPACK = 24, SG_OP_G2P_MIGRATE = 25, SG_OP_MIGRATE_APPEND = 26
+  SG_OP_HALO_PACK = 23, SG_OP_HALO_UNPACK = 24, SG_OP_G2P_MIGRATE = 25, SG_OP_MIGRATE_APPEND = 26,
+  SG_OP_LOSS_MEAN = 27, SG_OP_ADJ_INIT = 28, SG_OP_G2P_ADJ = 29, SG_OP_P2G_ADJ = 30
 };
 
 typedef struct {

@@ -285,6 +285,16 @@ int atomic_add(Grid* g, int f, const Coord& c, double v, bool activating) {
   return OK;
 }
 
+// Scatter-add with an explicit shadow magnitude for the contribution.
+int atomic_add_m(Grid* g, int f, const Coord& c, double v, double vm, bool activating) {
+  double old = read(g, f, c), om = read_mag(g, f, c);
+  int rc = prepare_write(g, f, c, activating);
+  if (rc) return rc;
+  g->fields[f].val[c] = old + v;
+  g->fields[f].mag[c] = om + vm;
+  return OK;
+}
+
 // End of task: values are stored as f32 / i32 (reading R14).
 int end_task(Grid* g) {
   for (auto& tc : g->touched) {
@@ -717,6 +727,9 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
       // mass m (forward, read), f4..f6 adjoint of p, f7 adjoint of m (scattered,
       // activating).  Arrays: a0 x_s, a1 J_s, a2..a5 adjoints (x, v, C, J) of
       // state s+1, a6 adjoint of x_s (written), a7 adjoint of J_s (written).
+      // The *m variables are the shadow magnitudes (reading R32): the sum of
+      // |terms| each result is accumulated from, propagated through products
+      // and quotients, so parity tolerances scale with them.
       if (nf < 8 || na < 8) return fail(g, E_ARG, "G2P_ADJ needs 8 fields and 8 arrays");
       const double dt = P(0), grav = P(2), bound = P(3), ng = P(4);
       const int D = 3;
@@ -731,8 +744,8 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
         }
         const double Jb1 = A_(g, ar[5], 0, i);
         // forward grid velocities of the 27 nodes and the new C (for tr C')
-        double u[27][3], mask[27][3], pn[27][3], mn[27];
-        double nC[3][3] = {{0}};
+        double u[27][3], um[27][3], mask[27][3], pn[27][3], pm_[27][3], mn[27], mm[27];
+        double trC = 0.0, trCm = 0.0;
         for (int a = 0, q = 0; a < 3; a++)
           for (int b = 0; b < 3; b++)
             for (int c = 0; c < 3; c++, q++) {
@@ -740,19 +753,28 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
               node_w(k, a, b, c, W, gW, dpos);
               Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
               int nd[3] = {(int)node[0], (int)node[1], (int)node[2]};
-              for (int r = 0; r < 3; r++) pn[q][r] = read(g, f[r], node);
+              for (int r = 0; r < 3; r++) { pn[q][r] = read(g, f[r], node); pm_[q][r] = read_mag(g, f[r], node); }
               mn[q] = read(g, f[3], node);
+              mm[q] = read_mag(g, f[3], node);
               grid_update(pn[q], mn[q], nd, dt, grav, bound, ng, D, u[q], mask[q]);
-              for (int r = 0; r < 3; r++)
-                for (int d = 0; d < 3; d++) nC[r][d] += s4 * W * u[q][r] * dpos[d];
+              for (int r = 0; r < 3; r++) {
+                um[q][r] = mn[q] > 0 ? (pm_[q][r] + std::fabs(pn[q][r]) * mm[q] / mn[q]) / mn[q] : pm_[q][r];
+                if (r == 1) um[q][r] += std::fabs(dt * grav);
+                um[q][r] *= mask[q][r];
+                trC += s4 * W * u[q][r] * dpos[r];
+                trCm += s4 * std::fabs(W) * um[q][r] * std::fabs(dpos[r]);
+              }
             }
-        double vt[3], Ct[3][3];
+        double vt[3], vtm[3], Ct[3][3], Ctm[3][3];
         for (int r = 0; r < 3; r++) {
           vt[r] = vb1[r] + dt * xb1[r];
-          for (int d = 0; d < 3; d++) Ct[r][d] = Cb1[r][d] + (r == d ? Jb1 * J * dt : 0.0);
+          vtm[r] = std::fabs(vb1[r]) + dt * std::fabs(xb1[r]);
+          for (int d = 0; d < 3; d++) {
+            Ct[r][d] = Cb1[r][d] + (r == d ? Jb1 * J * dt : 0.0);
+            Ctm[r][d] = std::fabs(Cb1[r][d]) + (r == d ? std::fabs(Jb1 * J * dt) : 0.0);
+          }
         }
-        const double trC = nC[0][0] + nC[1][1] + nC[2][2];
-        double Jb = Jb1 * (1.0 + dt * trC), mJ = std::fabs(Jb);
+        double Jb = Jb1 * (1.0 + dt * trC), mJ = std::fabs(Jb1) * (1.0 + dt * trCm);
         double xb[3] = {xb1[0], xb1[1], xb1[2]}, mx[3] = {std::fabs(xb1[0]), std::fabs(xb1[1]), std::fabs(xb1[2])};
         for (int a = 0, q = 0; a < 3 && !rc; a++)
           for (int b = 0; b < 3 && !rc; b++)
@@ -760,27 +782,41 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
               double W, gW[3], dpos[3];
               node_w(k, a, b, c, W, gW, dpos);
               Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
-              double gbar[3], Wbar = 0.0, dposbar[3] = {0, 0, 0};
+              double gbar[3], gbm[3], Wbar = 0.0, Wbm = 0.0, dposbar[3] = {0, 0, 0}, dpbm[3] = {0, 0, 0};
               for (int r = 0; r < 3; r++) {
-                double ct = 0.0;
-                for (int d = 0; d < 3; d++) ct += Ct[r][d] * dpos[d];
+                double ct = 0.0, ctm = 0.0;
+                for (int d = 0; d < 3; d++) { ct += Ct[r][d] * dpos[d]; ctm += Ctm[r][d] * std::fabs(dpos[d]); }
                 gbar[r] = W * vt[r] + s4 * W * ct;
+                gbm[r] = std::fabs(W) * (vtm[r] + s4 * ctm);
                 Wbar += u[q][r] * vt[r] + s4 * u[q][r] * ct;
-                for (int d = 0; d < 3; d++) dposbar[d] += s4 * W * Ct[r][d] * u[q][r];
+                Wbm += um[q][r] * (vtm[r] + s4 * ctm);
+                for (int d = 0; d < 3; d++) {
+                  dposbar[d] += s4 * W * Ct[r][d] * u[q][r];
+                  dpbm[d] += s4 * std::fabs(W) * Ctm[r][d] * um[q][r];
+                }
               }
               for (int d = 0; d < 3; d++) {
                 xb[d] += Wbar * gW[d] - dposbar[d];
-                mx[d] += std::fabs(Wbar * gW[d]) + std::fabs(dposbar[d]);
+                mx[d] += Wbm * std::fabs(gW[d]) + dpbm[d];
               }
               // GRID_OP adjoint: u = mask * (p / m - dt g e_y)
-              double ub[3], pb[3], mb = 0.0;
-              for (int r = 0; r < 3; r++) ub[r] = gbar[r] * mask[q][r];
+              double pb[3], pbm[3], mb = 0.0, mbm = 0.0;
               for (int r = 0; r < 3; r++) {
-                pb[r] = mn[q] > 0 ? ub[r] / mn[q] : ub[r];
-                if (mn[q] > 0) mb -= ub[r] * pn[q][r] / (mn[q] * mn[q]);
+                const double ub = gbar[r] * mask[q][r], ubm = gbm[r] * mask[q][r];
+                if (mn[q] > 0) {
+                  pb[r] = ub / mn[q];
+                  pbm[r] = (ubm + std::fabs(ub) * mm[q] / mn[q]) / mn[q];
+                  mb -= ub * pn[q][r] / (mn[q] * mn[q]);
+                  mbm += (ubm * std::fabs(pn[q][r]) + std::fabs(ub) * pm_[q][r] +
+                          2.0 * std::fabs(ub * pn[q][r]) * mm[q] / mn[q]) / (mn[q] * mn[q]);
+                } else {
+                  pb[r] = ub;
+                  pbm[r] = ubm;
+                }
               }
-              for (int r = 0; r < 3 && !rc; r++) rc = atomic_add(g, f[4 + r], node, pb[r], act_bit(activating, 4 + r));
-              if (!rc) rc = atomic_add(g, f[7], node, mb, act_bit(activating, 7));
+              for (int r = 0; r < 3 && !rc; r++)
+                rc = atomic_add_m(g, f[4 + r], node, pb[r], pbm[r], act_bit(activating, 4 + r));
+              if (!rc) rc = atomic_add_m(g, f[7], node, mb, mbm, act_bit(activating, 7));
             }
         for (int d = 0; d < 3; d++) { A_(g, ar[6], d, i) = xb[d]; M_(g, ar[6], d, i) = mx[d]; }
         A_(g, ar[7], 0, i) = Jb;
@@ -792,43 +828,50 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
       // Adjoint of P2G for step s.  p0 dt, p1 inv_dx, p2 p_mass, p3 p_vol, p4 E.
       // Fields f0..f2 adjoint of grid momentum, f3 adjoint of mass (gathered).
       // Arrays a0..a3 state s (x, v, C, J); a4 adjoint x_s (+=), a5 adjoint v_s,
-      // a6 adjoint C_s (written), a7 adjoint J_s (+=).
+      // a6 adjoint C_s (written), a7 adjoint J_s (+=).  Magnitudes as in G2P_ADJ.
       if (nf < 4 || na < 8) return fail(g, E_ARG, "P2G_ADJ needs 4 fields and 8 arrays");
       const double dt = P(0), pm = P(2), pv = P(3), E = P(4);
       const double kJ = -dt * 4.0 * E * pv * idx * idx;
       for (int64_t i = 0; i < n; i++) {
         Kernel k = kernel_of(ar[0], i);
         const double J = A_(g, ar[3], 0, i);
-        double v[3], A[3][3];
+        double v[3], A[3][3], Am[3][3];
         for (int r = 0; r < 3; r++) {
           v[r] = A_(g, ar[1], r, i);
-          for (int c = 0; c < 3; c++) A[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? kJ * (J - 1.0) : 0.0);
+          for (int c = 0; c < 3; c++) {
+            A[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? kJ * (J - 1.0) : 0.0);
+            Am[r][c] = std::fabs(pm * A_(g, ar[2], 3 * r + c, i)) + (r == c ? std::fabs(kJ) * (std::fabs(J) + 1.0) : 0.0);
+          }
         }
-        double vb[3] = {0, 0, 0}, Ab[3][3] = {{0}}, xb[3] = {0, 0, 0}, mx[3] = {0, 0, 0}, mv[3] = {0, 0, 0};
+        double vb[3] = {0, 0, 0}, Ab[3][3] = {{0}}, Abm[3][3] = {{0}}, xb[3] = {0, 0, 0}, mx[3] = {0, 0, 0},
+               mv[3] = {0, 0, 0};
         for (int a = 0; a < 3; a++)
           for (int b = 0; b < 3; b++)
             for (int c = 0; c < 3; c++) {
               double W, gW[3], dpos[3];
               node_w(k, a, b, c, W, gW, dpos);
               Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
-              double pb[3];
-              for (int r = 0; r < 3; r++) pb[r] = read(g, f[r], node);
-              const double mb = read(g, f[3], node);
-              double Wbar = mb * pm, dposbar[3] = {0, 0, 0};
+              double pb[3], pbm[3];
+              for (int r = 0; r < 3; r++) { pb[r] = read(g, f[r], node); pbm[r] = read_mag(g, f[r], node); }
+              const double mb = read(g, f[3], node), mbm = read_mag(g, f[3], node);
+              double Wbar = mb * pm, Wbm = mbm * pm, dposbar[3] = {0, 0, 0}, dpbm[3] = {0, 0, 0};
               for (int r = 0; r < 3; r++) {
-                double mom = pm * v[r];
-                for (int d = 0; d < 3; d++) mom += A[r][d] * dpos[d];
+                double mom = pm * v[r], momm = pm * std::fabs(v[r]);
+                for (int d = 0; d < 3; d++) { mom += A[r][d] * dpos[d]; momm += Am[r][d] * std::fabs(dpos[d]); }
                 Wbar += pb[r] * mom;
+                Wbm += pbm[r] * momm;
                 vb[r] += W * pm * pb[r];
-                mv[r] += std::fabs(W * pm * pb[r]);
+                mv[r] += std::fabs(W) * pm * pbm[r];
                 for (int d = 0; d < 3; d++) {
                   Ab[r][d] += W * pb[r] * dpos[d];
+                  Abm[r][d] += std::fabs(W) * pbm[r] * std::fabs(dpos[d]);
                   dposbar[d] += W * pb[r] * A[r][d];
+                  dpbm[d] += std::fabs(W) * pbm[r] * Am[r][d];
                 }
               }
               for (int d = 0; d < 3; d++) {
                 xb[d] += Wbar * gW[d] - dposbar[d];
-                mx[d] += std::fabs(Wbar * gW[d]) + std::fabs(dposbar[d]);
+                mx[d] += Wbm * std::fabs(gW[d]) + dpbm[d];
               }
             }
         for (int d = 0; d < 3; d++) {
@@ -838,12 +881,12 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
           M_(g, ar[5], d, i) = mv[d];
           for (int c = 0; c < 3; c++) {
             A_(g, ar[6], 3 * d + c, i) = pm * Ab[d][c];
-            M_(g, ar[6], 3 * d + c, i) = std::fabs(pm * Ab[d][c]) + 1e-30;
+            M_(g, ar[6], 3 * d + c, i) = pm * Abm[d][c];
           }
         }
         const double trA = Ab[0][0] + Ab[1][1] + Ab[2][2];
         A_(g, ar[7], 0, i) += kJ * trA;
-        M_(g, ar[7], 0, i) += std::fabs(kJ * trA);
+        M_(g, ar[7], 0, i) += std::fabs(kJ) * (Abm[0][0] + Abm[1][1] + Abm[2][2]);
       }
       round_arrays({ar[4], ar[5], ar[6], ar[7]});
     } break;

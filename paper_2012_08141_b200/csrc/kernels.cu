@@ -515,6 +515,7 @@ __global__ void k_clear_list(uint32_t* count) { *count = 0; }
 #include "mpm_ops.cuh"
 #include "struct_for.cuh"
 #include "exchange_ops.cuh"
+#include "mpm_adj.cuh"
 
 // ---------------------------------------------------------------------------
 // Serial and range-for
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(128) k_range_for(const __grid_constant__ RFArg
         case SG_OP_P2G: mpm_p2g<0>(A.C, A.C.trees[A.C.fields[op.f[0]].tree], op, i, A.task); break;
         case SG_OP_G2P: mpm_g2p<0>(A.C, A.C.trees[A.C.fields[op.f[0]].tree], op, i); break;
         case SG_OP_HALO_UNPACK: halo_unpack(A.C, op, i, A.task); break;
+        case SG_OP_ADJ_INIT: adj_init(A.C, op, i); break;
         default: break;
       }
     }
@@ -850,15 +852,41 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   return check_launch();
 }
 
+static bool lb2_tree(const DTree& t) {
+  const DLevel& d = t.lev[t.driving];
+  return d.lbelow[0] == 2 && d.lbelow[1] == 2 && d.lbelow[2] == 2 && t.lblk == 6;
+}
+
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task,
-                     void* stream, const RangeScratch* rs, const DTree* grid_tree) {
+                     void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  if (nops == 1 && (ops[0].op == SG_OP_G2P_ADJ || ops[0].op == SG_OP_P2G_ADJ)) {
+    Mpm2Args m;
+    m.T = *grid_tree; m.TG = tree2 ? *tree2 : *grid_tree; m.C = c; m.op = ops[0]; m.n = n; m.task = task;
+    const bool lb2 = lb2_tree(m.T) && lb2_tree(m.TG);
+    int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms() * 16);
+    if (ops[0].op == SG_OP_G2P_ADJ) {
+      if (lb2) k_g2p_adj<2><<<grid, 128, 0, s>>>(m);
+      else k_g2p_adj<0><<<grid, 128, 0, s>>>(m);
+    } else {
+      if (lb2) k_p2g_adj<2><<<grid, 128, 0, s>>>(m);
+      else k_p2g_adj<0><<<grid, 128, 0, s>>>(m);
+    }
+    return check_launch();
+  }
+  if (nops == 1 && ops[0].op == SG_OP_LOSS_MEAN) {
+    LossArgs m;
+    m.C = c; m.op = ops[0]; m.n = n;
+    m.target = c.scalars + (ops[0].scalar >= 0 ? ops[0].scalar : 0);
+    int grid = (int)std::min<int64_t>((n + LM_TPB - 1) / LM_TPB, (int64_t)std::min(c.max_grid, num_sms() * 4));
+    k_loss_mean<<<std::max(grid, 1), LM_TPB, 0, s>>>(m);
+    return check_launch();
+  }
   if (nops == 1 && grid_tree && (ops[0].op == SG_OP_P2G || ops[0].op == SG_OP_G2P)) {
     MpmArgs m;
     m.T = *grid_tree; m.C = c; m.op = ops[0]; m.n = n; m.dcount = dcount; m.task = task;
-    const bool lb2 = grid_tree->lev[grid_tree->driving].lbelow[0] == 2 && grid_tree->lev[grid_tree->driving].lbelow[1] == 2 &&
-                     grid_tree->lev[grid_tree->driving].lbelow[2] == 2 && grid_tree->lblk == 6;
+    const bool lb2 = lb2_tree(*grid_tree);
     int grid = (int)std::min<int64_t>((n + 127) / 128, (int64_t)num_sms() * 16);
     if (ops[0].op == SG_OP_P2G) {
       if (lb2) k_p2g<2><<<grid, 128, 0, s>>>(m);

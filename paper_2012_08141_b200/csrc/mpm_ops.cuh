@@ -186,27 +186,34 @@ __device__ __forceinline__ void mpm_gather(const DevCtx& C, const DTree& T, cons
       }
 }
 
+// G2P: in place on a0..a3, or (a4 set) reading state a0..a3 and writing the
+// new state to a4..a7 (C4 keeps every substep's state as a checkpoint).
 template <int LB>
 __device__ __forceinline__ void mpm_g2p(const DevCtx& C, const DTree& T, const DOp& op, int64_t i) {
-  const DArray X = C.arrays[op.a[0]], Vv = C.arrays[op.a[1]], Cm = C.arrays[op.a[2]], Jj = C.arrays[op.a[3]];
-  float* x = (float*)X.ptr;
-  float* v = (float*)Vv.ptr;
-  float* cm = (float*)Cm.ptr;
-  float* jj = (float*)Jj.ptr;
+  const int o = op.a[4] >= 0 ? 4 : 0;
+  const DArray X = C.arrays[op.a[0]], Jj = C.arrays[op.a[3]];
+  const DArray Xo = C.arrays[op.a[o]], Vo = C.arrays[op.a[o + 1]], Co = C.arrays[op.a[o + 2]],
+               Jo = C.arrays[op.a[o + 3]];
+  const float* x = (const float*)X.ptr;
+  float* xo = (float*)Xo.ptr;
+  float* vo = (float*)Vo.ptr;
+  float* co = (float*)Co.ptr;
+  float* jo = (float*)Jo.ptr;
   const float dt = op.p[0], inv_dx = op.p[1];
   const float dx = 1.0f / inv_dx;
   float xp[3] = {x[i], x[X.n + i], x[2 * X.n + i]};
+  const float J = ((const float*)Jj.ptr)[i];
   MpmKernel k = mpm_bspline(xp, inv_dx);
   float nv[3], nC[3][3];
   mpm_gather<LB>(C, T, op, k, dx, inv_dx, nv, nC);
 #pragma unroll
   for (int r = 0; r < 3; r++) {
-    v[r * Vv.n + i] = nv[r];
-    x[r * X.n + i] = xp[r] + dt * nv[r];
+    vo[r * Vo.n + i] = nv[r];
+    xo[r * Xo.n + i] = xp[r] + dt * nv[r];
 #pragma unroll
-    for (int d = 0; d < 3; d++) cm[(3 * r + d) * Cm.n + i] = nC[r][d];
+    for (int d = 0; d < 3; d++) co[(3 * r + d) * Co.n + i] = nC[r][d];
   }
-  jj[i] = jj[i] * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
+  jo[i] = J * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
 }
 
 // Grid update for one cell (struct-for).  cell0 points at the cell in field slot 0.

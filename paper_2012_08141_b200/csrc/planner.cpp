@@ -84,7 +84,27 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
       break;
     case SG_OP_G2P:
       for (int i = 0; i < 3; i++) F(i, R_READ, AC_DATA);
-      A(0, R_RW, AC_ID); A(1, R_WRITE, AC_ID, true); A(2, R_WRITE, AC_ID, true); A(3, R_RW, AC_ID);
+      if (t.arrays[4] >= 0) {   // out of place: state a0..a3 -> a4..a7
+        A(0, R_READ, AC_ID); A(3, R_READ, AC_ID);
+        for (int i = 4; i < 8; i++) A(i, R_WRITE, AC_ID, true);
+      } else {
+        A(0, R_RW, AC_ID); A(1, R_WRITE, AC_ID, true); A(2, R_WRITE, AC_ID, true); A(3, R_RW, AC_ID);
+      }
+      break;
+    case SG_OP_LOSS_MEAN: A(0, R_READ, AC_ID); F(0, R_RW, AC_CONST); break;
+    case SG_OP_ADJ_INIT:
+      for (int i = 0; i < 4; i++) A(i, R_WRITE, AC_ID, true);
+      break;
+    case SG_OP_G2P_ADJ:
+      for (int i = 0; i < 4; i++) F(i, R_READ, AC_DATA);
+      for (int i = 4; i < 8; i++) F(i, R_RW, AC_DATA);
+      for (int i = 0; i < 6; i++) A(i, R_READ, AC_ID);
+      A(6, R_WRITE, AC_ID, true); A(7, R_WRITE, AC_ID, true);
+      break;
+    case SG_OP_P2G_ADJ:
+      for (int i = 0; i < 4; i++) F(i, R_READ, AC_DATA);
+      for (int i = 0; i < 4; i++) A(i, R_READ, AC_ID);
+      A(4, R_RW, AC_ID); A(5, R_WRITE, AC_ID, true); A(6, R_WRITE, AC_ID, true); A(7, R_RW, AC_ID);
       break;
     case SG_OP_ARRAY_COUNT: A(0, R_WRITE, AC_CONST); break;
     case SG_OP_HALO_PACK:
@@ -115,7 +135,10 @@ static int op_min_fields(int op) {
     case SG_OP_ADD_CONST: case SG_OP_STENCIL: case SG_OP_REDUCE_SUM: return 2;
     case SG_OP_AXPY: case SG_OP_JACOBI: return 3;
     case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: case SG_OP_G2P_MIGRATE: return 4;
-    case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: return 0;
+    case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: return 0;
+    case SG_OP_LOSS_MEAN: return 1;
+    case SG_OP_G2P_ADJ: return 8;
+    case SG_OP_P2G_ADJ: return 4;
     case SG_OP_HALO_PACK: case SG_OP_HALO_UNPACK: return 1;
     default: return -1;
   }
@@ -245,6 +268,46 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
       }
       if (t.op == SG_OP_MIGRATE_APPEND) return SG_OK;
       break;   // G2P_MIGRATE: grid checks below
+    case SG_OP_LOSS_MEAN:
+      if (t.kind != SG_TASK_RANGE_FOR || t.arrays[0] < 0) { err = "LOSS_MEAN is a range-for op over arrays[0]"; return SG_ERR_ARG; }
+      if (L.field_tree[t.fields[0]] >= 0 || L.field_dtype[t.fields[0]] != SG_F32) { err = "LOSS_MEAN target must be a 0-D f32 field"; return SG_ERR_ARG; }
+      return SG_OK;
+    case SG_OP_ADJ_INIT:
+      if (t.kind != SG_TASK_RANGE_FOR) { err = "ADJ_INIT is a range-for op"; return SG_ERR_ARG; }
+      for (int i = 0; i < 4; i++) if (t.arrays[i] < 0) { err = "ADJ_INIT needs 4 arrays"; return SG_ERR_ARG; }
+      return SG_OK;
+    case SG_OP_G2P_ADJ:
+    case SG_OP_P2G_ADJ: {
+      if (t.kind != SG_TASK_RANGE_FOR) { err = "MPM adjoints are range-for ops"; return SG_ERR_ARG; }
+      for (int i = 0; i < 8; i++) if (t.arrays[i] < 0) { err = "MPM adjoints need 8 arrays"; return SG_ERR_ARG; }
+      const int ng = t.op == SG_OP_G2P_ADJ ? 2 : 1;
+      int trees[2];
+      for (int k = 0; k < ng; k++) {
+        int tree = L.field_tree[t.fields[4 * k]];
+        if (tree < 0 || L.trees[tree].nd != 3 || L.trees[tree].driving < 0) { err = "MPM grid fields must live in a 3-D sparse tree"; return SG_ERR_ARG; }
+        for (int i = 4 * k; i < 4 * k + 4; i++)
+          if (L.field_tree[t.fields[i]] != tree || L.field_dtype[t.fields[i]] != SG_F32) { err = "MPM grid fields must be f32 fields of one tree"; return SG_ERR_ARG; }
+        trees[k] = tree;
+      }
+      if (ng == 2) {
+        if (trees[0] == trees[1]) { err = "G2P_ADJ adjoint fields need their own tree"; return SG_ERR_ARG; }
+        for (int a = 0; a < 3; a++) {
+          int64_t ra = 1, rb = 1;
+          for (int s : L.trees[trees[0]].levels) ra *= L.nodes[s].extent[a];
+          for (int s : L.trees[trees[1]].levels) rb *= L.nodes[s].extent[a];
+          if (ra != rb) { err = "G2P_ADJ trees must have the same resolution"; return SG_ERR_ARG; }
+        }
+        if (L.trees[trees[0]].levels.size() != L.trees[trees[1]].levels.size()) { err = "G2P_ADJ trees must have the same shape"; return SG_ERR_ARG; }
+        for (size_t k = 0; k < L.trees[trees[0]].levels.size(); k++) {
+          const auto& A = L.nodes[L.trees[trees[0]].levels[k]];
+          const auto& B = L.nodes[L.trees[trees[1]].levels[k]];
+          if (A.kind != B.kind || A.extent[0] != B.extent[0] || A.extent[1] != B.extent[1] || A.extent[2] != B.extent[2]) {
+            err = "G2P_ADJ trees must have the same shape"; return SG_ERR_ARG;
+          }
+        }
+      }
+      return SG_OK;
+    }
     case SG_OP_HALO_PACK:
       if (!sf || t.arrays[0] < 0) { err = "HALO_PACK is a struct-for op with a buffer in arrays[0]"; return SG_ERR_ARG; }
       break;
@@ -603,7 +666,8 @@ static bool pass_fusion(const HLayout& L, std::vector<PTask>& seq, PlanStats& st
           if (A.n != B.n || (A.n < 0 && A.t.arrays[0] != B.t.arrays[0])) continue;
           // ops with their own kernels (scan / append / unpack) run alone
           auto solo = [](int op) {
-            return op == SG_OP_G2P_MIGRATE || op == SG_OP_MIGRATE_APPEND || op == SG_OP_HALO_UNPACK;
+            return op == SG_OP_G2P_MIGRATE || op == SG_OP_MIGRATE_APPEND || op == SG_OP_HALO_UNPACK ||
+                   op == SG_OP_LOSS_MEAN || op == SG_OP_G2P_ADJ || op == SG_OP_P2G_ADJ;
           };
           if (solo(A.t.op) || solo(B.t.op)) continue;
         }

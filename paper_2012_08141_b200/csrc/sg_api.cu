@@ -639,7 +639,9 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       const DTree* gt = nullptr;
       if (tk.fields[0] >= 0 && tk.fields[0] < (int)g->L.field_tree.size() && g->L.field_tree[tk.fields[0]] >= 0)
         gt = &g->dtrees[g->L.field_tree[tk.fields[0]]];
-      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt);
+      const DTree* gt2 = nullptr;   // G2P_ADJ: the adjoint tree
+      if (tk.op == SG_OP_G2P_ADJ) gt2 = &g->dtrees[g->L.field_tree[tk.fields[4]]];
+      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt, gt2);
     } break;
     case TT_SERIAL: {
       DOp ops[SG_MAXOPS];

@@ -156,7 +156,7 @@ struct RangeScratch {
   uint32_t* ctl;      // [0..3] migrate tile/done/epoch/count, [5] append ticket
 };
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task_id,
-                     void* stream, const RangeScratch* rs, const DTree* grid_tree);
+                     void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2);
 int launch_serial(const DevCtx& c, const DOp* ops, int nops, int task_id, void* stream);
 int launch_deactivate(const DevCtx& c, const DTree& t, int tree_id, int level, const DList* lists,
                       int task_id, void* stream);

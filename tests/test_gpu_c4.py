@@ -1,0 +1,130 @@
+"""GPU parity of the C4 differentiable-MPM path (-m gpu).
+
+* one backward substep, both sides fed the same seeded state and adjoint seed:
+  grid-adjoint tree masks exact, grid adjoints and particle adjoints within
+  1e-4 of the oracle's shadow magnitude M (reading R32), at a small size and at
+  the full 64^3 / 100K-particle size;
+* a whole small forward + backward window (T = 4, all passes): loss 1e-5,
+  final state and gradient within 1e-3 of M (the f32 rounding of each substep
+  feeds the next, reading R17);
+* full size (T = 64): the gradient is finite and its directional derivative
+  along the initial velocity matches f32 central differences of the GPU loss.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2012_08141_b200 import sg  # noqa: E402
+from test_gpu_parity import as_set  # noqa: E402
+
+
+def gpu_run(prog, passes=None):
+    g = sg.Grid(prog["desc"])
+    stats = sg.replay(g, prog, passes=passes, device="cuda")
+    g.sync()
+    return g, g.tensors, stats
+
+
+def close(got, want, mag, tol, what):
+    got = np.asarray(got, dtype=np.float64)
+    bound = tol * np.maximum(np.abs(want), mag)
+    bad = np.abs(got - want) > bound
+    assert not bad.any(), (f"{what}: {bad.sum()}/{bad.size} off, worst abs {np.abs(got - want)[bad].max():.3e}, "
+                           f"rel-to-M {(np.abs(got - want) / np.maximum(mag, 1e-300)).max():.3e}")
+
+
+def one_substep_program(n_grid, n, seed, dt=2e-4):
+    """Backward of one substep from the seeded initial state with a random
+    adjoint seed of state 1 (no ADJ_INIT): identical inputs on both sides."""
+    L, lv, lg = W.c4_layout(n_grid)
+    prm = W.mpm_params(n_grid, dt=dt)
+    arrays = W.c4_arrays(n, 1, n_grid, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    for k in ("x", "v", "C", "J"):
+        arrays[f"adjA_{k}"] = rng.standard_normal(arrays[f"adjA_{k}"].shape).astype(np.float32)
+    calls = W.c4_backward_calls(L, lv, lg, n, 1, prm)[1:]
+    calls.append(W.flush())
+    return W.program(L, calls, arrays=arrays, name="C4-1"), L, lg
+
+
+def check_one_substep(prog, L, lg, tol=1e-4):
+    o = oracle.run_program(prog)
+    g, arrs, st = gpu_run(prog)
+    for s in lg:
+        if L.rows[s][0] in (W.BITMASKED, W.POINTER):
+            assert as_set(g.mask(s)) == as_set(o.mask(s)), f"adjoint tree mask {s}"
+    for name in ("gpx", "gpy", "gpz", "gm"):
+        fid = L.fields[name]
+        want, mag = o.field(fid, with_mag=True)
+        close(g.field(fid), want, mag, tol, f"grid adjoint {name}")
+    names = list(prog["arrays"])
+    for i in range(12, 16):   # adjoint buffer B = d F / d state 0
+        want, mag = o.array(i, with_mag=True)
+        close(arrs[names[i]].cpu().numpy(), want, mag, tol, f"particle adjoint {names[i]}")
+    return st
+
+
+def test_c4_one_backward_substep_small():
+    prog, L, lg = one_substep_program(32, 4000, seed=11)
+    check_one_substep(prog, L, lg)
+
+
+def test_c4_one_backward_substep_full_size():
+    prog, L, lg = one_substep_program(64, 100_000, seed=12)
+    check_one_substep(prog, L, lg)
+
+
+@pytest.mark.parametrize("passes", [0, "all"])
+def test_c4_small_window(passes):
+    T = 4
+    prog = W.c4_program(n_grid=32, n_particles=4000, T=T, seed=13, passes="all")
+    o = oracle.run_program(prog)
+    g, arrs, st = gpu_run(prog, passes)
+    L = prog["layout"]
+    loss = float(g.field(L.fields["loss"]).reshape(-1)[0])
+    want = float(o.field(L.fields["loss"]).reshape(-1)[0])
+    assert loss == pytest.approx(want, rel=1e-5)
+    names = list(prog["arrays"])
+    for i in list(range(4 * T, 4 * T + 4)) + prog["result_arrays"]:
+        want, mag = o.array(i, with_mag=True)
+        close(arrs[names[i]].cpu().numpy(), want, mag, 1e-3, names[i])
+    if passes == "all":
+        assert st[0]["dead_removed"] == 4 * T
+
+
+def test_c4_full_size_gradient_properties():
+    T, n = 64, 100_000
+    prog = W.c4_program(n_grid=64, n_particles=n, T=T, seed=0)
+    g, arrs, st = gpu_run(prog)
+    L = prog["layout"]
+    names = list(prog["arrays"])
+    grads = [arrs[names[i]].double().cpu().numpy() for i in prog["result_arrays"]]
+    assert all(np.isfinite(a).all() for a in grads)
+    # momentum: the summed x-gradient w.r.t. v0_x is T dt (f32 params) up to f32 drift
+    dt32 = float(np.float32(prog["params"]["dt"]))
+    assert grads[1][0].sum() == pytest.approx(T * dt32, rel=2e-3)
+    # directional derivative along a random v0 perturbation vs f32 central differences
+    # (d_x has mean 1 so the loss change, ~T dt h, sits well above the f32 loss resolution)
+    d = np.random.default_rng(3).standard_normal((3, n)).astype(np.float32)
+    d[0] += 1.0
+    v0 = prog["arrays"]["v0"]
+    h = 0.05
+    Lf, lv, lg = W.c4_layout(64)
+
+    def loss_at(v):
+        arrays = dict(prog["arrays"])
+        arrays["v0"] = v.astype(np.float32)
+        calls = W.c4_forward_calls(Lf, lv, lg, n, T, prog["params"]) + [W.flush()]
+        gg, _, _ = gpu_run(W.program(Lf, calls, arrays=arrays))
+        return float(gg.field(Lf.fields["loss"]).reshape(-1)[0])
+
+    fd = (loss_at(v0 + h * d) - loss_at(v0 - h * d)) / (2 * h)
+    ad = float((grads[1] * d).sum())
+    assert ad == pytest.approx(fd, rel=2e-2, abs=2e-6)

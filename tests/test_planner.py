@@ -210,6 +210,47 @@ def test_chain_schedule_soundness_on_oracle(seed):
         assert np.array_equal(o.field(fid), ref.field(fid)), (seed, name)
 
 
+# ---------------------------------------------------------------------------
+# C4 (differentiable MPM): the forward gradient clears are dead stores
+# ("clear_all_gradients ... a typical source of dead stores");
+# an unobserved loss is dead too (the autodiff example).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("T", [1, 2, 4])
+def test_c4_dse_removes_forward_gradient_clears(T):
+    prog = W.c4_program(n_grid=16, n_particles=100, T=T)
+    st, plans = plan_counts(prog)
+    s = st[0]
+    # eager lowering: forward substep = deactivate (+2 listgens), 4 grad
+    # clears (+2 listgens each), P2G, GRID_OP (+2 listgens), G2P = 19; backward substep =
+    # deactivate grid (+2), P2G, deactivate grad (+2), G2P_ADJ, P2G_ADJ = 10; +3 loss/seed
+    assert s["tasks_lowered"] == 29 * T + 3
+    assert s["dead_removed"] == 4 * T                # one grad clear per field per substep
+    assert s["launches"] == 15 * T + 2
+    rf_groups = {int(r[0]) for r in plans[0] if sg.TASK_TYPES[r[1]] == "range_for"}
+    # P2G, G2P per forward substep; P2G, G2P_ADJ, P2G_ADJ per backward substep;
+    # LOSS_MEAN; ADJ_INIT is fused into an independent range-for (same range)
+    assert len(rf_groups) == 5 * T + 1
+    assert sum(sg.TASK_TYPES[r[1]] == "range_for" for r in plans[0]) == 5 * T + 2
+    st_dse, _ = plan_counts(prog, passes="dse")
+    assert st_dse[0]["dead_removed"] == 12 * T        # clears plus their listgens
+    # an unobserved loss (observed = no fields) is dead as well
+    L = prog["layout"]
+    prog2 = W.c4_program(n_grid=16, n_particles=100, T=T, observed=[])
+    st2, _ = plan_counts(prog2)
+    assert st2[0]["dead_removed"] == 4 * T + 2
+
+
+@pytest.mark.parametrize("passes", [0, 1, 4, 8, 15, 31])
+def test_c4_schedule_soundness_on_oracle(passes):
+    prog = W.c4_program(n_grid=16, n_particles=60, T=2, side=6, center=(0.5, 0.5, 0.5))
+    ref = oracle.run_program(prog)
+    o = replay_plan_on_oracle(prog, passes)
+    for i in range(len(prog["arrays"])):
+        assert np.array_equal(o.array(i), ref.array(i)), (passes, i)
+    L = prog["layout"]
+    assert np.array_equal(o.field(L.fields["loss"]), ref.field(L.fields["loss"]))
+
+
 def test_plan_is_topological_and_deterministic():
     p1 = plan_counts(W.c2_program())[1][0]
     p2 = plan_counts(W.c2_program())[1][0]
@@ -223,6 +264,8 @@ def replay_plan_on_oracle(prog, passes):
     """Eager oracle vs oracle executing the planner's schedule window by window."""
     g = sg.Grid(prog["desc"], plan_only=True)
     o = oracle.Oracle(prog["desc"])
+    for arr in prog.get("arrays", {}).values():
+        o.register_array(arr)
     window = []
     for c in prog["calls"]:
         if c["call"] != "flush":
@@ -233,6 +276,8 @@ def replay_plan_on_oracle(prog, passes):
                 g.struct_for(c["op"], c["snode"], c["fields"], c.get("params", []), c.get("activating", []))
             elif k == "serial":
                 g.serial(c["op"], c["fields"], c.get("params", []))
+            elif k == "range_for":
+                g.range_for(c["op"], c["n"], c["fields"], c["arrays"], c.get("params", []), c.get("activating", []))
             elif k == "clear":
                 g.clear(c["target"], sg.CLEAR_VALUES if c["mode"] == "values" else sg.DEACTIVATE)
             elif k == "listgen":
@@ -254,6 +299,8 @@ def replay_plan_on_oracle(prog, passes):
             elif t == "serial":
                 f = c["fields"][0] if c["call"] == "serial" else c["target"]
                 o.serial_task("CLEAR_SCALAR", [f])
+            elif t == "range_for":
+                o.range_for_task(c["op"], c["n"], c["fields"], c["arrays"], c.get("params", []), int(act))
             elif t == "struct_for":
                 if c["call"] == "clear":
                     o.struct_for_task("FILL", int(snode), [c["target"]], [0.0], 0)
