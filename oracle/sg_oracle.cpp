@@ -743,6 +743,14 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
           for (int d = 0; d < 3; d++) Cb1[r][d] = A_(g, ar[4], 3 * r + d, i);
         }
         const double Jb1 = A_(g, ar[5], 0, i);
+        // input shadow magnitudes (adjoints of s+1 and J_s come from earlier tasks)
+        const double Jm = M_(g, ar[1], 0, i), Jb1m = M_(g, ar[5], 0, i);
+        double xb1m[3], vb1m[3], Cb1m[3][3];
+        for (int r = 0; r < 3; r++) {
+          xb1m[r] = M_(g, ar[2], r, i);
+          vb1m[r] = M_(g, ar[3], r, i);
+          for (int d = 0; d < 3; d++) Cb1m[r][d] = M_(g, ar[4], 3 * r + d, i);
+        }
         // forward grid velocities of the 27 nodes and the new C (for tr C')
         double u[27][3], um[27][3], mask[27][3], pn[27][3], pm_[27][3], mn[27], mm[27];
         double trC = 0.0, trCm = 0.0;
@@ -768,14 +776,14 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
         double vt[3], vtm[3], Ct[3][3], Ctm[3][3];
         for (int r = 0; r < 3; r++) {
           vt[r] = vb1[r] + dt * xb1[r];
-          vtm[r] = std::fabs(vb1[r]) + dt * std::fabs(xb1[r]);
+          vtm[r] = vb1m[r] + dt * xb1m[r];
           for (int d = 0; d < 3; d++) {
             Ct[r][d] = Cb1[r][d] + (r == d ? Jb1 * J * dt : 0.0);
-            Ctm[r][d] = std::fabs(Cb1[r][d]) + (r == d ? std::fabs(Jb1 * J * dt) : 0.0);
+            Ctm[r][d] = Cb1m[r][d] + (r == d ? Jb1m * Jm * dt : 0.0);
           }
         }
-        double Jb = Jb1 * (1.0 + dt * trC), mJ = std::fabs(Jb1) * (1.0 + dt * trCm);
-        double xb[3] = {xb1[0], xb1[1], xb1[2]}, mx[3] = {std::fabs(xb1[0]), std::fabs(xb1[1]), std::fabs(xb1[2])};
+        double Jb = Jb1 * (1.0 + dt * trC), mJ = Jb1m * (1.0 + dt * trCm);
+        double xb[3] = {xb1[0], xb1[1], xb1[2]}, mx[3] = {xb1m[0], xb1m[1], xb1m[2]};
         for (int a = 0, q = 0; a < 3 && !rc; a++)
           for (int b = 0; b < 3 && !rc; b++)
             for (int c = 0; c < 3 && !rc; c++, q++) {
@@ -806,7 +814,7 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
                 if (mn[q] > 0) {
                   pb[r] = ub / mn[q];
                   pbm[r] = (ubm + std::fabs(ub) * mm[q] / mn[q]) / mn[q];
-                  mb -= ub * pn[q][r] / (mn[q] * mn[q]);
+                  mb -= pb[r] * (pn[q][r] / mn[q]);
                   mbm += (ubm * std::fabs(pn[q][r]) + std::fabs(ub) * pm_[q][r] +
                           2.0 * std::fabs(ub * pn[q][r]) * mm[q] / mn[q]) / (mn[q] * mn[q]);
                 } else {
@@ -835,12 +843,14 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
       for (int64_t i = 0; i < n; i++) {
         Kernel k = kernel_of(ar[0], i);
         const double J = A_(g, ar[3], 0, i);
-        double v[3], A[3][3], Am[3][3];
+        const double Jm = M_(g, ar[3], 0, i);
+        double v[3], vm[3], A[3][3], Am[3][3];
         for (int r = 0; r < 3; r++) {
           v[r] = A_(g, ar[1], r, i);
+          vm[r] = M_(g, ar[1], r, i);
           for (int c = 0; c < 3; c++) {
             A[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? kJ * (J - 1.0) : 0.0);
-            Am[r][c] = std::fabs(pm * A_(g, ar[2], 3 * r + c, i)) + (r == c ? std::fabs(kJ) * (std::fabs(J) + 1.0) : 0.0);
+            Am[r][c] = pm * M_(g, ar[2], 3 * r + c, i) + (r == c ? std::fabs(kJ) * (Jm + 1.0) : 0.0);
           }
         }
         double vb[3] = {0, 0, 0}, Ab[3][3] = {{0}}, Abm[3][3] = {{0}}, xb[3] = {0, 0, 0}, mx[3] = {0, 0, 0},
@@ -856,7 +866,7 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
               const double mb = read(g, f[3], node), mbm = read_mag(g, f[3], node);
               double Wbar = mb * pm, Wbm = mbm * pm, dposbar[3] = {0, 0, 0}, dpbm[3] = {0, 0, 0};
               for (int r = 0; r < 3; r++) {
-                double mom = pm * v[r], momm = pm * std::fabs(v[r]);
+                double mom = pm * v[r], momm = pm * vm[r];
                 for (int d = 0; d < 3; d++) { mom += A[r][d] * dpos[d]; momm += Am[r][d] * std::fabs(dpos[d]); }
                 Wbar += pb[r] * mom;
                 Wbm += pbm[r] * momm;

@@ -150,8 +150,9 @@ __device__ __forceinline__ void mpm_g2p_adj(const Mpm2Args& A, int64_t i) {
 #pragma unroll
         for (int r = 0; r < 3; r++) {
           const float ub = gbar[r] * mask[r];
-          atomicAdd(gb[r] + og, m > 0.0f ? ub / m : ub);
-          if (m > 0.0f) mb -= ub * pn[r] / (m * m);
+          const float pb = m > 0.0f ? ub / m : ub;
+          atomicAdd(gb[r] + og, pb);
+          if (m > 0.0f) mb -= pb * (pn[r] / m);   // (ub/m)(p/m): m*m underflows in f32 at the cloud's rim
         }
         atomicAdd(gb[3] + og, mb);
       }

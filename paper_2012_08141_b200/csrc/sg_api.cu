@@ -423,7 +423,18 @@ extern "C" sg_status sg_destroy(sg_grid* g) {
 
 extern "C" sg_status sg_register_array(sg_grid* g, void* ptr, int64_t n, int32_t dtype, int32_t ncomp, int32_t* id) {
   if (!g || !id || n < 0 || ncomp < 1) return fail(SG_ERR_ARG, "bad array");
-  if ((int)g->arrays.size() >= g->d_arrays_cap && !g->plan_only) return fail(SG_ERR_ARG, "too many arrays");
+  if ((int)g->arrays.size() >= g->d_arrays_cap && !g->plan_only) {
+    // grow the device table (C4 registers one state per substep); the old
+    // table stays allocated: launches already enqueued still point at it
+    const int cap = g->d_arrays_cap * 2;
+    DArray* t = (DArray*)g->dev_alloc((size_t)cap * sizeof(DArray));
+    if (!t) return fail(SG_ERR_CUDA, "array table allocation failed");
+    CUDA_TRY(cudaMemcpyAsync(t, g->d_arrays, (size_t)g->d_arrays_cap * sizeof(DArray), cudaMemcpyDeviceToDevice,
+                             g->stream));
+    g->d_arrays = t;
+    g->d_arrays_cap = cap;
+    g->ctx.arrays = t;
+  }
   DArray a{ptr, n, ncomp, dtype, nullptr};
   g->arrays.push_back(a);
   *id = (int32_t)g->arrays.size() - 1;

@@ -32,9 +32,12 @@ def gpu_run(prog, passes=None):
     return g, g.tensors, stats
 
 
-def close(got, want, mag, tol, what):
+def close(got, want, mag, tol, what, floor=0.0):
+    """|got - want| <= tol * max(|want|, M, floor * max|want|): the floor covers
+    entries whose true value is ~0 (e.g. d mean(x) / d v_y) where f32 roundoff
+    of the O(scale) terms they are combined from exceeds their own M."""
     got = np.asarray(got, dtype=np.float64)
-    bound = tol * np.maximum(np.abs(want), mag)
+    bound = tol * np.maximum(np.maximum(np.abs(want), mag), floor * np.abs(want).max())
     bad = np.abs(got - want) > bound
     assert not bad.any(), (f"{what}: {bad.sum()}/{bad.size} off, worst abs {np.abs(got - want)[bad].max():.3e}, "
                            f"rel-to-M {(np.abs(got - want) / np.maximum(mag, 1e-300)).max():.3e}")
@@ -94,7 +97,7 @@ def test_c4_small_window(passes):
     names = list(prog["arrays"])
     for i in list(range(4 * T, 4 * T + 4)) + prog["result_arrays"]:
         want, mag = o.array(i, with_mag=True)
-        close(arrs[names[i]].cpu().numpy(), want, mag, 1e-3, names[i])
+        close(arrs[names[i]].cpu().numpy(), want, mag, 1e-3, names[i], floor=1e-5)
     if passes == "all":
         assert st[0]["dead_removed"] == 4 * T
 
