@@ -232,7 +232,7 @@ def cpu_baseline(args, max_seconds=30.0):
             "host_cpus": os.cpu_count()}
 
 
-def _timed_flushes(grid, enqueue, steps, warmup, l2=None):
+def _timed_flushes(grid, enqueue, steps, warmup, l2=None, after_warmup=None):
     """Device time (ms) of `steps` flushes; each flush = one step of a config."""
     import torch
     stream = torch.cuda.current_stream()
@@ -240,6 +240,8 @@ def _timed_flushes(grid, enqueue, steps, warmup, l2=None):
         enqueue()
         st = grid.flush("all")
     torch.cuda.synchronize()
+    if after_warmup:
+        after_warmup()   # e.g. drop the launch profile of the warm-up (lazy module loading, allocations)
     ms = 0.0
     for _ in range(steps):
         if l2 is not None:
@@ -322,7 +324,7 @@ def measure_c3(steps=20, warmup=3, n=1_000_000):
                 g.struct_for(c["op"], c["snode"], c["fields"], c["params"], c["activating"])
 
     sg.set_profiling(g, True)
-    ms, st = _timed_flushes(g, enqueue, steps, warmup)
+    ms, st = _timed_flushes(g, enqueue, steps, warmup, after_warmup=lambda: sg.profile_read(g))
     prof = sg.profile_read(g)
     sg.set_profiling(g, False)
     per = {}
@@ -362,14 +364,16 @@ def measure_c4(steps=5, warmup=3, n=100_000, T=64):
         g.register_array(t, a.shape[0])
     calls = [c for c in prog["calls"] if c["call"] != "flush"]
     sg.set_profiling(g, True)
-    ms, st = _timed_flushes(g, lambda: _enqueue_calls(g, sg, calls), steps, warmup)
+    ms, st = _timed_flushes(g, lambda: _enqueue_calls(g, sg, calls), steps, warmup,
+                            after_warmup=lambda: sg.profile_read(g))
     prof = sg.profile_read(g)
     sg.set_profiling(g, False)
     per = {}
     names = {0: "activate", 1: "listgen", 3: "struct_for", 4: "range_for", 5: "serial", 6: "deactivate"}
+    names.update({300 + v: k for k, v in sg.OPS.items()})
     for k, (t, c) in prof.items():
         if k in names:
-            per[names[k]] = {"us": t / max(c, 1) * 1e3, "launches": c / max(steps, 1)}
+            per[names[k]] = {"us": round(t / max(c, 1) * 1e3, 2), "launches": c / steps}
     loss = float(g.field(prog["layout"].fields["loss"]).reshape(-1)[0])
     return {"iterations_per_s": 1000.0 / ms, "ms_per_iteration": ms, "launches_per_iteration": st["launches"],
             "tasks_lowered": st["tasks_lowered"], "dead_removed": st["dead_removed"],

@@ -248,7 +248,7 @@ sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count);
  * number of launches since the last read (kinds: 0 activate, 1 listgen,
  * 2 clear_list, 3 struct_for, 4 range_for, 5 serial, 6 deactivate; struct-for
  * launches are also accumulated under 100 + op of their first member, listgens
- * under 200 + snode). */
+ * under 200 + snode, range-for launches under 300 + op of their first member). */
 sg_status sg_set_profiling(sg_grid* g, int32_t on);
 sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int32_t n_kinds);
 

@@ -8,7 +8,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsg.so")
 BUILD = os.path.join(HERE, "build")
 SOURCES = ["kernels.cu", "sg_api.cu", "planner.cpp"]
-DEPS = SOURCES + ["sg_internal.h", "planner.h", "mpm_ops.cuh", "struct_for.cuh", "exchange_ops.cuh", "mpm_adj.cuh", "../../include/sg.h"]
+DEPS = SOURCES + ["sg_internal.h", "planner.h", "mpm_ops.cuh", "struct_for.cuh", "exchange_ops.cuh", "mpm_adj.cuh", "mpm_bin.cuh", "../../include/sg.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

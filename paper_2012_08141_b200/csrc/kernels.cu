@@ -330,10 +330,15 @@ __device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint3
 
 __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGArgs a) {
   __shared__ uint32_t s_warp[LG_TPB / 32];
-  __shared__ uint32_t s_tile, s_base, s_total, s_epoch;
+  __shared__ uint32_t s_tile, s_base, s_total, s_epoch, s_run;
   __shared__ uint32_t s_stage[LG_STAGE];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_epoch = ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu;
+  // solo: one CTA walks the tiles in order with a running prefix -- no tile
+  // counter, no look-back, no finisher atomics (small lists are a chain of
+  // dependent memory round trips, so every one removed counts)
+  const bool solo = gridDim.x == 1;
+  uint32_t solo_tile = 0;
+  if (threadIdx.x == 0) { s_epoch = solo ? 0u : ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu; s_run = 0u; }
   uint32_t nparent = a.mode == 0 ? 1u : ld_volatile(a.pcount);
   uint64_t nchunks = (uint64_t)nparent << a.lcpp;
   uint32_t ntiles = (uint32_t)((nchunks + LG_TILE - 1) / LG_TILE);
@@ -341,9 +346,14 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
   __syncthreads();
   const uint32_t epoch = s_epoch;
   while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&a.out.ctl[0], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    uint32_t tile;
+    if (solo) {
+      tile = solo_tile++;
+    } else {
+      if (threadIdx.x == 0) s_tile = atomicAdd(&a.out.ctl[0], 1u);
+      __syncthreads();
+      tile = s_tile;
+    }
     if (tile >= ntiles) break;
     uint32_t bits[LG_CPT], cs[LG_CPT], fs[LG_CPT];
     uint32_t cnt = 0;
@@ -413,8 +423,9 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       if (lane == 0) {
         s_total = total;
         // publish the aggregate now, so successors can look back while we stage
-        atomicExch((unsigned long long*)&a.out.status[tile],
-                   (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, total));
+        if (!solo)
+          atomicExch((unsigned long long*)&a.out.status[tile],
+                     (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, total));
       }
     }
     __syncthreads();
@@ -434,7 +445,9 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
         }
       }
     }
-    if (warp == 0) {
+    if (solo) {
+      if (threadIdx.x == 0) s_base = s_run;
+    } else if (warp == 0) {
       const uint32_t total = s_total;
       // single-pass decoupled look-back (deterministic tile order), one warp
       // inspecting 32 predecessors per step
@@ -496,6 +509,16 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       }
       __syncthreads();
     }
+    if (solo && threadIdx.x == 0) s_run = base + total;
+  }
+  if (solo) {
+    if (threadIdx.x == 0) {
+      uint32_t n = s_run;
+      if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
+      *a.out.count = n;
+      a.out.ctl[4] = 0u;   // the block table (if any) is stale until a struct-for rebuilds it
+    }
+    return;
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -516,6 +539,7 @@ __global__ void k_clear_list(uint32_t* count) { *count = 0; }
 #include "struct_for.cuh"
 #include "exchange_ops.cuh"
 #include "mpm_adj.cuh"
+#include "mpm_bin.cuh"
 
 // ---------------------------------------------------------------------------
 // Serial and range-for
@@ -857,10 +881,43 @@ static bool lb2_tree(const DTree& t) {
   return d.lbelow[0] == 2 && d.lbelow[1] == 2 && d.lbelow[2] == 2 && t.lblk == 6;
 }
 
+uint32_t bin_ntiles(uint32_t nkeys) { return (nkeys + BIN_TILE - 1) / BIN_TILE; }
+
+int launch_bin(const DBins& b, const float* x, int64_t xs, int64_t n, const int32_t* dcount, float inv_dx,
+               void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  BinArgs a;
+  a.B = b; a.x = x; a.xs = xs; a.n = n; a.dcount = dcount; a.inv_dx = inv_dx;
+  a.ntiles = bin_ntiles(b.nkeys);
+  const int gp = (int)std::max<int64_t>(1, std::min<int64_t>((n + BIN_TPB - 1) / BIN_TPB, (int64_t)num_sms() * 8));
+  const int gt = (int)std::min<uint32_t>(a.ntiles, (uint32_t)num_sms() * 4);
+  k_bin_count<<<gp, BIN_TPB, 0, s>>>(a);
+  k_bin_tiles<<<gt, BIN_TPB, 0, s>>>(a);
+  k_bin_top<<<1, 1024, 0, s>>>(a);
+  k_bin_apply<<<gt, BIN_TPB, 0, s>>>(a);
+  k_bin_scatter<<<gp, BIN_TPB, 0, s>>>(a);
+  return check_launch();
+}
+
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task,
-                     void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2) {
+                     void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2,
+                     const DBins* bins) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  if (nops == 1 && bins) {   // binned MPM kernels (LB = 2 trees; bins built by the caller)
+    MpmBinArgs m;
+    m.T = *grid_tree; m.TG = tree2 ? *tree2 : *grid_tree; m.C = c; m.op = ops[0]; m.B = *bins; m.task = task;
+    // (bin, chunk) grid: x strides over the non-empty bins, y over a bin's chunks
+    const dim3 grid((unsigned)num_sms() * 2, MB_CHUNKS_Y);
+    switch (ops[0].op) {
+      case SG_OP_P2G: k_p2g_bin<<<grid, MB_TPB, 0, s>>>(m); break;
+      case SG_OP_G2P: k_g2p_bin<<<grid, MB_TPB, 0, s>>>(m); break;
+      case SG_OP_G2P_ADJ: k_g2p_adj_bin<<<grid, MB_TPB, 0, s>>>(m); break;
+      case SG_OP_P2G_ADJ: k_p2g_adj_bin<<<grid, MB_TPB, 0, s>>>(m); break;
+      default: return -1;
+    }
+    return check_launch();
+  }
   if (nops == 1 && (ops[0].op == SG_OP_G2P_ADJ || ops[0].op == SG_OP_P2G_ADJ)) {
     Mpm2Args m;
     m.T = *grid_tree; m.TG = tree2 ? *tree2 : *grid_tree; m.C = c; m.op = ops[0]; m.n = n; m.task = task;

@@ -36,9 +36,8 @@ struct Mpm2Args {
 };
 
 template <int LB>
-__device__ __forceinline__ void mpm_g2p_adj(const Mpm2Args& A, int64_t i) {
-  const DevCtx& C = A.C;
-  const DOp& op = A.op;
+__device__ __forceinline__ void mpm_g2p_adj(const DevCtx& C, const DTree& T, const DTree& TG, const DOp& op,
+                                            int64_t i, int task) {
   const DArray X = C.arrays[op.a[0]];
   const int64_t nx = X.n;
   const float* x = (const float*)X.ptr;
@@ -64,8 +63,6 @@ __device__ __forceinline__ void mpm_g2p_adj(const Mpm2Args& A, int64_t i) {
     for (int d = 0; d < 3; d++) Ct[r][d] = cb1[(3 * r + d) * n1c + i] + (r == d ? Jb1 * J * dt : 0.0f);
   }
 
-  const DTree& T = A.T;
-  const DTree& TG = A.TG;
   const uint64_t fs = 1ull << T.ln_leaf, fsg = 1ull << TG.ln_leaf;
   const uint32_t* pool = T.seg[T.nseg - 1].base;
   uint32_t* poolg = TG.seg[TG.nseg - 1].base;
@@ -77,9 +74,9 @@ __device__ __forceinline__ void mpm_g2p_adj(const Mpm2Args& A, int64_t i) {
     gb[r] = (float*)(poolg + (uint64_t)op.slot[4 + r] * fsg);
   }
   MpmBlocks B, BG;
-  mpm_blocks<false, LB>(C, T, k.base, B, A.task);
-  if (op.act) mpm_blocks<true, LB>(C, TG, k.base, BG, A.task);
-  else mpm_blocks<false, LB>(C, TG, k.base, BG, A.task);
+  mpm_blocks<false, LB>(C, T, k.base, B, task);
+  if (op.act) mpm_blocks<true, LB>(C, TG, k.base, BG, task);
+  else mpm_blocks<false, LB>(C, TG, k.base, BG, task);
 
   auto node_u = [&](uint32_t off, int a, int b, int c, float pn[3], float& m, float u[3], float mask[3]) {
     m = 0.0f;
@@ -143,7 +140,7 @@ __device__ __forceinline__ void mpm_g2p_adj(const Mpm2Args& A, int64_t i) {
         for (int d = 0; d < 3; d++) xb[d] += Wbar * gW[d] - dposbar[d];
         const uint32_t og = mpm_node_off<LB>(TG, BG, k.base, a, b, c);
         if (og == SG_NO_BLOCK) {
-          if (C.debug) set_err(C, op.act ? SG_ERR_RANGE : SG_ERR_DEMOTION_TRAP, A.task);
+          if (C.debug) set_err(C, op.act ? SG_ERR_RANGE : SG_ERR_DEMOTION_TRAP, task);
           continue;
         }
         float mb = 0.0f;
@@ -162,9 +159,7 @@ __device__ __forceinline__ void mpm_g2p_adj(const Mpm2Args& A, int64_t i) {
 }
 
 template <int LB>
-__device__ __forceinline__ void mpm_p2g_adj(const Mpm2Args& A, int64_t i) {
-  const DevCtx& C = A.C;
-  const DOp& op = A.op;
+__device__ __forceinline__ void mpm_p2g_adj(const DevCtx& C, const DTree& T, const DOp& op, int64_t i, int task) {
   const DArray X = C.arrays[op.a[0]];
   const int64_t nx = X.n, nv = C.arrays[op.a[1]].n, nc = C.arrays[op.a[2]].n;
   const float* x = (const float*)X.ptr;
@@ -190,14 +185,13 @@ __device__ __forceinline__ void mpm_p2g_adj(const Mpm2Args& A, int64_t i) {
 #pragma unroll
     for (int c = 0; c < 3; c++) Am[r][c] = pm * cm[(3 * r + c) * nc + i] + (r == c ? kJ * (J - 1.0f) : 0.0f);
   }
-  const DTree& T = A.T;
   const uint64_t fs = 1ull << T.ln_leaf;
   const uint32_t* pool = T.seg[T.nseg - 1].base;
   const float* gb[4];
 #pragma unroll
   for (int r = 0; r < 4; r++) gb[r] = (const float*)(pool + (uint64_t)op.slot[r] * fs);
   MpmBlocks B;
-  mpm_blocks<false, LB>(C, T, k.base, B, A.task);
+  mpm_blocks<false, LB>(C, T, k.base, B, task);
   float xbar[3] = {0.0f, 0.0f, 0.0f}, vbar[3] = {0.0f, 0.0f, 0.0f}, Ab[3][3];
 #pragma unroll
   for (int r = 0; r < 3; r++)
@@ -245,13 +239,13 @@ __device__ __forceinline__ void mpm_p2g_adj(const Mpm2Args& A, int64_t i) {
 template <int LB>
 __global__ void __launch_bounds__(128, 3) k_g2p_adj(const __grid_constant__ Mpm2Args A) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x)
-    mpm_g2p_adj<LB>(A, i);
+    mpm_g2p_adj<LB>(A.C, A.T, A.TG, A.op, i, A.task);
 }
 
 template <int LB>
 __global__ void __launch_bounds__(128, 4) k_p2g_adj(const __grid_constant__ Mpm2Args A) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n; i += (int64_t)gridDim.x * blockDim.x)
-    mpm_p2g_adj<LB>(A, i);
+    mpm_p2g_adj<LB>(A.C, A.T, A.op, i, A.task);
 }
 
 // ADJ_INIT: a0[p0][i] = p1, every other entry of a0..a3 = 0 (generic range-for body).

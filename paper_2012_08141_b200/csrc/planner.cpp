@@ -129,6 +129,13 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
   return u;
 }
 
+uint32_t task_array_writes(const sg_task& t) {
+  uint32_t m = 0;
+  for (const OpUse& u : op_uses(t))
+    if (u.array && (u.role & R_WRITE)) m |= 1u << u.slot;
+  return m;
+}
+
 static int op_min_fields(int op) {
   switch (op) {
     case SG_OP_FILL: case SG_OP_INC: case SG_OP_JITTER: case SG_OP_CLEAR_SCALAR: case SG_OP_DOWNSAMPLE: return 1;

@@ -111,5 +111,8 @@ struct Graph {
 };
 Graph build_graph(const std::vector<PTask>& seq);
 
+// Bit i set: the op writes arrays[i] (from the planner's op-use table).
+uint32_t task_array_writes(const sg_task& t);
+
 }  // namespace sg
 #endif

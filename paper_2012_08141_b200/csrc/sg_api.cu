@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -56,6 +57,18 @@ struct sg_grid {
   uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
   uint64_t mig_tiles = 0;
   uint32_t* mig_ctl = nullptr;
+  // particle bins (binned MPM kernels) + a one-entry cache keyed by the
+  // position array, its write epoch, the tree and the range
+  DBins bins{};
+  int64_t bin_cap = 0;
+  uint32_t bin_keys_cap = 0;
+  bool bin_valid = false;
+  int bin_xarr = -1, bin_tree = -1;
+  uint64_t bin_epoch = 0;
+  int64_t bin_n = 0;
+  const int32_t* bin_dcount = nullptr;
+  bool no_bin = false;                 // SG_NO_BIN=1: per-particle kernels (A/B measurements)
+  std::vector<uint64_t> arr_epoch;     // bumped by every launched task that writes the array
   // launch profiling (benchmarks): event pairs per launch group
   bool profiling = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -350,6 +363,7 @@ extern "C" sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_o
   if (o) g->opts = *o;
   g->plan_only = g->opts.plan_only != 0;
   g->stream = (cudaStream_t)g->opts.stream;
+  { const char* e = std::getenv("SG_NO_BIN"); g->no_bin = e && e[0] == '1'; }
   sg_status rc = build_layout(nodes, n, g->L);
   if (rc) { delete g; return rc; }
   g->dtrees.resize(g->L.trees.size());
@@ -437,6 +451,7 @@ extern "C" sg_status sg_register_array(sg_grid* g, void* ptr, int64_t n, int32_t
   }
   DArray a{ptr, n, ncomp, dtype, nullptr};
   g->arrays.push_back(a);
+  g->arr_epoch.push_back(0);
   *id = (int32_t)g->arrays.size() - 1;
   if (!g->plan_only)
     CUDA_TRY(cudaMemcpyAsync(g->d_arrays + *id, &a, sizeof(DArray), cudaMemcpyHostToDevice, g->stream));
@@ -535,6 +550,54 @@ static int grid_hint_struct(const sg_grid* g, const DTree& T) {
   uint64_t cap = g->lists.empty() ? 1 : 1;
   (void)cap;
   return g->num_sms * 8;
+}
+
+static bool tree_lb2(const DTree& t) {
+  if (t.nd != 3 || t.driving < 0 || t.lblk != 6) return false;
+  const DLevel& d = t.lev[t.driving];
+  return d.lbelow[0] == 2 && d.lbelow[1] == 2 && d.lbelow[2] == 2;
+}
+
+// Bins of the particles in position array xa over tree `tree` (4^3 leaf
+// blocks); rebuilt unless the cache holds the same (array, epoch, tree, range).
+static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t n, const int32_t* dcount) {
+  const DTree& T = g->dtrees[tree];
+  const DLevel& leaf = T.lev[T.nlev - 1];
+  int nb[3];
+  for (int a = 0; a < 3; a++) nb[a] = (1 << leaf.lres[a]) >> 2;
+  const uint64_t nk = (uint64_t)nb[0] * nb[1] * nb[2] + 1;
+  if (nk > 0x7fffffffull) return fail(SG_ERR_ARG, "too many leaf blocks for particle binning");
+  const uint32_t nkeys = (uint32_t)nk;
+  const int64_t cap = g->arrays[xa].n;
+  if (cap > g->bin_cap) {
+    g->bins.rank = (uint32_t*)g->dev_alloc((size_t)cap * 4);
+    g->bins.key = (uint32_t*)g->dev_alloc((size_t)cap * 4);
+    g->bins.perm = (uint32_t*)g->dev_alloc((size_t)cap * 4);
+    if (!g->bins.rank || !g->bins.key || !g->bins.perm) return fail(SG_ERR_CUDA, "bin allocation failed");
+    g->bin_cap = cap;
+  }
+  if (nkeys > g->bin_keys_cap) {
+    const uint32_t nt = bin_ntiles(nkeys);
+    g->bins.hist = (uint32_t*)g->dev_alloc((size_t)nt * 2048 * 4);
+    g->bins.off = (uint32_t*)g->dev_alloc(((size_t)nkeys + 1) * 4);
+    g->bins.tsum = (uint32_t*)g->dev_alloc((size_t)nt * 8);
+    g->bins.bins = (uint32_t*)g->dev_alloc((size_t)nkeys * 4);
+    if (!g->bins.nbins) g->bins.nbins = (uint32_t*)g->dev_alloc(16);
+    if (!g->bins.hist || !g->bins.off || !g->bins.tsum || !g->bins.bins || !g->bins.nbins)
+      return fail(SG_ERR_CUDA, "bin allocation failed");
+    CUDA_TRY(cudaMemsetAsync(g->bins.hist, 0, (size_t)nt * 2048 * 4, g->stream));
+    g->bin_keys_cap = nkeys;
+  }
+  g->bins.nkeys = nkeys;
+  for (int a = 0; a < 3; a++) g->bins.nb[a] = nb[a];
+  if (g->bin_valid && g->bin_xarr == xa && g->bin_epoch == g->arr_epoch[xa] && g->bin_tree == tree &&
+      g->bin_n == n && g->bin_dcount == dcount)
+    return SG_OK;
+  if (launch_bin(g->bins, (const float*)g->arrays[xa].ptr, g->arrays[xa].n, n, dcount, inv_dx, g->stream))
+    return fail(SG_ERR_CUDA, std::string("binning launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  g->bin_valid = true;
+  g->bin_xarr = xa; g->bin_epoch = g->arr_epoch[xa]; g->bin_tree = tree; g->bin_n = n; g->bin_dcount = dcount;
+  return SG_OK;
 }
 
 static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const std::vector<uint32_t>& acts,
@@ -652,7 +715,13 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
         gt = &g->dtrees[g->L.field_tree[tk.fields[0]]];
       const DTree* gt2 = nullptr;   // G2P_ADJ: the adjoint tree
       if (tk.op == SG_OP_G2P_ADJ) gt2 = &g->dtrees[g->L.field_tree[tk.fields[4]]];
-      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt, gt2);
+      const DBins* bp = nullptr;
+      const bool mpm_op = tk.op == SG_OP_P2G || tk.op == SG_OP_G2P || tk.op == SG_OP_G2P_ADJ || tk.op == SG_OP_P2G_ADJ;
+      if (nops == 1 && mpm_op && gt && !g->no_bin && tree_lb2(*gt) && (!gt2 || tree_lb2(*gt2))) {
+        if ((rc = ensure_bins(g, g->L.field_tree[tk.fields[0]], tk.arrays[0], ops[0].p[1], n, dcount))) return rc;
+        bp = &g->bins;
+      }
+      rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt, gt2, bp);
     } break;
     case TT_SERIAL: {
       DOp ops[SG_MAXOPS];
@@ -667,6 +736,14 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
     default: rc = SG_ERR_ARG;
   }
   if (rc) return fail(rc, std::string("launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  if (t0.type == TT_RANGE_FOR || t0.type == TT_SERIAL || t0.type == TT_STRUCT_FOR) {
+    for (int m : members) {
+      const sg_task& tk = g->eager[m].t;
+      const uint32_t w = task_array_writes(tk);
+      for (int s = 0; s < 8; s++)
+        if (((w >> s) & 1u) && tk.arrays[s] >= 0 && tk.arrays[s] < (int)g->arr_epoch.size()) g->arr_epoch[tk.arrays[s]]++;
+    }
+  }
   st.launches++;
   return SG_OK;
 }
@@ -685,6 +762,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
   }
   st.tasks_lowered = (int64_t)g->eager.size();
   g->last_plan.clear();
+  g->bin_valid = false;   // arrays may have been rewritten outside the library since the last flush
   if (g->eager.empty()) {
     if (out) *out = st;
     return SG_OK;
@@ -730,7 +808,8 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         e1 = g->get_event();
         cudaEventRecord(e1, g->stream);
         const PTask& t = g->eager[mem[0]];
-        int key = t.type == TT_STRUCT_FOR ? 100 + t.t.op : t.type == TT_LISTGEN ? 200 + t.snode : t.type;
+        int key = t.type == TT_STRUCT_FOR ? 100 + t.t.op : t.type == TT_LISTGEN ? 200 + t.snode
+                : t.type == TT_RANGE_FOR ? 300 + t.t.op : t.type;
         g->prof_pending.push_back({key, {e0, e1}});
       }
     }
@@ -918,7 +997,8 @@ extern "C" sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int
     float t = 0;
     cudaEventElapsedTime(&t, p.second.first, p.second.second);
     int key = p.first;
-    int kinds[2] = {key >= 200 ? TT_LISTGEN : key >= 100 ? TT_STRUCT_FOR : key, key >= 100 ? key : -1};
+    int kinds[2] = {key >= 300 ? TT_RANGE_FOR : key >= 200 ? TT_LISTGEN : key >= 100 ? TT_STRUCT_FOR : key,
+                    key >= 100 ? key : -1};
     for (int k : kinds) {
       if (k >= 0 && k < n_kinds) { ms[k] += t; count[k]++; }
     }

@@ -122,6 +122,20 @@ struct DOp {
   float p[8];
 };
 
+// Particle bins (csrc/mpm_bin.cuh): counting sort of particle ids by leaf block.
+struct DBins {
+  uint32_t* hist;     // [nkeys_pad] counts, zero between uses
+  uint32_t* rank;     // [cap] rank of particle i within its bin
+  uint32_t* key;      // [cap] bin of particle i
+  uint32_t* off;      // [nkeys + 1] exclusive prefix of the counts (off[nkeys] = n)
+  uint32_t* tsum;     // [2 * ntiles] per-tile (count, non-empty) sums -> prefixes
+  uint32_t* bins;     // [nkeys] non-empty keys, ascending
+  uint32_t* nbins;    // [1]
+  uint32_t* perm;     // [cap] particle ids sorted by bin (stable within a bin: no)
+  uint32_t nkeys;     // blocks in the domain + 1 (overflow)
+  int nb[3];          // blocks per axis
+};
+
 struct DevCtx {
   DTree* trees;        // device array
   DField* fields;      // device array
@@ -156,7 +170,13 @@ struct RangeScratch {
   uint32_t* ctl;      // [0..3] migrate tile/done/epoch/count, [5] append ticket
 };
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task_id,
-                     void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2);
+                     void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2,
+                     const DBins* bins);
+// Bin the particles of position array x (3 comps, component stride xs) by the
+// leaf blocks of a tree with 4^3 blocks (nb blocks per axis).
+int launch_bin(const DBins& b, const float* x, int64_t xs, int64_t n, const int32_t* dcount, float inv_dx,
+               void* stream);
+uint32_t bin_ntiles(uint32_t nkeys);
 int launch_serial(const DevCtx& c, const DOp* ops, int nops, int task_id, void* stream);
 int launch_deactivate(const DevCtx& c, const DTree& t, int tree_id, int level, const DList* lists,
                       int task_id, void* stream);

@@ -371,7 +371,7 @@ def set_array_count(grid, array_id, count_tensor):
     grid._keep.append(count_tensor)
     _check(_lib.sg_set_array_count(grid.h, array_id, _vp(count_tensor.data_ptr())))
 
-PROFILE_KINDS = 300
+PROFILE_KINDS = 400
 
 
 def set_profiling(grid, on=True):
@@ -379,7 +379,8 @@ def set_profiling(grid, on=True):
 
 
 def profile_read(grid):
-    """{kind: (total_ms, launches)}; kinds 0..6 task types, 100+op struct-for ops."""
+    """{kind: (total_ms, launches)}; kinds 0..6 task types, 100+op struct-for ops,
+    200+snode listgens, 300+op range-for ops."""
     ms = (ctypes.c_double * PROFILE_KINDS)()
     cnt = (ctypes.c_int64 * PROFILE_KINDS)()
     _check(_lib.sg_profile_read(grid.h, ms, cnt, PROFILE_KINDS))

@@ -74,7 +74,11 @@ def check_one_substep(prog, L, lg, tol=1e-4):
     return st
 
 
-def test_c4_one_backward_substep_small():
+@pytest.mark.parametrize("binned", [True, False])
+def test_c4_one_backward_substep_small(binned, monkeypatch):
+    # binned kernels (default) and the per-particle kernels (SG_NO_BIN=1)
+    if not binned:
+        monkeypatch.setenv("SG_NO_BIN", "1")
     prog, L, lg = one_substep_program(32, 4000, seed=11)
     check_one_substep(prog, L, lg)
 

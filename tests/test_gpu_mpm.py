@@ -47,8 +47,10 @@ def compare_mpm(g, arrs, o, prog, tol=1e-5, grid_fields=None):
         assert not bad.any(), f"array {name}: {bad.sum()} off, worst {np.abs(got - want)[bad].max()}"
 
 
-@pytest.mark.parametrize("passes", [0, "all"])
-def test_c3_small_one_step(passes):
+@pytest.mark.parametrize("passes,binned", [(0, True), ("all", True), ("all", False)])
+def test_c3_small_one_step(passes, binned, monkeypatch):
+    if not binned:   # per-particle P2G / G2P kernels (SG_NO_BIN=1) instead of the binned ones
+        monkeypatch.setenv("SG_NO_BIN", "1")
     prog = W.c3_program(n_grid=32, n_particles=4000, steps=1, seed=5, v_scale=1.0, J_jitter=0.02,
                         lo=0.2, hi=0.7)
     o = oracle.run_program(prog)
