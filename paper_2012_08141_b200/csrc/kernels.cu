@@ -859,6 +859,19 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   if (nd == 3 && a->lb[0] == 3 && a->lb[1] == 3 && a->lb[2] == 3) gl = 1;
   else if (nd == 3 && a->lb[0] == 2 && a->lb[1] == 2 && a->lb[2] == 2) gl = 2;
   else if (nd == 2 && a->lb[0] == 2 && a->lb[1] == 2) gl = 3;
+  // dedicated kernel: a lone f32 JACOBI over 8^3 dense blocks with a block table
+  if (nops == 1 && ops[0].op == SG_OP_JACOBI && gl == 1 && !i32 && !t.leaf_bitmasked && nphases <= 1 && drive &&
+      drive->table && getenv("SG_NO_JAC8") == nullptr) {
+    JacArgs j;
+    j.T = t; j.entries = drive->entries; j.count = drive->count; j.table = drive->table; j.table_ctl = drive->ctl;
+    const uint64_t fs = 1ull << t.ln_leaf;
+    j.s_dst = (uint64_t)ops[0].slot[0] * fs; j.s_src = (uint64_t)ops[0].slot[1] * fs;
+    j.s_rhs = (uint64_t)ops[0].slot[2] * fs;
+    j.inv = 1.0f / 6.0f;
+    k_jacobi8<<<num_sms() * 4, 256, 0, s>>>(j);
+    delete a;
+    return check_launch();
+  }
 #define SG_SF_LAUNCH(V)                                                                           \
   switch (nd * 10 + gl) {                                                                         \
     case 10: sf_dispatch<V, 1, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \

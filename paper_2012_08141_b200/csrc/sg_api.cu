@@ -49,7 +49,15 @@ struct sg_grid {
   std::vector<std::pair<const int32_t*, int64_t>> coords_seen;
   std::unordered_map<uint64_t, Plan> cache;
   std::vector<PlanRecord> last_plan;
-  int64_t task_counter = 0;
+  int64_t task_counter = 0;         // launch index inside the current flush (error reports)
+  // CUDA graphs: a plan that already ran once is captured (on a private
+  // stream), instantiated once per plan and updated in place afterwards, and
+  // replayed with one cudaGraphLaunch on the user stream
+  bool use_graphs = true;           // SG_NO_GRAPH=1 disables
+  cudaStream_t user_stream = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  std::unordered_map<uint64_t, cudaGraphExec_t> gexec;
+  std::unordered_map<uint64_t, int> plan_runs;
   int num_sms = 148;
   char* chain_buf = nullptr;        // SG_PASS_CHAIN op tables
   size_t chain_bytes = 0;
@@ -83,7 +91,7 @@ struct sg_grid {
   void* dev_alloc(size_t bytes) {
     if (bytes == 0) bytes = 4;
     void* p = nullptr;
-    if (opts.alloc) p = opts.alloc(opts.alloc_ctx, bytes, (void*)stream);
+    if (opts.alloc) p = opts.alloc(opts.alloc_ctx, bytes, (void*)user_stream);
     else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
     if (p) allocs.push_back(p);
     return p;
@@ -363,7 +371,9 @@ extern "C" sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_o
   if (o) g->opts = *o;
   g->plan_only = g->opts.plan_only != 0;
   g->stream = (cudaStream_t)g->opts.stream;
+  g->user_stream = g->stream;
   { const char* e = std::getenv("SG_NO_BIN"); g->no_bin = e && e[0] == '1'; }
+  { const char* e = std::getenv("SG_NO_GRAPH"); g->use_graphs = !(e && e[0] == '1'); }
   sg_status rc = build_layout(nodes, n, g->L);
   if (rc) { delete g; return rc; }
   g->dtrees.resize(g->L.trees.size());
@@ -431,6 +441,9 @@ extern "C" sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_o
 extern "C" sg_status sg_destroy(sg_grid* g) {
   if (!g) return SG_OK;
   if (!g->plan_only) cudaStreamSynchronize(g->stream);
+  for (auto& kv : g->gexec)
+    if (kv.second) cudaGraphExecDestroy(kv.second);
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   delete g;
   return SG_OK;
 }
@@ -603,7 +616,7 @@ static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t
 static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const std::vector<uint32_t>& acts,
                               const std::vector<int>& phase_end, sg_stats& st) {
   const PTask& t0 = g->eager[members[0]];
-  int task = (int)(g->task_counter++ & 0x7FFFFFFF);
+  int task = (int)(g->task_counter++ & 0x7FFFFFFF);   // launch index in the flush: stable across replays
   int rc = 0;
   switch (t0.type) {
     case TT_ACTIVATE: {
@@ -786,6 +799,24 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
   auto t1 = std::chrono::steady_clock::now();
   st.plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
   sg_status rc = SG_OK;
+  g->task_counter = 0;
+  // CUDA graph replay of a plan that already ran once (its allocations done);
+  // chains upload a host op table per flush and stay on direct launches
+  bool capturing = false;
+  const cudaStream_t user = g->stream;
+  if (!g->plan_only && g->use_graphs && !g->profiling && g->plan_runs[key]++ > 0) {
+    bool chain = false;
+    for (const auto& pe : plan->phase_ends) chain |= pe.size() > 1;
+    if (!chain) {
+      if (!g->cap_stream) cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking);
+      if (g->cap_stream && cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+        g->stream = g->cap_stream;
+        capturing = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
   for (size_t gi = 0; gi < plan->groups.size(); gi++) {
     const auto& mem = plan->groups[gi];
     const auto& acts = plan->acts[gi];
@@ -812,6 +843,29 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
                 : t.type == TT_RANGE_FOR ? 300 + t.t.op : t.type;
         g->prof_pending.push_back({key, {e0, e1}});
       }
+    }
+  }
+  if (capturing) {
+    g->stream = user;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(g->cap_stream, &graph);
+    if (e != cudaSuccess || rc) {
+      if (graph) cudaGraphDestroy(graph);
+      if (!rc) rc = fail(SG_ERR_CUDA, std::string("graph capture failed: ") + cudaGetErrorString(e));
+    } else {
+      cudaGraphExec_t& ex = g->gexec[key];
+      bool ok = false;
+      if (ex) {
+        cudaGraphExecUpdateResultInfo info;
+        ok = cudaGraphExecUpdate(ex, graph, &info) == cudaSuccess;
+        if (!ok) { cudaGetLastError(); cudaGraphExecDestroy(ex); ex = nullptr; }
+      }
+      if (!ok && cudaGraphInstantiate(&ex, graph, 0) != cudaSuccess) {
+        ex = nullptr;
+        rc = fail(SG_ERR_CUDA, "graph instantiation failed");
+      }
+      if (ex && cudaGraphLaunch(ex, g->stream) != cudaSuccess) rc = fail(SG_ERR_CUDA, "graph launch failed");
+      cudaGraphDestroy(graph);
     }
   }
   g->eager.clear();

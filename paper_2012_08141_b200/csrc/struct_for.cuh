@@ -733,3 +733,126 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5)
   if (A.has_reduce) finish_reductions<V>(A, s_ops, last_n);
   sf_mark_table(A, rows_ok0);
 }
+
+// ---------------------------------------------------------------------------
+// Dedicated JACOBI for 8^3 dense leaf blocks (C2, JAC-XL): a lone f32 JACOBI
+// op is the solve's hot loop (89% of the C2 step), so it gets a kernel without
+// the op-table interpreter or shared-memory tiles.  One warp per half block
+// (two quads of 4 cells along z per lane, 64 per warp).
+// Block rows (block + 6 face neighbours) come from the list's block table (one
+// 12-word row read by 12 lanes, broadcast by shuffles); the fast-axis
+// neighbours inside the block come from the partner lane by one shuffle, the
+// rest are uint4 rows (in-block, or the neighbour block's facing plane,
+// predicated off -- reading 0 -- when the neighbour is absent).
+// Same arithmetic order as the interpreter's quad path.
+// ---------------------------------------------------------------------------
+struct JacArgs {
+  DTree T;
+  const uint32_t* entries;
+  const uint32_t* count;
+  BlockRow* table;
+  uint32_t* table_ctl;
+  uint64_t s_dst, s_src, s_rhs;   // field offsets (words) from the pool base
+  float inv;
+};
+
+// out of line: the slow path must not shape the hot loop's register allocation
+__device__ __noinline__ void jac_row_slow(const DTree& T, uint32_t entry, BlockRow* out) {
+  make_block_row(T, entry, out);
+}
+
+__device__ __forceinline__ float4 u2f(uint4 u) {
+  return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+}
+
+__global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacArgs A) {
+  const uint32_t* P = A.T.seg[A.T.nseg - 1].base;
+  const uint32_t* __restrict__ src = P + A.s_src;
+  const uint32_t* __restrict__ rhs = P + A.s_rhs;
+  uint32_t* dst = const_cast<uint32_t*>(P) + A.s_dst;
+  const uint32_t nent = *A.count;
+  const bool rows_ok = *(volatile const uint32_t*)&A.table_ctl[4] != 0u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), GW = gridDim.x * (blockDim.x >> 5);
+  // one warp per half block; a lane owns the quads at x0 = 4*part + 2*(lane/16)
+  // and x0 + 1 (same y, z-half): their shared x face is loaded once
+  const int xp2 = (lane >> 4) * 2, y = (lane >> 1) & 7, zh = lane & 1;
+  for (uint32_t wq = gw; wq < nent * 2u; wq += GW) {
+    const uint32_t e = wq >> 1, part = wq & 1u;
+    uint32_t blk, nb[6];
+    if (rows_ok) {
+      const uint32_t rv = lane < 12 ? reinterpret_cast<const uint32_t*>(A.table + e)[lane] : 0u;
+      blk = __shfl_sync(0xffffffffu, rv, 0);
+#pragma unroll
+      for (int d = 0; d < 6; d++) nb[d] = __shfl_sync(0xffffffffu, rv, 6 + d);
+    } else {
+      // no table yet (first struct-for after a listgen): every lane resolves
+      // the row; the part-0 warp stores it for the following launches
+      BlockRow r;
+      jac_row_slow(A.T, A.entries[e], &r);
+      if (part == 0 && lane == 0) A.table[e] = r;
+      blk = r.blk;
+#pragma unroll
+      for (int d = 0; d < 6; d++) nb[d] = r.nbr[d];
+    }
+    if (blk == SG_NO_BLOCK) continue;
+    const int x0 = (int)part * 4 + xp2;
+    const uint32_t j0 = ((uint32_t)x0 << 6) | ((uint32_t)y << 3) | ((uint32_t)zh << 2), j1 = j0 + 64u;
+    const uint32_t o0 = blk + j0, o1 = o0 + 64u;
+    // every load of both quads issued before the arithmetic
+    const uint4 c0u = *reinterpret_cast<const uint4*>(src + o0);
+    const uint4 c1u = *reinterpret_cast<const uint4*>(src + o1);
+    const uint4 r0u = *reinterpret_cast<const uint4*>(rhs + o0);
+    const uint4 r1u = *reinterpret_cast<const uint4*>(rhs + o1);
+    const uint32_t nz = zh ? nb[5] : nb[4];
+    const uint32_t zo = zh ? 0u : 7u;
+    const float z0 = __uint_as_float(ld1_if(src + nz + (j0 & ~7u) + zo, nz != SG_NO_BLOCK));
+    const float z1 = __uint_as_float(ld1_if(src + nz + (j1 & ~7u) + zo, nz != SG_NO_BLOCK));
+    const uint4 xmu = ld4_if(src + (x0 > 0 ? o0 - 64u : nb[0] + j0 + 448u), x0 > 0 || nb[0] != SG_NO_BLOCK);
+    const uint4 xpu = ld4_if(src + (x0 + 1 < 7 ? o1 + 64u : nb[1] + j1 - 448u), x0 + 1 < 7 || nb[1] != SG_NO_BLOCK);
+    const bool ym_in = y > 0, yp_in = y < 7;
+    const uint32_t ym0 = ym_in ? o0 - 8u : nb[2] + j0 + 56u, yp0 = yp_in ? o0 + 8u : nb[3] + j0 - 56u;
+    const uint4 ym0u = ld4_if(src + ym0, ym_in || nb[2] != SG_NO_BLOCK);
+    const uint4 yp0u = ld4_if(src + yp0, yp_in || nb[3] != SG_NO_BLOCK);
+    const uint4 ym1u = ld4_if(src + ym0 + 64u, ym_in || nb[2] != SG_NO_BLOCK);
+    const uint4 yp1u = ld4_if(src + yp0 + 64u, yp_in || nb[3] != SG_NO_BLOCK);
+    const float4 c0 = u2f(c0u), c1 = u2f(c1u);
+    const float p0 = __shfl_xor_sync(0xffffffffu, zh ? c0.x : c0.w, 1);
+    const float p1 = __shfl_xor_sync(0xffffffffu, zh ? c1.x : c1.w, 1);
+    const float inv = A.inv;
+    {
+      const float lo = zh ? p0 : z0, hi = zh ? z0 : p0;
+      const float4 xm = u2f(xmu), xp = c1, ym = u2f(ym0u), yp = u2f(yp0u), r = u2f(r0u);
+      float s0 = lo + c0.y, s1 = c0.x + c0.z, s2 = c0.y + c0.w, s3 = c0.z + hi;
+      s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
+      s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
+      s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
+      s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
+      *reinterpret_cast<uint4*>(dst + o0) = make_uint4(__float_as_uint((r.x + s0) * inv), __float_as_uint((r.y + s1) * inv),
+                                                       __float_as_uint((r.z + s2) * inv), __float_as_uint((r.w + s3) * inv));
+    }
+    {
+      const float lo = zh ? p1 : z1, hi = zh ? z1 : p1;
+      const float4 xm = c0, xp = u2f(xpu), ym = u2f(ym1u), yp = u2f(yp1u), r = u2f(r1u);
+      float s0 = lo + c1.y, s1 = c1.x + c1.z, s2 = c1.y + c1.w, s3 = c1.z + hi;
+      s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
+      s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
+      s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
+      s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
+      *reinterpret_cast<uint4*>(dst + o1) = make_uint4(__float_as_uint((r.x + s0) * inv), __float_as_uint((r.y + s1) * inv),
+                                                       __float_as_uint((r.z + s2) * inv), __float_as_uint((r.w + s3) * inv));
+    }
+  }
+  // the rows built here (no table yet) become the list's block table
+  if (!rows_ok) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&A.table_ctl[3], 1u) == gridDim.x - 1) {
+        A.table_ctl[3] = 0u;
+        __threadfence();
+        A.table_ctl[4] = 1u;
+      }
+    }
+  }
+}

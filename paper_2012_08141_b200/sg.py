@@ -213,6 +213,14 @@ class Grid:
         _check(_lib.sg_listgen(self.h, snode))
 
     def task(self, kind, op, snode=-1, fields=(), arrays=(), params=(), activating=(), n=0):
+        # marshalled descriptors are memoized: repeated launches (solver loops)
+        # cost one ctypes call
+        key = (kind, op, snode, tuple(fields), tuple(arrays), tuple(params), tuple(activating), n)
+        cache = self.__dict__.setdefault("_task_cache", {})
+        t = cache.get(key)
+        if t is not None:
+            _check(_lib.sg_struct_for(self.h, ctypes.byref(t)))
+            return
         t = Task()
         t.kind = kind
         t.op = OPS[op] if isinstance(op, str) else op
@@ -223,6 +231,8 @@ class Grid:
             t.arrays[i] = arrays[i] if i < len(arrays) else -1
             t.params[i] = params[i] if i < len(params) else 0.0
         t.activating = sum(1 << i for i, a in enumerate(activating) if a)
+        if len(cache) < 65536:
+            cache[key] = t
         _check(_lib.sg_struct_for(self.h, ctypes.byref(t)))
 
     def struct_for(self, op, snode, fields, params=(), activating=()):
