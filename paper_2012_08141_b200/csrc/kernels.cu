@@ -1003,6 +1003,47 @@ int launch_serial(const DevCtx& c, const DOp* ops, int nops, int, void* stream) 
   return check_launch();
 }
 
+// DEACTIVATE as a pool reset (reading R33): the deactivated level is the
+// tree's first sparse level, so every container of every pool is freed -- zero
+// the root container and each pool's allocated containers (free-listed ones are
+// already zero), then the last CTA resets the bump counters and free lists.
+struct ResetArgs {
+  DTree T;
+};
+
+__global__ void __launch_bounds__(256) k_deactivate_reset(const __grid_constant__ ResetArgs A) {
+  const DTree& T = A.T;
+  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gsz = (uint64_t)gridDim.x * blockDim.x;
+  for (int s = 0; s < T.nseg; s++) {
+    const DSeg& S = T.seg[s];
+    uint64_t n = 1;
+    if (s > 0) {
+      const int32_t b = *(volatile const int32_t*)&S.alloc[0];
+      n = (uint64_t)min((uint32_t)max(b, 0), S.capacity);
+    }
+    const uint64_t words = n * S.stride;   // containers are 128-byte aligned: stride % 4 == 0
+    uint4* p = reinterpret_cast<uint4*>(S.base);
+    for (uint64_t i = gtid; i < words / 4; i += gsz) p[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (T.nseg < 2) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&T.seg[1].alloc[2], 1) == (int)gridDim.x - 1) {
+      for (int s = 1; s < T.nseg; s++) { T.seg[s].alloc[0] = 0; T.seg[s].alloc[1] = 0; }
+      T.seg[1].alloc[2] = 0;
+      __threadfence();
+    }
+  }
+}
+
+int launch_deactivate_reset(const DTree& t, void* stream) {
+  ResetArgs a;
+  a.T = t;
+  k_deactivate_reset<<<num_sms() * 4, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch();
+}
+
 int launch_deactivate(const DevCtx& c, const DTree& t, int, int level, const DList* lists, int, void* stream) {
   DeArgs a;
   a.T = t; a.C = c; a.ls = level;

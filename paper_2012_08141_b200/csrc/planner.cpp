@@ -37,6 +37,18 @@ std::vector<int> HLayout::listed_levels(int t) const {
   return out;
 }
 
+bool HLayout::deactivate_resets(int snode) const {
+  if (snode <= 0 || snode >= (int)nodes.size() || snode_tree[snode] < 0) return false;
+  const HTree& T = trees[snode_tree[snode]];
+  int first = -1;
+  for (int s : T.levels)
+    if (is_sparse(s)) { first = s; break; }
+  if (first != snode) return false;
+  double cells = 1.0;
+  for (int s : T.levels) cells *= (double)nodes[s].extent[0] * nodes[s].extent[1] * nodes[s].extent[2];
+  return cells * 4.0 * std::max<size_t>(1, T.fields.size()) <= 64.0 * 1024 * 1024;
+}
+
 std::vector<int> HLayout::sparse_levels(int t) const {
   std::vector<int> out;
   for (int s : trees[t].levels)
@@ -189,16 +201,18 @@ void task_meta(const HLayout& L, PTask& t) {
       break;
     case TT_DEACTIVATE: {
       const HTree& T = L.trees[t.tree];
-      for (int s : L.listed_levels(t.tree)) t.in.push_back({skey(ST_LIST, s), AC_NONE, false});
+      const bool reset = L.deactivate_resets(t.snode);
+      if (!reset)
+        for (int s : L.listed_levels(t.tree)) t.in.push_back({skey(ST_LIST, s), AC_NONE, false});
       int pos = L.snode_pos[t.snode];
       for (size_t k = pos; k < T.levels.size(); k++) {
         int s = T.levels[k];
         if (!L.is_sparse(s)) continue;
-        t.in.push_back({skey(ST_MASK, s), AC_NONE, false});
+        if (!reset) t.in.push_back({skey(ST_MASK, s), AC_NONE, false});
         t.out.push_back({skey(ST_MASK, s), AC_NONE, true});
         if (L.nodes[s].kind == SG_POINTER) {
-          t.in.push_back({skey(ST_ALLOC, s), AC_NONE, false});
-          t.out.push_back({skey(ST_ALLOC, s), AC_NONE, false});
+          if (!reset) t.in.push_back({skey(ST_ALLOC, s), AC_NONE, false});
+          t.out.push_back({skey(ST_ALLOC, s), AC_NONE, reset});
         }
       }
       for (int f : T.fields) t.out.push_back({skey(ST_VALUE, f), AC_ID, true});

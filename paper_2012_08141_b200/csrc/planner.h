@@ -32,6 +32,10 @@ struct HLayout {
   // sparse levels a struct-for over tree t needs a list for (reading R5)
   std::vector<int> listed_levels(int t) const;
   std::vector<int> sparse_levels(int t) const;
+  // DEACTIVATE of the tree's first sparse level on a tree whose dense volume is
+  // at most 64 MiB runs as a pool RESET (zero every allocated container, reset
+  // the allocators): no list input, so its listgens fall to DSE (reading R33)
+  bool deactivate_resets(int snode) const;
 };
 
 // ---- states ------------------------------------------------

@@ -744,7 +744,8 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
     } break;
     case TT_DEACTIVATE: {
       const DTree& T = g->dtrees[t0.tree];
-      rc = launch_deactivate(g->ctx, T, t0.tree, g->L.snode_pos[t0.snode], g->lists[t0.tree].data(), task, g->stream);
+      if (g->L.deactivate_resets(t0.snode)) rc = launch_deactivate_reset(T, g->stream);
+      else rc = launch_deactivate(g->ctx, T, t0.tree, g->L.snode_pos[t0.snode], g->lists[t0.tree].data(), task, g->stream);
     } break;
     default: rc = SG_ERR_ARG;
   }

@@ -180,6 +180,7 @@ uint32_t bin_ntiles(uint32_t nkeys);
 int launch_serial(const DevCtx& c, const DOp* ops, int nops, int task_id, void* stream);
 int launch_deactivate(const DevCtx& c, const DTree& t, int tree_id, int level, const DList* lists,
                       int task_id, void* stream);
+int launch_deactivate_reset(const DTree& t, void* stream);
 int launch_read_field(const DevCtx& c, const DTree& t, int tree_id, int slot, uint32_t* dense, void* stream);
 int launch_load_field(const DevCtx& c, const DTree& t, int tree_id, int slot, const uint32_t* dense, void* stream);
 int launch_mask_scan(const DevCtx& c, const DTree& t, int tree_id, int level, uint8_t* flags, void* stream);

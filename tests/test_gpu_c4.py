@@ -103,7 +103,7 @@ def test_c4_small_window(passes):
         want, mag = o.array(i, with_mag=True)
         close(arrs[names[i]].cpu().numpy(), want, mag, 1e-3, names[i], floor=1e-5)
     if passes == "all":
-        assert st[0]["dead_removed"] == 4 * T
+        assert st[0]["dead_removed"] == 8 * T
 
 
 def test_c4_full_size_gradient_properties():

@@ -224,20 +224,32 @@ def test_c4_dse_removes_forward_gradient_clears(T):
     # clears (+2 listgens each), P2G, GRID_OP (+2 listgens), G2P = 19; backward substep =
     # deactivate grid (+2), P2G, deactivate grad (+2), G2P_ADJ, P2G_ADJ = 10; +3 loss/seed
     assert s["tasks_lowered"] == 29 * T + 3
-    assert s["dead_removed"] == 4 * T                # one grad clear per field per substep
-    assert s["launches"] == 15 * T + 2
+    # dead per substep: the 4 forward grad clears, and 4 listgens that only fed
+    # DEACTIVATEs -- a whole-tree DEACTIVATE on these small trees is a pool reset
+    # with no list input (reading R33)
+    assert s["dead_removed"] == 8 * T
+    assert s["launches"] == 11 * T + 2
     rf_groups = {int(r[0]) for r in plans[0] if sg.TASK_TYPES[r[1]] == "range_for"}
     # P2G, G2P per forward substep; P2G, G2P_ADJ, P2G_ADJ per backward substep;
     # LOSS_MEAN; ADJ_INIT is fused into an independent range-for (same range)
     assert len(rf_groups) == 5 * T + 1
     assert sum(sg.TASK_TYPES[r[1]] == "range_for" for r in plans[0]) == 5 * T + 2
     st_dse, _ = plan_counts(prog, passes="dse")
-    assert st_dse[0]["dead_removed"] == 12 * T        # clears plus their listgens
+    assert st_dse[0]["dead_removed"] == 18 * T        # clears plus their listgens, reset inputs
     # an unobserved loss (observed = no fields) is dead as well
     L = prog["layout"]
     prog2 = W.c4_program(n_grid=16, n_particles=100, T=T, observed=[])
     st2, _ = plan_counts(prog2)
-    assert st2[0]["dead_removed"] == 4 * T + 2
+    assert st2[0]["dead_removed"] == 8 * T + 2
+
+
+def test_deactivate_reset_rule():
+    # R33: whole-tree DEACTIVATE of a small tree runs as a pool reset (no lists);
+    # a deeper level, or a tree whose dense volume exceeds 64 MiB, keeps the list-based kernel
+    st, plans = plan_counts(W.c3_program(n_grid=32, n_particles=100, steps=1))
+    assert types_of(plans[0]) == ["deactivate", "range_for", "listgen", "listgen", "struct_for", "range_for"]
+    st5, plans5 = plan_counts(W.c5_program(n_grid=512, n_particles=100, steps=1))
+    assert types_of(plans5[0])[:3] == ["listgen", "listgen", "deactivate"]
 
 
 @pytest.mark.parametrize("passes", [0, 1, 4, 8, 15, 31])
