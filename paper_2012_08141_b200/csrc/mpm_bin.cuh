@@ -64,6 +64,31 @@ __global__ void __launch_bounds__(BIN_TPB) k_bin_count(const __grid_constant__ B
   }
 }
 
+// Small key spaces (C4: 4K blocks): per-CTA shared-memory histogram over a
+// contiguous particle range, then one global atomic per (CTA, non-empty key);
+// the global atomics on a few hundred hot keys were the count kernel's cost.
+constexpr int BIN_SMEM_KEYS = 8192;
+__global__ void __launch_bounds__(BIN_TPB) k_bin_count_smem(const __grid_constant__ BinArgs A) {
+  __shared__ uint32_t sh[BIN_SMEM_KEYS];
+  const int64_t n = A.dcount ? (int64_t)*A.dcount : A.n;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+  for (uint32_t k = threadIdx.x; k < A.B.nkeys; k += BIN_TPB) sh[k] = 0u;
+  __syncthreads();
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += BIN_TPB) {
+    const uint32_t k = bin_key_of(A.B, A.x, A.xs, i, A.inv_dx);
+    A.B.key[i] = k;
+    A.B.rank[i] = atomicAdd(&sh[k], 1u);
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < A.B.nkeys; k += BIN_TPB) {
+    const uint32_t c = sh[k];
+    sh[k] = c ? atomicAdd(&A.B.hist[k], c) : 0u;
+  }
+  __syncthreads();
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += BIN_TPB) A.B.rank[i] += sh[A.B.key[i]];
+}
+
 __device__ __forceinline__ void block_sum2(uint32_t& a, uint32_t& b) {
   __shared__ uint32_t s[2][BIN_TPB / 32];
 #pragma unroll

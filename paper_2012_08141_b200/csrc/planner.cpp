@@ -685,10 +685,11 @@ static bool pass_fusion(const HLayout& L, std::vector<PTask>& seq, PlanStats& st
         } else if (A.type == TT_RANGE_FOR) {
           // same range: equal host extent, or the same device-counted array
           if (A.n != B.n || (A.n < 0 && A.t.arrays[0] != B.t.arrays[0])) continue;
-          // ops with their own kernels (scan / append / unpack) run alone
+          // ops with their own kernels (scan / append / unpack, the binned MPM transfers) run alone
           auto solo = [](int op) {
             return op == SG_OP_G2P_MIGRATE || op == SG_OP_MIGRATE_APPEND || op == SG_OP_HALO_UNPACK ||
-                   op == SG_OP_LOSS_MEAN || op == SG_OP_G2P_ADJ || op == SG_OP_P2G_ADJ;
+                   op == SG_OP_LOSS_MEAN || op == SG_OP_G2P_ADJ || op == SG_OP_P2G_ADJ || op == SG_OP_P2G ||
+                   op == SG_OP_G2P;
           };
           if (solo(A.t.op) || solo(B.t.op)) continue;
         }
