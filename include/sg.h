@@ -149,6 +149,13 @@ enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
  *                           state s; a4 adjoint x_s (+=), a5 adjoint v_s (=), a6
  *                           adjoint C_s (=), a7 adjoint J_s (+=); p0 dt, p1 inv_dx,
  *                           p2 p_mass, p3 p_vol, p4 E
+ * Multigrid (SURVEY N1; PAPER.md:348-361 restriction, :438-441 MGPCG), A = -Laplacian, h = 1:
+ *   SMOOTH_RB    struct-for red-black Gauss-Seidel half sweep: cells with (sum c) % 2 == p0
+ *                           get f0[c] = (f1[c] + sum_nbr f0) / (2D); f0 neighbour access
+ *   RESTRICT     struct-for f0[c//2] += p0 * (f1[c] - A f2[c])   f0 on the half-resolution
+ *                           tree (activating, demotable like DOWNSAMPLE); f2 neighbour access
+ *   PROLONG      struct-for f0[c] += f1[c//2]                    f1 on the half-resolution tree
+ *   RESID_NORM2  struct-for f0[] += (f1[c] - A f2[c])^2          f0 0-D (reduction)
  * Inactive or out-of-bound reads give 0. */
 enum {
   SG_OP_FILL = 1, SG_OP_ADD_CONST = 2, SG_OP_INC = 3, SG_OP_AXPY = 4, SG_OP_STENCIL = 5,
@@ -156,7 +163,8 @@ enum {
   SG_OP_CLEAR_SCALAR = 10, SG_OP_ARRAY_COUNT = 11,
   SG_OP_P2G = 20, SG_OP_GRID_OP = 21, SG_OP_G2P = 22,
   SG_OP_HALO_PACK = 23, SG_OP_HALO_UNPACK = 24, SG_OP_G2P_MIGRATE = 25, SG_OP_MIGRATE_APPEND = 26,
-  SG_OP_LOSS_MEAN = 27, SG_OP_ADJ_INIT = 28, SG_OP_G2P_ADJ = 29, SG_OP_P2G_ADJ = 30
+  SG_OP_LOSS_MEAN = 27, SG_OP_ADJ_INIT = 28, SG_OP_G2P_ADJ = 29, SG_OP_P2G_ADJ = 30,
+  SG_OP_SMOOTH_RB = 31, SG_OP_RESTRICT = 32, SG_OP_PROLONG = 33, SG_OP_RESID_NORM2 = 34
 };
 
 typedef struct {

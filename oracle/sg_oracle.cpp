@@ -59,7 +59,8 @@ enum {
   OP_JACOBI = 6, OP_REDUCE_SUM = 7, OP_DOWNSAMPLE = 8, OP_JITTER = 9,
   OP_CLEAR_SCALAR = 10,
   OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22,
-  OP_LOSS_MEAN = 27, OP_ADJ_INIT = 28, OP_G2P_ADJ = 29, OP_P2G_ADJ = 30
+  OP_LOSS_MEAN = 27, OP_ADJ_INIT = 28, OP_G2P_ADJ = 29, OP_P2G_ADJ = 30,
+  OP_SMOOTH_RB = 31, OP_RESTRICT = 32, OP_PROLONG = 33, OP_RESID_NORM2 = 34
 };
 
 typedef std::array<int64_t, 3> Coord;
@@ -505,6 +506,64 @@ int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const 
         Coord h{c[0] / 2, c[1] / 2, c[2] / 2};
         double x = (nf > 1 && f[1] >= 0) ? read(g, f[1], c) : 0.0;
         if (!rc) rc = atomic_add(g, f[0], h, P(0) * x + P(1), act_bit(activating, 0));
+      });
+      break;
+    // --- multigrid (PAPER.md:348-361 restriction, PAPER.md:438-441 MGPCG
+    // after hu2019taichi: red-black smoothing, residual restriction, prolongation).
+    // A = -Laplacian with h = 1 on the level's grid; inactive / out-of-bound reads 0.
+    case OP_SMOOTH_RB:
+      // red-black Gauss-Seidel half sweep: cells with (sum c) % 2 == p0 get
+      // z = (r + sum_nbr z) / (2D); the other colour is only read
+      if (!need(2)) return fail(g, E_ARG, "SMOOTH_RB needs 2 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        const long par = ((long)c[0] + c[1] + c[2]) & 1;
+        if (par != (long)P(0)) return;
+        double s = read(g, f[1], c), m = read_mag(g, f[1], c);
+        for (int a = 0; a < D; a++) {
+          s += read(g, f[0], shift(c, a, +1)) + read(g, f[0], shift(c, a, -1));
+          m += read_mag(g, f[0], shift(c, a, +1)) + read_mag(g, f[0], shift(c, a, -1));
+        }
+        if (!rc) rc = write(g, f[0], c, s / (2.0 * D), act_bit(activating, 0), m / (2.0 * D));
+      });
+      break;
+    case OP_RESTRICT:
+      // coarse r[c // 2] += p0 * (r[c] - A z[c])   (fields: f0 coarse target, f1 r, f2 z)
+      if (!need(3)) return fail(g, E_ARG, "RESTRICT needs 3 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        double az = 2.0 * D * read(g, f[2], c), m = 2.0 * D * read_mag(g, f[2], c);
+        for (int a = 0; a < D; a++) {
+          az -= read(g, f[2], shift(c, a, +1)) + read(g, f[2], shift(c, a, -1));
+          m += read_mag(g, f[2], shift(c, a, +1)) + read_mag(g, f[2], shift(c, a, -1));
+        }
+        const double res = read(g, f[1], c) - az;
+        m += read_mag(g, f[1], c);
+        Coord h{c[0] / 2, c[1] / 2, c[2] / 2};
+        if (!rc) rc = atomic_add_m(g, f[0], h, P(0) * res, std::fabs(P(0)) * m, act_bit(activating, 0));
+      });
+      break;
+    case OP_PROLONG:
+      // fine z[c] += coarse z[c // 2]   (fields: f0 fine target, f1 coarse source)
+      if (!need(2)) return fail(g, E_ARG, "PROLONG needs 2 fields");
+      for_struct(g, t, [&](const Coord& c) {
+        Coord h{c[0] / 2, c[1] / 2, c[2] / 2};
+        const double v = read(g, f[0], c) + read(g, f[1], h);
+        const double m = read_mag(g, f[0], c) + read_mag(g, f[1], h);
+        if (!rc) rc = write(g, f[0], c, v, act_bit(activating, 0), m);
+      });
+      break;
+    case OP_RESID_NORM2:
+      // s[] += (r[c] - A z[c])^2   (fields: f0 0-D target, f1 r, f2 z)
+      if (!need(3)) return fail(g, E_ARG, "RESID_NORM2 needs 3 fields");
+      if (g->trees[g->fields[f[0]].tree].nd != 0) return fail(g, E_ARG, "RESID_NORM2 target must be 0-D");
+      for_struct(g, t, [&](const Coord& c) {
+        double az = 2.0 * D * read(g, f[2], c), m = 2.0 * D * read_mag(g, f[2], c);
+        for (int a = 0; a < D; a++) {
+          az -= read(g, f[2], shift(c, a, +1)) + read(g, f[2], shift(c, a, -1));
+          m += read_mag(g, f[2], shift(c, a, +1)) + read_mag(g, f[2], shift(c, a, -1));
+        }
+        const double res = read(g, f[1], c) - az;
+        m += read_mag(g, f[1], c);
+        if (!rc) rc = atomic_add_m(g, f[0], Coord{0, 0, 0}, res * res, 2.0 * std::fabs(res) * m, false);
       });
       break;
     case OP_JITTER:

@@ -816,13 +816,15 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   a->table = drive ? drive->table : nullptr;
   a->table_ctl = drive ? drive->ctl : nullptr;
   a->has_reduce = 0;
-  for (int o = 0; o < nops; o++) a->has_reduce |= ops[o].op == SG_OP_REDUCE_SUM;
+  for (int o = 0; o < nops; o++) a->has_reduce |= ops[o].op == SG_OP_REDUCE_SUM || ops[o].op == SG_OP_RESID_NORM2;
   a->need_nbr = 0;
   bool i32 = false;
   for (int o = 0; o < nops; o++) {
     a->ops[o] = ops[o];
     int op = ops[o].op;
-    if (op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER) a->need_nbr = 1;
+    if (op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER || op == SG_OP_SMOOTH_RB ||
+        op == SG_OP_RESTRICT || op == SG_OP_RESID_NORM2)
+      a->need_nbr = 1;
     a->aux[o] = 0;
   }
   if (chain_needs_nbr) a->need_nbr = 1;

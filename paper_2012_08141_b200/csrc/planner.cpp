@@ -104,6 +104,10 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
       }
       break;
     case SG_OP_LOSS_MEAN: A(0, R_READ, AC_ID); F(0, R_RW, AC_CONST); break;
+    case SG_OP_SMOOTH_RB: F(1, R_READ, AC_ID); F(0, R_RW, AC_NBR); break;
+    case SG_OP_RESTRICT: F(1, R_READ, AC_ID); F(2, R_READ, AC_NBR); F(0, R_RW, AC_DIV2); break;
+    case SG_OP_PROLONG: F(1, R_READ, AC_DIV2); F(0, R_RW, AC_ID); break;
+    case SG_OP_RESID_NORM2: F(1, R_READ, AC_ID); F(2, R_READ, AC_NBR); F(0, R_RW, AC_CONST); break;
     case SG_OP_ADJ_INIT:
       for (int i = 0; i < 4; i++) A(i, R_WRITE, AC_ID, true);
       break;
@@ -156,6 +160,8 @@ static int op_min_fields(int op) {
     case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: case SG_OP_G2P_MIGRATE: return 4;
     case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: return 0;
     case SG_OP_LOSS_MEAN: return 1;
+    case SG_OP_SMOOTH_RB: case SG_OP_PROLONG: return 2;
+    case SG_OP_RESTRICT: case SG_OP_RESID_NORM2: return 3;
     case SG_OP_G2P_ADJ: return 8;
     case SG_OP_P2G_ADJ: return 4;
     case SG_OP_HALO_PACK: case SG_OP_HALO_UNPACK: return 1;
@@ -797,7 +803,8 @@ static void pass_chain(const HLayout& L, std::vector<PTask>& seq, const std::vec
     }
   };
   auto group_reduces = [&](const PTask& t) {
-    for (int m : t.members) if (eager[m].t.op == SG_OP_REDUCE_SUM) return true;
+    for (int m : t.members)
+      if (eager[m].t.op == SG_OP_REDUCE_SUM || eager[m].t.op == SG_OP_RESID_NORM2) return true;
     return false;
   };
   for (int i = 0; i < n; i++) {

@@ -658,7 +658,8 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
         for (int i = 0; i < nops; i++) {
           make_op(g, g->eager[members[i]], acts[i], t0.tree, all[i]);
           int op = all[i].op;
-          nbr |= op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER;
+          nbr |= op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER || op == SG_OP_SMOOTH_RB ||
+                 op == SG_OP_RESTRICT || op == SG_OP_RESID_NORM2;
         }
         const size_t bytes = nops * sizeof(DOp) + phase_end.size() * sizeof(int) + 64;
         if (bytes > g->chain_bytes) {

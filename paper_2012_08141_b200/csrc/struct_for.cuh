@@ -113,7 +113,7 @@ __device__ void finish_reductions(const SFArgs& A, const DOp* ops, int nops) {
   if (!s_last) return;
   __threadfence();
   for (int o = 0; o < nops; o++) {
-    if (ops[o].op != SG_OP_REDUCE_SUM) continue;
+    if (ops[o].op != SG_OP_REDUCE_SUM && ops[o].op != SG_OP_RESID_NORM2) continue;
     double t = 0.0;   // fixed-order tree sum over CTAs
     for (int b = threadIdx.x; b < G; b += SF_TPB) t += *(volatile double*)&A.C.partials[o * A.C.max_grid + b];
     s_sum[threadIdx.x] = t;
@@ -197,6 +197,25 @@ __device__ __noinline__ void apply_downsample(const SFArgs& A, const DOp& op, co
   atomic_add_v(cont + T2.payload_off + ((uint64_t)tf.slot << T2.ln_leaf) + idx, val);
 }
 
+// Value of field f (another tree, e.g. the coarse level) at cell h; 0 when inactive.
+template <typename V>
+__device__ __noinline__ V read_other(const SFArgs& A, int f, const int h[3]) {
+  const DField& tf = A.C.fields[f];
+  const DTree& T2 = A.C.trees[tf.tree];
+  if (!in_domain(T2, h)) return V(0);
+  uint32_t idx;
+  uint32_t* cont = locate(T2, h, idx);
+  if (!cont) return V(0);
+  return ldv<V>(cont + T2.payload_off + ((uint64_t)tf.slot << T2.ln_leaf) + idx);
+}
+
+// r - A z at the cell (A = -Laplacian, h = 1)
+template <typename V>
+__device__ __forceinline__ V residual_at(const CellCtx& x, int slot_r, int slot_z) {
+  const int D = x.T->nd;
+  return ld_id<V>(x, slot_r) - ((V)(2 * D) * ld_id<V>(x, slot_z) - nbr_sum<V>(x, slot_z));
+}
+
 // One op on one cell (GENERIC path, and the per-lane ops of the QUAD path).
 // Returns the REDUCE contribution.
 template <typename V>
@@ -222,6 +241,21 @@ __device__ __forceinline__ V apply_cell(const SFArgs& A, const DOp& op, const Ce
       if ((x.c[0] & 1) == 0) st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + ld_nbr<V>(x, op.slot[0], 0, +1));
       break;
     case SG_OP_GRID_OP: mpm_grid_op(op, x.c, cell_ptr(x, 0), x.fstride); break;
+    case SG_OP_SMOOTH_RB:
+      if (((x.c[0] + x.c[1] + x.c[2]) & 1) == (int)op.p[0])
+        st_id<V>(x, op.slot[0], (ld_id<V>(x, op.slot[1]) + nbr_sum<V>(x, op.slot[0])) / (V)(2 * D));
+      break;
+    case SG_OP_RESTRICT:
+      apply_downsample<V>(A, op, x.c, (V)op.p[0] * residual_at<V>(x, op.slot[1], op.slot[2]));
+      break;
+    case SG_OP_PROLONG: {
+      const int h[3] = {x.c[0] >> 1, x.c[1] >> 1, x.c[2] >> 1};
+      st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + read_other<V>(A, op.f[1], h));
+    } break;
+    case SG_OP_RESID_NORM2: {
+      const V r = residual_at<V>(x, op.slot[1], op.slot[2]);
+      return r * r;
+    }
     default: break;
   }
   return V(0);
@@ -490,7 +524,8 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int n
         }
       } break;
       default: {
-        // per-lane ops (DOWNSAMPLE, JITTER, GRID_OP)
+        // per-lane ops (DOWNSAMPLE, JITTER, GRID_OP, multigrid)
+        V acc = V(0);
         for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
           QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
           if (x.off == SG_NO_BLOCK) continue;
@@ -501,9 +536,10 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int n
 #pragma unroll
             for (int a = 0; a < 3; a++) c.c[a] = tile.org[x.e][a] + x.r[a];
             c.c[ND - 1] += k;
-            apply_cell<V>(A, op, c);
+            acc += apply_cell<V>(A, op, c);
           }
         }
+        if (op.op == SG_OP_RESID_NORM2) warp_add<V>(o, acc);
       } break;
     }
   }
@@ -555,7 +591,7 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const DOp* ops, int n
       x.c[2] = tile.org[x.e][2] + bc[2];
       acc += apply_cell<V>(A, op, x);
     }
-    if (op.op == SG_OP_REDUCE_SUM) warp_add<V>(o, acc);
+    if (op.op == SG_OP_REDUCE_SUM || op.op == SG_OP_RESID_NORM2) warp_add<V>(o, acc);
   }
 }
 

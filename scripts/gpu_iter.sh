@@ -8,7 +8,7 @@ python - <<PY
 import json
 d=json.load(open('gpurun_out/${TAG}_bench.json'))
 print('C2', d['value'], 'jac us', d['roofline']['avg_launch_us'], 'share', d['roofline']['share_of_step'], 'e2e', d['e2e']['value'])
-for k,v in d.get('extra',{}).items(): print(k, {kk: vv for kk, vv in v.items() if kk in ('steps_per_s','solves_per_s','launches_per_step','avg_launch_us','achieved_GBps','frac','error','avg_us_per_launch_kind','result_s','iterations_per_s','launches_per_iteration','ms_per_iteration','loss','dead_removed')})
+for k,v in d.get('extra',{}).items(): print(k, {kk: vv for kk, vv in v.items() if kk in ('steps_per_s','solves_per_s','launches_per_step','avg_launch_us','achieved_GBps','frac','error','vcycles_per_s','launches_per_solve','avg_us_per_launch_kind','result_s','iterations_per_s','launches_per_iteration','ms_per_iteration','loss','dead_removed')})
 PY
 [ -n "$SKIP_NCU" ] && exit 0
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python scripts/prof_c2.py 2 > /dev/null 2>&1; echo launches rc=$?

@@ -1,0 +1,75 @@
+"""GPU parity of the multigrid workload against the oracle (-m gpu).
+
+Masks of every level exact (the coarse levels are activated by RESTRICT's
+activate-on-write, demoted after the first cycle); z and r of every level and
+the residual norm within 1e-4 of the oracle's shadow magnitude M (several
+Gauss-Seidel sweeps and restrictions compound the f32 rounding, reading R29).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2012_08141_b200 import sg  # noqa: E402
+from test_gpu_parity import as_set  # noqa: E402
+
+
+def compare(g, o, prog, tol=1e-4):
+    L = prog["layout"]
+    for lv in prog["levels"]:
+        for s in lv:
+            if L.rows[s][0] in (W.BITMASKED, W.POINTER):
+                assert as_set(g.mask(s)) == as_set(o.mask(s)), f"mask {s}"
+    for name, fid in L.fields.items():
+        want, mag = o.field(fid, with_mag=True)
+        got = np.asarray(g.field(fid), dtype=np.float64)
+        bad = np.abs(got - want) > tol * np.maximum(np.abs(want), mag)
+        assert not bad.any(), f"{name}: {bad.sum()} off, worst {np.abs(got - want)[bad].max():.3e}"
+
+
+@pytest.mark.parametrize("passes", [0, "all"])
+def test_mg_small(passes):
+    prog = W.mg_program(n=64, levels=3, block=8, cycles=3, radius_frac=0.3)
+    o = oracle.run_program(prog)
+    g = sg.Grid(prog["desc"])
+    st = sg.replay(g, prog, passes=passes, device="cuda")
+    g.sync()
+    compare(g, o, prog)
+    if passes == "all":
+        assert st[0]["demotions"] == 2 * 2
+
+
+def test_mg_full_size_one_cycle_and_replay():
+    prog = W.mg_program(n=512, cycles=1)
+    o = oracle.run_program(prog)
+    g = sg.Grid(prog["desc"])
+    sg.replay(g, prog, device="cuda")
+    g.sync()
+    compare(g, o, prog)
+    # the same flush again (plan cache hit, CUDA-graph replay) gives the same z0
+    L = prog["layout"]
+    z_first = g.field(L.fields["z0"]).copy()
+    g2 = sg.Grid(prog["desc"])
+    for _ in range(3):
+        sg.replay(g2, prog, device="cuda")
+    g2.sync()
+    # each replay re-solves from z0 = 0 (FILL) and r0 = 1: the same result up to the
+    # order of RESTRICT's atomic adds
+    np.testing.assert_allclose(g2.field(L.fields["z0"]), z_first, rtol=1e-5, atol=1e-6 * np.abs(z_first).max())
+
+
+def test_mg_full_size_ten_cycles_converge():
+    res = []
+    for cycles in (2, 10):
+        prog = W.mg_program(n=512, cycles=cycles)
+        g = sg.Grid(prog["desc"])
+        sg.replay(g, prog, device="cuda")
+        g.sync()
+        res.append(float(np.asarray(g.field(prog["layout"].fields["res"])).reshape(-1)[0]))
+    assert np.isfinite(res).all() and res[1] < 0.5 * res[0]

@@ -243,6 +243,31 @@ def test_c4_dse_removes_forward_gradient_clears(T):
     assert st2[0]["dead_removed"] == 8 * T + 2
 
 
+def test_mg_demotion_and_listgen_removal():
+    # SURVEY N1, PAPER.md:438-441 (MGPCG: restriction/smoothing/prolongation listgens
+    # 351,440 -> 343) and PAPER.md:346-361 (demotion of the [i//2] restriction).
+    prog = W.mg_program(n=512, cycles=10)
+    st, _ = plan_counts(prog)
+    s = st[0]
+    assert s["demotions"] == 3 * 9            # RESTRICT into the 3 coarse levels, cycles 2..10
+    assert s["listgen_launched"] == 7         # 4 levels' lists once, coarse ones after cycle 1
+    assert s["tasks_fused"] == 31             # the two coarse clears per level, FILL r0 + FILL z0
+    st0, _ = plan_counts(prog, passes=0)
+    assert st0[0]["launches"] == s["tasks_lowered"] == 1048
+    nodem, _ = plan_counts(prog, passes=15 & ~2)
+    assert nodem[0]["demotions"] == 0 and nodem[0]["listgen_launched"] == 34
+    assert nodem[0]["launches"] > s["launches"]
+
+
+@pytest.mark.parametrize("passes", [0, 1, 3, 15])
+def test_mg_schedule_soundness_on_oracle(passes):
+    prog = W.mg_program(n=64, levels=3, block=8, cycles=2, radius_frac=0.3)
+    ref = oracle.run_program(prog)
+    o = replay_plan_on_oracle(prog, passes)
+    for name, fid in prog["layout"].fields.items():
+        assert np.array_equal(o.field(fid), ref.field(fid)), (passes, name)
+
+
 def test_deactivate_reset_rule():
     # R33: whole-tree DEACTIVATE of a small tree runs as a pool reset (no lists);
     # a deeper level, or a tree whose dense volume exceeds 64 MiB, keeps the list-based kernel

@@ -382,6 +382,93 @@ def c4_program(n_grid=64, n_particles=100_000, T=64, seed=0, passes="all", comp=
 
 
 # ----------------------------------------------------------------------------
+# MG: multigrid V-cycle Poisson solver in the style of the paper's
+# MGPCG benchmark (512^2 domain, sparsely populated region,
+# four levels, each a two-level sparse grid; hu2019taichi's MGPCG): red-black
+# Gauss-Seidel smoothing, residual restriction with activate-on-write on the
+# coarse level (demoted after the first cycle), prolongation.
+# ----------------------------------------------------------------------------
+def mg_layout(n=512, levels=4, block=16):
+    L = Layout()
+    lv = []
+    for l in range(levels):
+        nl = n >> l
+        b = min(block, nl)
+        ids = L.chain([("pointer", (nl // b,) * 2), ("dense", (b,) * 2)],
+                      [(f"z{l}", "f32"), (f"r{l}", "f32")])
+        lv.append(ids)
+    L.scalar("res")
+    return L, lv
+
+
+def mg_region(n=512, block=16, radius_frac=0.3125, center=(0.5, 0.5)):
+    """Block origins (pointer-cell coords) of the finest level's active region:
+    blocks whose nearest point lies inside a disk of radius radius_frac * n."""
+    nb = n // block
+    cx, cy = center[0] * n, center[1] * n
+    R = radius_frac * n
+    out = []
+    for i in range(nb):
+        for j in range(nb):
+            x0, y0 = i * block, j * block
+            dx = max(x0 - cx, 0.0, cx - (x0 + block))
+            dy = max(y0 - cy, 0.0, cy - (y0 + block))
+            if dx * dx + dy * dy < R * R:
+                out.append((x0, y0))
+    return np.asarray(out, dtype=np.int32)
+
+
+def mg_vcycle_calls(L, lv, levels=4, nu=2, bottom=8, weight=1.0):
+    f = L.fields
+    z = [f[f"z{l}"] for l in range(levels)]
+    r = [f[f"r{l}"] for l in range(levels)]
+    leaf = [ids[-1] for ids in lv]
+    calls = []
+
+    def smooth(l, order=(0, 1)):
+        return [struct_for("SMOOTH_RB", leaf[l], [z[l], r[l]], [p]) for p in order]
+
+    for l in range(levels - 1):
+        for _ in range(nu):
+            calls += smooth(l)
+        calls += [clear_values(r[l + 1]), clear_values(z[l + 1])]
+        calls.append(struct_for("RESTRICT", leaf[l], [r[l + 1], r[l], z[l]], [weight], [True]))
+    for _ in range(bottom):
+        calls += smooth(levels - 1)
+    for l in reversed(range(levels - 1)):
+        calls.append(struct_for("PROLONG", leaf[l], [z[l], z[l + 1]]))
+        for _ in range(nu):
+            calls += smooth(l, (1, 0))
+    return calls
+
+
+def mg_solve_calls(L, lv, coords, cycles=10, levels=4, nu=2, bottom=8, dim=2, with_residual=True):
+    """Activate the finest level, r0 = 1 (the right-hand side), z0 = 0, then
+    `cycles` V-cycles; finally res = ||r0 - A z0||^2.  Restriction weight
+    4 / 2^dim (= 1 in 2-D): the h^2 scaling of the coarse operator times the
+    average over the 2^dim children."""
+    f = L.fields
+    calls = [activate(f["z0"], coords), struct_for("FILL", lv[0][-1], [f["r0"]], [1.0]),
+             struct_for("FILL", lv[0][-1], [f["z0"]], [0.0])]
+    for _ in range(cycles):
+        calls += mg_vcycle_calls(L, lv, levels, nu, bottom, weight=2.0 / (1 << dim))
+    if with_residual:
+        calls += [serial("CLEAR_SCALAR", [f["res"]]),
+                  struct_for("RESID_NORM2", lv[0][-1], [f["res"], f["r0"], f["z0"]])]
+    return calls
+
+
+def mg_program(n=512, levels=4, block=16, cycles=10, nu=2, bottom=8, radius_frac=0.3125, passes="all"):
+    L, lv = mg_layout(n, levels, block)
+    coords = mg_region(n, block, radius_frac)
+    calls = mg_solve_calls(L, lv, coords, cycles, levels, nu, bottom)
+    calls.append(flush(passes))
+    prog = program(L, calls, name="MG")
+    prog["levels"] = lv
+    return prog
+
+
+# ----------------------------------------------------------------------------
 # C5: large sparse MPM, 512^3 bound, x-slab sharded.
 # pointer(P^3) [n/P cells each] -> bitmasked((n/P/4)^3) -> dense(4^3).
 # ----------------------------------------------------------------------------
