@@ -906,11 +906,9 @@ int launch_bin(const DBins& b, const float* x, int64_t xs, int64_t n, const int3
   a.ntiles = bin_ntiles(b.nkeys);
   const int gp = (int)std::max<int64_t>(1, std::min<int64_t>((n + BIN_TPB - 1) / BIN_TPB, (int64_t)num_sms() * 8));
   const int gt = (int)std::min<uint32_t>(a.ntiles, (uint32_t)num_sms() * 4);
-  if (b.nkeys <= (uint32_t)BIN_SMEM_KEYS)
-    k_bin_count_smem<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, (int64_t)num_sms() * 2)),
-                       BIN_TPB, 0, s>>>(a);
-  else
-    k_bin_count<<<gp, BIN_TPB, 0, s>>>(a);
+  // (a shared-memory histogram variant, k_bin_count_smem, measured slower on C4:
+  // 14.4 vs 10.0 us -- profiles/r01_launches_c4_t31.csv)
+  k_bin_count<<<gp, BIN_TPB, 0, s>>>(a);
   k_bin_tiles<<<gt, BIN_TPB, 0, s>>>(a);
   k_bin_top<<<1, 1024, 0, s>>>(a);
   k_bin_apply<<<gt, BIN_TPB, 0, s>>>(a);
