@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(MG_TPB) k_g2p_migrate(const __grid_constant__ 
   float* jj = (float*)Jj.ptr;
   uint32_t* id = (uint32_t*)Id.ptr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_epoch = *(volatile uint32_t*)&A.ctl[2] & 0x3FFFFFFFu;
+  if (threadIdx.x == 0) s_epoch = A.ctl[2] & 0x3FFFFFFFu;   // bumped by an earlier launch
   const uint32_t n = *X.dcount;
   const uint32_t ntiles = (n + MG_TPB - 1) / MG_TPB;
   const float dt = op.p[0], inv_dx = op.p[1], lo = op.p[2], hi = op.p[3];
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(MG_TPB) k_g2p_migrate(const __grid_constant__ 
         uint32_t fl = 2u;
         if (q >= 0) {
           do {
-            s = *(volatile uint64_t*)&st[q];
+            s = ld_volatile64(&st[q]);
             fl = ((uint32_t)(s >> 34) == epoch) ? (uint32_t)(s >> 32) & 3u : 0u;
           } while (fl == 0u);
         }

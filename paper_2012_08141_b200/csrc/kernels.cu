@@ -33,8 +33,21 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) { return *(volatile const uint32_t*)p; }
-__device__ __forceinline__ uint64_t ld_volatile64(const uint64_t* p) { return *(volatile const uint64_t*)p; }
+// Loads of words other CTAs of the SAME launch may be writing (look-back
+// descriptors, mask words under activation): device-scope relaxed, so L2 is
+// the coherence point (a C++ volatile load compiles to a system-scope strong
+// load).  Words written by EARLIER launches (list counts, table flags, pool
+// counters) are read with plain loads: the kernel boundary orders them.
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_volatile64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void set_err(const DevCtx& C, int code, int task) {
   if (atomicCAS(&C.err[0], 0u, (uint32_t)code) == 0u) C.err[1] = (uint32_t)task;
@@ -339,7 +352,7 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
   const bool solo = gridDim.x == 1;
   uint32_t solo_tile = 0;
   if (threadIdx.x == 0) { s_epoch = solo ? 0u : ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu; s_run = 0u; }
-  uint32_t nparent = a.mode == 0 ? 1u : ld_volatile(a.pcount);
+  uint32_t nparent = a.mode == 0 ? 1u : *a.pcount;
   uint64_t nchunks = (uint64_t)nparent << a.lcpp;
   uint32_t ntiles = (uint32_t)((nchunks + LG_TILE - 1) / LG_TILE);
   const uint32_t lnS = a.T.lev[a.ls].ln;
@@ -598,7 +611,7 @@ struct DeArgs {
 
 __global__ void __launch_bounds__(256) k_deactivate(const __grid_constant__ DeArgs A) {
   const DTree& T = A.T;
-  const uint32_t nblk = A.drive_entries ? ld_volatile(A.drive_count) : 1u;
+  const uint32_t nblk = A.drive_entries ? *A.drive_count : 1u;
   const uint32_t blk = 1u << T.lblk;
   const uint64_t fstride = 1ull << T.ln_leaf;
   // phase 1: zero the payload (and leaf bits) of every active block
@@ -621,7 +634,7 @@ __global__ void __launch_bounds__(256) k_deactivate(const __grid_constant__ DeAr
   for (int l = A.ls; l < T.nlev; l++) {
     if (!A.lent[l]) continue;
     const DLevel& L = T.lev[l];
-    uint32_t n = ld_volatile(A.lcnt[l]);
+    uint32_t n = *A.lcnt[l];
     for (uint64_t i = gtid; i < n; i += gsz) {
       uint32_t e = A.lent[l][i];
       uint32_t cs = e >> L.ln, idx = e & ((1u << L.ln) - 1u);
@@ -1022,7 +1035,7 @@ __global__ void __launch_bounds__(256) k_deactivate_reset(const __grid_constant_
     const DSeg& S = T.seg[s];
     uint64_t n = 1;
     if (s > 0) {
-      const int32_t b = *(volatile const int32_t*)&S.alloc[0];
+      const int32_t b = S.alloc[0];
       n = (uint64_t)min((uint32_t)max(b, 0), S.capacity);
     }
     const uint64_t words = n * S.stride;   // containers are 128-byte aligned: stride % 4 == 0

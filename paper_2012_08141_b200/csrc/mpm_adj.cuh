@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(LM_TPB) k_loss_mean(const __grid_constant__ Lo
   if (!s_last) return;
   __threadfence();
   double u = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += LM_TPB) u += *(volatile double*)&A.C.partials[b];
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += LM_TPB) u += __ldcg(&A.C.partials[b]);
   s[threadIdx.x] = u;
   __syncthreads();
   for (int w = LM_TPB / 2; w > 0; w >>= 1) {

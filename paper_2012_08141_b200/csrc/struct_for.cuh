@@ -115,7 +115,7 @@ __device__ void finish_reductions(const SFArgs& A, const DOp* ops, int nops) {
   for (int o = 0; o < nops; o++) {
     if (ops[o].op != SG_OP_REDUCE_SUM && ops[o].op != SG_OP_RESID_NORM2) continue;
     double t = 0.0;   // fixed-order tree sum over CTAs
-    for (int b = threadIdx.x; b < G; b += SF_TPB) t += *(volatile double*)&A.C.partials[o * A.C.max_grid + b];
+    for (int b = threadIdx.x; b < G; b += SF_TPB) t += __ldcg(&A.C.partials[o * A.C.max_grid + b]);
     s_sum[threadIdx.x] = t;
     __syncthreads();
     for (int w = SF_TPB / 2; w > 0; w >>= 1) {
@@ -730,7 +730,7 @@ template <typename V, int ND, bool PAIR, int GL>
 __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __grid_constant__ SFArgs A) {
   __shared__ SFTile tile;
   if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
-  const bool rows_ok = A.table && *(volatile uint32_t*)&A.table_ctl[4] != 0u;
+  const bool rows_ok = A.table && A.table_ctl[4] != 0u;   // set by an earlier launch
   sf_tiles<V, ND, PAIR, GL>(A, A.ops, A.nops, tile, rows_ok);
   if (A.has_reduce) finish_reductions<V>(A, A.ops, A.nops);
   sf_mark_table(A, rows_ok);
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5)
   __shared__ DOp s_ops[SG_MAXOPS];
   cg::grid_group grid = cg::this_grid();
   if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
-  const bool rows_ok0 = A.table && *(volatile uint32_t*)&A.table_ctl[4] != 0u;
+  const bool rows_ok0 = A.table && A.table_ctl[4] != 0u;
   int begin = 0;
   int last_n = 0;
   for (int p = 0; p < nphases; p++) {
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacA
   const uint32_t* __restrict__ rhs = P + A.s_rhs;
   uint32_t* dst = const_cast<uint32_t*>(P) + A.s_dst;
   const uint32_t nent = *A.count;
-  const bool rows_ok = *(volatile const uint32_t*)&A.table_ctl[4] != 0u;
+  const bool rows_ok = A.table_ctl[4] != 0u;   // set by an earlier launch
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), GW = gridDim.x * (blockDim.x >> 5);
   // one warp per half block; a lane owns the quads at x0 = 4*part + 2*(lane/16)
