@@ -632,7 +632,8 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       const int lratio = pk >= 0 && T.lev[pk].seg == T.lev[k].seg ? T.lev[k].ln - T.lev[pk].ln : T.lev[k].ln;
       const uint64_t pcap = parent ? parent->capacity : 1;
       const uint64_t ptiles = (pcap * (1ull << std::max(0, lratio - 5)) + 1023) / 1024;
-      int hint = (int)std::max<uint64_t>(1, std::min<uint64_t>(ptiles, (uint64_t)g->num_sms * 4));
+      // (the launcher clamps the grid; an uncapped hint lets it pick the two-pass scheme for big lists)
+      int hint = (int)std::max<uint64_t>(1, std::min<uint64_t>(ptiles, 0x7fffffffull));
       rc = launch_listgen(g->ctx, T, t0.tree, k, pk, parent, g->lists[t0.tree][k], task, g->stream, hint);
       st.listgen_launched++;
     } break;
