@@ -430,6 +430,30 @@ def measure_mg(steps=10, warmup=3, cycles=10):
             "active_cells_finest": int(len(calls[0]["coords"]) * 256)}
 
 
+def measure_mgpcg(steps=5, warmup=3, iters=10):
+    """N1 in the paper's form: MGPCG (CG preconditioned by one V-cycle),
+    512^2, 4 levels, 10 CG iterations per solve."""
+    import torch
+    from paper_2012_08141_b200 import sg
+    prog = W.mgpcg_program(n=512, iters=iters)
+    g = sg.Grid(prog["desc"])
+    L = prog["layout"]
+    calls = [c for c in prog["calls"] if c["call"] != "flush"]
+    coords = torch.as_tensor(calls[0]["coords"]).cuda()
+
+    def enqueue():
+        g.activate(calls[0]["field"], coords)
+        _enqueue_calls(g, sg, calls[1:])
+
+    ms, st = _timed_flushes(g, enqueue, steps, warmup)
+    rtr = float(np.asarray(g.field(L.fields["rTr"])).reshape(-1)[0])
+    return {"solves_per_s": 1000.0 / ms, "ms_per_solve": ms, "cg_iterations": iters,
+            "launches_per_solve": st["launches"], "tasks_lowered": st["tasks_lowered"],
+            "listgens_launched": st["listgen_launched"], "listgens_removed": st["listgens_removed"],
+            "demotions": st["demotions"], "tasks_fused": st["tasks_fused"], "dead_removed": st["dead_removed"],
+            "final_rTr": rtr}
+
+
 def run_c5(args, rank, world, local):
     """C5: 512^3 sparse MPM, 16M particles in an x-spanning bar, sharded in x
     slabs over the ranks (strong scaling); NCCL P2P halo / migration."""
@@ -562,7 +586,7 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "scripts"))
             import xl_bench
             extra = {}
-            for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3), ("c4", measure_c4), ("mg", measure_mg),
+            for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3), ("c4", measure_c4), ("mg", measure_mg), ("mgpcg", measure_mgpcg),
                              ("jac_xl", xl_bench.jac_xl), ("lg_xl", xl_bench.lg_xl)):
                 try:
                     extra[name] = fn()

@@ -156,6 +156,12 @@ enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
  *                           tree (activating, demotable like DOWNSAMPLE); f2 neighbour access
  *   PROLONG      struct-for f0[c] += f1[c//2]                    f1 on the half-resolution tree
  *   RESID_NORM2  struct-for f0[] += (f1[c] - A f2[c])^2          f0 0-D (reduction)
+ * Conjugate gradients around the V-cycle (MGPCG); scalars are 0-D
+ * fields read on the device, so no host round trip:
+ *   DOT          struct-for f0[] += p0 * f1[c] * f2[c]            f0 0-D (reduction)
+ *   AXPY_RATIO   struct-for f0[c] += p0 * (f2[] / f3[]) * f1[c]  f2, f3 0-D
+ *   XPAY_RATIO   struct-for f0[c] = f1[c] + (f2[] / f3[]) * f0[c]
+ *   COPY_SCALAR  serial     f0[] = f1[]                            both 0-D
  * Inactive or out-of-bound reads give 0. */
 enum {
   SG_OP_FILL = 1, SG_OP_ADD_CONST = 2, SG_OP_INC = 3, SG_OP_AXPY = 4, SG_OP_STENCIL = 5,
@@ -164,7 +170,8 @@ enum {
   SG_OP_P2G = 20, SG_OP_GRID_OP = 21, SG_OP_G2P = 22,
   SG_OP_HALO_PACK = 23, SG_OP_HALO_UNPACK = 24, SG_OP_G2P_MIGRATE = 25, SG_OP_MIGRATE_APPEND = 26,
   SG_OP_LOSS_MEAN = 27, SG_OP_ADJ_INIT = 28, SG_OP_G2P_ADJ = 29, SG_OP_P2G_ADJ = 30,
-  SG_OP_SMOOTH_RB = 31, SG_OP_RESTRICT = 32, SG_OP_PROLONG = 33, SG_OP_RESID_NORM2 = 34
+  SG_OP_SMOOTH_RB = 31, SG_OP_RESTRICT = 32, SG_OP_PROLONG = 33, SG_OP_RESID_NORM2 = 34,
+  SG_OP_DOT = 35, SG_OP_AXPY_RATIO = 36, SG_OP_XPAY_RATIO = 37, SG_OP_COPY_SCALAR = 38
 };
 
 typedef struct {

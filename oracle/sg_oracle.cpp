@@ -60,7 +60,8 @@ enum {
   OP_CLEAR_SCALAR = 10,
   OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22,
   OP_LOSS_MEAN = 27, OP_ADJ_INIT = 28, OP_G2P_ADJ = 29, OP_P2G_ADJ = 30,
-  OP_SMOOTH_RB = 31, OP_RESTRICT = 32, OP_PROLONG = 33, OP_RESID_NORM2 = 34
+  OP_SMOOTH_RB = 31, OP_RESTRICT = 32, OP_PROLONG = 33, OP_RESID_NORM2 = 34,
+  OP_DOT = 35, OP_AXPY_RATIO = 36, OP_XPAY_RATIO = 37, OP_COPY_SCALAR = 38
 };
 
 typedef std::array<int64_t, 3> Coord;
@@ -566,6 +567,42 @@ int struct_for(Grid* g, int op, int leaf_snode, const int32_t* f, int nf, const 
         if (!rc) rc = atomic_add_m(g, f[0], Coord{0, 0, 0}, res * res, 2.0 * std::fabs(res) * m, false);
       });
       break;
+    // --- conjugate gradients around the multigrid preconditioner (MGPCG, PAPER.md:438-441;
+    // hu2019taichi): dot products into 0-D fields, updates scaled by a ratio of 0-D fields
+    case OP_DOT:
+      // f0[] += p0 * f1[c] * f2[c]
+      if (!need(3)) return fail(g, E_ARG, "DOT needs 3 fields");
+      if (g->trees[g->fields[f[0]].tree].nd != 0) return fail(g, E_ARG, "DOT target must be 0-D");
+      for_struct(g, t, [&](const Coord& c) {
+        const double a = read(g, f[1], c), b = read(g, f[2], c);
+        const double m = std::fabs(P(0)) * read_mag(g, f[1], c) * read_mag(g, f[2], c);
+        if (!rc) rc = atomic_add_m(g, f[0], Coord{0, 0, 0}, P(0) * a * b, m, false);
+      });
+      break;
+    case OP_AXPY_RATIO:
+    case OP_XPAY_RATIO: {
+      // AXPY_RATIO: f0[c] += p0 * (f2[] / f3[]) * f1[c];  XPAY_RATIO: f0[c] = f1[c] + (f2[] / f3[]) * f0[c]
+      if (!need(4)) return fail(g, E_ARG, "ratio updates need 4 fields");
+      for (int k = 2; k < 4; k++)
+        if (g->trees[g->fields[f[k]].tree].nd != 0) return fail(g, E_ARG, "ratio operands must be 0-D");
+      const Coord z{0, 0, 0};
+      const double num = read(g, f[2], z), den = read(g, f[3], z);
+      const double ratio = num / den;
+      const double rm = (read_mag(g, f[2], z) + std::fabs(ratio) * read_mag(g, f[3], z)) / std::fabs(den);
+      for_struct(g, t, [&](const Coord& c) {
+        const double a = read(g, f[1], c), am = read_mag(g, f[1], c);
+        const double o = read(g, f[0], c), om = read_mag(g, f[0], c);
+        double v, m;
+        if (op == OP_AXPY_RATIO) {
+          v = o + P(0) * ratio * a;
+          m = om + std::fabs(P(0)) * (std::fabs(ratio) * am + rm * std::fabs(a));
+        } else {
+          v = a + ratio * o;
+          m = am + std::fabs(ratio) * om + rm * std::fabs(o);
+        }
+        if (!rc) rc = write(g, f[0], c, v, act_bit(activating, 0), m);
+      });
+    } break;
     case OP_JITTER:
       // x[i] += x[i + 1] for even i along axis 0 (PAPER.md:505 deep_hierarchy)
       if (!need(1)) return fail(g, E_ARG, "JITTER needs 1 field");
@@ -973,6 +1010,16 @@ int serial(Grid* g, int op, const int32_t* f, int nf, const float* p, int np) {
       if (nf < 1 || !field_ok(g, f[0])) return fail(g, E_ARG, "CLEAR_SCALAR needs a field");
       if (g->trees[g->fields[f[0]].tree].nd != 0) return fail(g, E_ARG, "CLEAR_SCALAR target must be 0-D");
       int rc = write(g, f[0], Coord{0, 0, 0}, 0.0, false, 0.0);
+      if (rc) { g->touched.clear(); return rc; }
+      return end_task(g);
+    }
+    case OP_COPY_SCALAR: {
+      // f0[] = f1[]  (MGPCG: zTr_old = zTr_new)
+      if (nf < 2 || !field_ok(g, f[0]) || !field_ok(g, f[1])) return fail(g, E_ARG, "COPY_SCALAR needs 2 fields");
+      if (g->trees[g->fields[f[0]].tree].nd != 0 || g->trees[g->fields[f[1]].tree].nd != 0)
+        return fail(g, E_ARG, "COPY_SCALAR operands must be 0-D");
+      const Coord z{0, 0, 0};
+      int rc = write(g, f[0], z, read(g, f[1], z), false, read_mag(g, f[1], z));
       if (rc) { g->touched.clear(); return rc; }
       return end_task(g);
     }

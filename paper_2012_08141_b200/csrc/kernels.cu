@@ -639,6 +639,8 @@ struct SerArgs {
 __global__ void k_serial(const __grid_constant__ SerArgs A) {
   for (int o = 0; o < A.nops; o++) {
     if (A.ops[o].op == SG_OP_CLEAR_SCALAR) *(uint32_t*)A.aux[o] = 0u;
+    if (A.ops[o].op == SG_OP_COPY_SCALAR)
+      *(uint32_t*)A.aux[o] = A.C.scalars[A.C.fields[A.ops[o].f[1]].scalar];
     if (A.ops[o].op == SG_OP_ARRAY_COUNT) *A.C.arrays[A.ops[o].a[0]].dcount = (int32_t)A.ops[o].p[0];
   }
 }
@@ -914,7 +916,8 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   a->table = drive ? drive->table : nullptr;
   a->table_ctl = drive ? drive->ctl : nullptr;
   a->has_reduce = 0;
-  for (int o = 0; o < nops; o++) a->has_reduce |= ops[o].op == SG_OP_REDUCE_SUM || ops[o].op == SG_OP_RESID_NORM2;
+  for (int o = 0; o < nops; o++)
+    a->has_reduce |= ops[o].op == SG_OP_REDUCE_SUM || ops[o].op == SG_OP_RESID_NORM2 || ops[o].op == SG_OP_DOT;
   a->need_nbr = 0;
   bool i32 = false;
   for (int o = 0; o < nops; o++) {

@@ -108,6 +108,10 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
     case SG_OP_RESTRICT: F(1, R_READ, AC_ID); F(2, R_READ, AC_NBR); F(0, R_RW, AC_DIV2); break;
     case SG_OP_PROLONG: F(1, R_READ, AC_DIV2); F(0, R_RW, AC_ID); break;
     case SG_OP_RESID_NORM2: F(1, R_READ, AC_ID); F(2, R_READ, AC_NBR); F(0, R_RW, AC_CONST); break;
+    case SG_OP_DOT: F(1, R_READ, AC_ID); F(2, R_READ, AC_ID); F(0, R_RW, AC_CONST); break;
+    case SG_OP_AXPY_RATIO:
+    case SG_OP_XPAY_RATIO: F(1, R_READ, AC_ID); F(2, R_READ, AC_CONST); F(3, R_READ, AC_CONST); F(0, R_RW, AC_ID); break;
+    case SG_OP_COPY_SCALAR: F(1, R_READ, AC_CONST); F(0, R_WRITE, AC_CONST, true); break;
     case SG_OP_ADJ_INIT:
       for (int i = 0; i < 4; i++) A(i, R_WRITE, AC_ID, true);
       break;
@@ -161,7 +165,9 @@ static int op_min_fields(int op) {
     case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: return 0;
     case SG_OP_LOSS_MEAN: return 1;
     case SG_OP_SMOOTH_RB: case SG_OP_PROLONG: return 2;
-    case SG_OP_RESTRICT: case SG_OP_RESID_NORM2: return 3;
+    case SG_OP_RESTRICT: case SG_OP_RESID_NORM2: case SG_OP_DOT: return 3;
+    case SG_OP_AXPY_RATIO: case SG_OP_XPAY_RATIO: return 4;
+    case SG_OP_COPY_SCALAR: return 2;
     case SG_OP_G2P_ADJ: return 8;
     case SG_OP_P2G_ADJ: return 4;
     case SG_OP_HALO_PACK: case SG_OP_HALO_UNPACK: return 1;
@@ -342,6 +348,13 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
   }
   if (t.op == SG_OP_CLEAR_SCALAR) {
     if (t.kind != SG_TASK_SERIAL || L.field_tree[t.fields[0]] >= 0) { err = "CLEAR_SCALAR is a serial op on a 0-D field"; return SG_ERR_ARG; }
+    return SG_OK;
+  }
+  if (t.op == SG_OP_COPY_SCALAR) {
+    if (t.kind != SG_TASK_SERIAL || L.field_tree[t.fields[0]] >= 0 || L.field_tree[t.fields[1]] >= 0 ||
+        L.field_dtype[t.fields[0]] != L.field_dtype[t.fields[1]]) {
+      err = "COPY_SCALAR is a serial op on two 0-D fields of one dtype"; return SG_ERR_ARG;
+    }
     return SG_OK;
   }
   if (t.op == SG_OP_P2G || t.op == SG_OP_G2P || t.op == SG_OP_GRID_OP || t.op == SG_OP_G2P_MIGRATE) {
@@ -804,7 +817,8 @@ static void pass_chain(const HLayout& L, std::vector<PTask>& seq, const std::vec
   };
   auto group_reduces = [&](const PTask& t) {
     for (int m : t.members)
-      if (eager[m].t.op == SG_OP_REDUCE_SUM || eager[m].t.op == SG_OP_RESID_NORM2) return true;
+      if (eager[m].t.op == SG_OP_REDUCE_SUM || eager[m].t.op == SG_OP_RESID_NORM2 || eager[m].t.op == SG_OP_DOT)
+        return true;
     return false;
   };
   for (int i = 0; i < n; i++) {

@@ -113,7 +113,7 @@ __device__ void finish_reductions(const SFArgs& A, const DOp* ops, int nops) {
   if (!s_last) return;
   __threadfence();
   for (int o = 0; o < nops; o++) {
-    if (ops[o].op != SG_OP_REDUCE_SUM && ops[o].op != SG_OP_RESID_NORM2) continue;
+    if (ops[o].op != SG_OP_REDUCE_SUM && ops[o].op != SG_OP_RESID_NORM2 && ops[o].op != SG_OP_DOT) continue;
     double t = 0.0;   // fixed-order tree sum over CTAs
     for (int b = threadIdx.x; b < G; b += SF_TPB) t += __ldcg(&A.C.partials[o * A.C.max_grid + b]);
     s_sum[threadIdx.x] = t;
@@ -209,6 +209,12 @@ __device__ __noinline__ V read_other(const SFArgs& A, int f, const int h[3]) {
   return ldv<V>(cont + T2.payload_off + ((uint64_t)tf.slot << T2.ln_leaf) + idx);
 }
 
+// Value of a 0-D field (written by an earlier launch).
+template <typename V>
+__device__ __forceinline__ V scalar_of(const SFArgs& A, int f) {
+  return ldv<V>(A.C.scalars + A.C.fields[f].scalar);
+}
+
 // r - A z at the cell (A = -Laplacian, h = 1)
 template <typename V>
 __device__ __forceinline__ V residual_at(const CellCtx& x, int slot_r, int slot_z) {
@@ -256,6 +262,15 @@ __device__ __forceinline__ V apply_cell(const SFArgs& A, const DOp& op, const Ce
       const V r = residual_at<V>(x, op.slot[1], op.slot[2]);
       return r * r;
     }
+    case SG_OP_DOT: return (V)op.p[0] * ld_id<V>(x, op.slot[1]) * ld_id<V>(x, op.slot[2]);
+    case SG_OP_AXPY_RATIO:
+    case SG_OP_XPAY_RATIO: {
+      const V ratio = scalar_of<V>(A, op.f[2]) / scalar_of<V>(A, op.f[3]);
+      if (op.op == SG_OP_AXPY_RATIO)
+        st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[0]) + (V)op.p[0] * ratio * ld_id<V>(x, op.slot[1]));
+      else
+        st_id<V>(x, op.slot[0], ld_id<V>(x, op.slot[1]) + ratio * ld_id<V>(x, op.slot[0]));
+    } break;
     default: break;
   }
   return V(0);
@@ -539,7 +554,7 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int n
             acc += apply_cell<V>(A, op, c);
           }
         }
-        if (op.op == SG_OP_RESID_NORM2) warp_add<V>(o, acc);
+        if (op.op == SG_OP_RESID_NORM2 || op.op == SG_OP_DOT) warp_add<V>(o, acc);
       } break;
     }
   }
@@ -591,7 +606,7 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const DOp* ops, int n
       x.c[2] = tile.org[x.e][2] + bc[2];
       acc += apply_cell<V>(A, op, x);
     }
-    if (op.op == SG_OP_REDUCE_SUM || op.op == SG_OP_RESID_NORM2) warp_add<V>(o, acc);
+    if (op.op == SG_OP_REDUCE_SUM || op.op == SG_OP_RESID_NORM2 || op.op == SG_OP_DOT) warp_add<V>(o, acc);
   }
 }
 

@@ -28,7 +28,8 @@ OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6
        "DOWNSAMPLE": 8, "JITTER": 9, "CLEAR_SCALAR": 10, "ARRAY_COUNT": 11, "P2G": 20, "GRID_OP": 21, "G2P": 22,
        "HALO_PACK": 23, "HALO_UNPACK": 24, "G2P_MIGRATE": 25, "MIGRATE_APPEND": 26,
        "LOSS_MEAN": 27, "ADJ_INIT": 28, "G2P_ADJ": 29, "P2G_ADJ": 30,
-       "SMOOTH_RB": 31, "RESTRICT": 32, "PROLONG": 33, "RESID_NORM2": 34}
+       "SMOOTH_RB": 31, "RESTRICT": 32, "PROLONG": 33, "RESID_NORM2": 34,
+       "DOT": 35, "AXPY_RATIO": 36, "XPAY_RATIO": 37, "COPY_SCALAR": 38}
 CLEAR_VALUES, DEACTIVATE = 0, 1
 PASS_LISTGEN_REMOVAL, PASS_ACT_DEMOTION, PASS_FUSION, PASS_DSE = 1, 2, 4, 8
 PASS_ALL = 15

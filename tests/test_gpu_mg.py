@@ -75,3 +75,35 @@ def test_mg_full_size_ten_cycles_converge():
     # (4 levels down to a 64^2 bottom grid smoothed 8 times: a slow V-cycle on
     # its own -- the paper wraps it in CG -- but the residual must keep falling)
     assert np.isfinite(res).all() and res[1] < 0.9 * res[0]
+
+
+def test_mgpcg_small():
+    """MGPCG: two CG iterations on 64^2 -- every field within 1e-3 of M (CG
+    divides by device-computed dot products; reading R32's multi-step bound)."""
+    prog = W.mgpcg_program(n=64, levels=3, block=8, iters=2, radius_frac=0.3)
+    o = oracle.run_program(prog)
+    g = sg.Grid(prog["desc"])
+    sg.replay(g, prog, device="cuda")
+    g.sync()
+    compare(g, o, prog, tol=1e-3)
+
+
+def test_mgpcg_full_size_converges():
+    """512^2, 4 levels: the CG residual falls by > 1e4 in 10 iterations and x
+    matches the oracle's x after 2 iterations."""
+    prog = W.mgpcg_program(n=512, iters=10)
+    g = sg.Grid(prog["desc"])
+    sg.replay(g, prog, device="cuda")
+    g.sync()
+    L = prog["layout"]
+    rTr = float(np.asarray(g.field(L.fields["rTr"])).reshape(-1)[0])
+    n_active = len(W.mg_region(512, 16, 0.3125)) * 256
+    assert np.isfinite(rTr) and rTr < 1e-4 * n_active
+    prog2 = W.mgpcg_program(n=512, iters=2)
+    o = oracle.run_program(prog2)
+    g2 = sg.Grid(prog2["desc"])
+    sg.replay(g2, prog2, device="cuda")
+    g2.sync()
+    want, mag = o.field(L.fields["x"], with_mag=True)
+    got = np.asarray(g2.field(L.fields["x"]), dtype=np.float64)
+    assert (np.abs(got - want) <= 1e-3 * np.maximum(np.abs(want), mag)).all()

@@ -137,3 +137,59 @@ def test_mg_residual_decreases():
         res.append(float(np.asarray(o.field(prog["layout"].fields["res"])).reshape(-1)[0]))
     assert res[0] > res[1] > res[2] > res[3]
     assert res[3] < 0.25 * res[0]
+
+
+def test_mgpcg_solves_the_masked_poisson_system():
+    """MGPCG (CG preconditioned by one V-cycle): after 10
+    iterations x solves A x = 1 on the active region, checked against a direct
+    sparse solve of the same masked 5-point system (scipy)."""
+    from scipy.sparse import lil_matrix
+    from scipy.sparse.linalg import spsolve
+    prog = W.mgpcg_program(n=N, levels=LEVELS, block=BLOCK, iters=10, radius_frac=RADIUS)
+    o = run_exact(prog)
+    L = prog["layout"]
+    x = o.field(L.fields["x"])
+    m = dense_masks()[0]
+    act = np.argwhere(m > 0)
+    idx = -np.ones((N, N), dtype=np.int64)
+    idx[tuple(act.T)] = np.arange(len(act))
+    A = lil_matrix((len(act), len(act)))
+    for k, (i, j) in enumerate(act):
+        A[k, k] = 4.0
+        for di, dj in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+            ii, jj = i + di, j + dj
+            if 0 <= ii < N and 0 <= jj < N and idx[ii, jj] >= 0:
+                A[k, idx[ii, jj]] = -1.0
+    xs = spsolve(A.tocsr(), np.ones(len(act)))
+    assert np.abs(x[tuple(act.T)] - xs).max() < 1e-5 * np.abs(xs).max()
+    assert float(np.asarray(o.field(L.fields["rTr"])).reshape(-1)[0]) < 1e-4
+    assert not x[m == 0].any()
+
+
+def test_cg_ops_closed_form():
+    """DOT, AXPY_RATIO, XPAY_RATIO, COPY_SCALAR on known fields."""
+    L, lv = W.mg_layout(16, 1, 8, cg=True)
+    f = L.fields
+    o = Oracle(L.desc())
+    o.set_exact(True)
+    coords = np.array([[0, 0], [8, 8]], dtype=np.int32)
+    o.call(W.activate(f["z0"], coords))
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal((16, 16)), rng.standard_normal((16, 16))
+    m = np.zeros((16, 16))
+    m[0:8, 0:8] = m[8:16, 8:16] = 1
+    o.load_field(f["x"], a)
+    o.load_field(f["p"], b)
+    leaf = lv[0][-1]
+    for c in (W.serial("CLEAR_SCALAR", [f["zTr_old"]]), W.struct_for("DOT", leaf, [f["zTr_old"], f["x"], f["p"]], [2.0]),
+              W.serial("CLEAR_SCALAR", [f["pAp"]]), W.struct_for("DOT", leaf, [f["pAp"], f["x"], f["x"]], [1.0])):
+        o.call(c)
+    dot_ab, dot_aa = 2.0 * (a * b * m).sum(), (a * a * m).sum()
+    assert float(o.field(f["zTr_old"]).reshape(-1)[0]) == pytest.approx(dot_ab, rel=1e-12)
+    o.call(W.struct_for("AXPY_RATIO", leaf, [f["p"], f["x"], f["zTr_old"], f["pAp"]], [-0.5]))
+    want_p = (b - 0.5 * (dot_ab / dot_aa) * a) * m
+    np.testing.assert_allclose(o.field(f["p"]), want_p, rtol=1e-12, atol=1e-12)
+    o.call(W.struct_for("XPAY_RATIO", leaf, [f["x"], f["p"], f["pAp"], f["zTr_old"]]))
+    np.testing.assert_allclose(o.field(f["x"]), (want_p + (dot_aa / dot_ab) * a) * m, rtol=1e-12, atol=1e-12)
+    o.call(W.serial("COPY_SCALAR", [f["rTr"], f["pAp"]]))
+    assert float(o.field(f["rTr"]).reshape(-1)[0]) == pytest.approx(dot_aa, rel=1e-15)

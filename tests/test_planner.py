@@ -259,6 +259,27 @@ def test_mg_demotion_and_listgen_removal():
     assert nodem[0]["launches"] > s["launches"]
 
 
+def test_mgpcg_counts():
+    # MGPCG: listgens 657 -> 7; demotion alone accounts for 37 -> 7
+    # (the paper: 6.7x from demotion); the per-iteration residual monitor (rTr) is
+    # overwritten before it is observed except in the last iteration: DSE
+    prog = W.mgpcg_program(n=512, iters=10)
+    s = plan_counts(prog)[0][0]
+    assert (s["tasks_lowered"], s["launches"], s["listgen_launched"]) == (1356, 599, 7)
+    assert s["dead_removed"] == 2 * 9 and s["demotions"] == 30
+    nodem = plan_counts(prog, passes=15 & ~2)[0][0]
+    assert nodem["listgen_launched"] == 37
+
+
+@pytest.mark.parametrize("passes", [0, 1, 3, 15])
+def test_mgpcg_schedule_soundness_on_oracle(passes):
+    prog = W.mgpcg_program(n=64, levels=3, block=8, iters=3, radius_frac=0.3)
+    ref = oracle.run_program(prog)
+    o = replay_plan_on_oracle(prog, passes)
+    for name, fid in prog["layout"].fields.items():
+        assert np.array_equal(o.field(fid), ref.field(fid)), (passes, name)
+
+
 @pytest.mark.parametrize("passes", [0, 1, 3, 15])
 def test_mg_schedule_soundness_on_oracle(passes):
     prog = W.mg_program(n=64, levels=3, block=8, cycles=2, radius_frac=0.3)
@@ -334,8 +355,10 @@ def replay_plan_on_oracle(prog, passes):
             elif t == "deactivate":
                 o.deactivate_task(int(snode))
             elif t == "serial":
-                f = c["fields"][0] if c["call"] == "serial" else c["target"]
-                o.serial_task("CLEAR_SCALAR", [f])
+                if c["call"] == "serial":
+                    o.serial_task(c["op"], c["fields"], c.get("params", []))
+                else:
+                    o.serial_task("CLEAR_SCALAR", [c["target"]])
             elif t == "range_for":
                 o.range_for_task(c["op"], c["n"], c["fields"], c["arrays"], c.get("params", []), int(act))
             elif t == "struct_for":

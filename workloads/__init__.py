@@ -388,16 +388,21 @@ def c4_program(n_grid=64, n_particles=100_000, T=64, seed=0, passes="all", comp=
 # Gauss-Seidel smoothing, residual restriction with activate-on-write on the
 # coarse level (demoted after the first cycle), prolongation.
 # ----------------------------------------------------------------------------
-def mg_layout(n=512, levels=4, block=16):
+def mg_layout(n=512, levels=4, block=16, cg=False):
     L = Layout()
     lv = []
     for l in range(levels):
         nl = n >> l
         b = min(block, nl)
-        ids = L.chain([("pointer", (nl // b,) * 2), ("dense", (b,) * 2)],
-                      [(f"z{l}", "f32"), (f"r{l}", "f32")])
+        fields = [(f"z{l}", "f32"), (f"r{l}", "f32")]
+        if cg and l == 0:
+            fields += [("x", "f32"), ("p", "f32"), ("Ap", "f32")]
+        ids = L.chain([("pointer", (nl // b,) * 2), ("dense", (b,) * 2)], fields)
         lv.append(ids)
     L.scalar("res")
+    if cg:
+        for name in ("zTr_old", "zTr_new", "pAp", "rTr"):
+            L.scalar(name)
     return L, lv
 
 
@@ -456,6 +461,47 @@ def mg_solve_calls(L, lv, coords, cycles=10, levels=4, nu=2, bottom=8, dim=2, wi
         calls += [serial("CLEAR_SCALAR", [f["res"]]),
                   struct_for("RESID_NORM2", lv[0][-1], [f["res"], f["r0"], f["z0"]])]
     return calls
+
+
+def mgpcg_calls(L, lv, coords, iters=10, levels=4, nu=2, bottom=8, dim=2):
+    """Conjugate gradients preconditioned by one V-cycle (MGPCG, PAPER.md:438-441
+    after hu2019taichi): solve A x = b (b = 1 on the active region).  The
+    V-cycle works on (z0, r0), so r0 doubles as the CG residual.  STENCIL gives
+    -A p, so pAp = -<p, STENCIL p> and r -= alpha A p becomes r += alpha (-A p)."""
+    f = L.fields
+    leaf0 = lv[0][-1]
+    w = 2.0 / (1 << dim)
+
+    def precondition():
+        return [struct_for("FILL", leaf0, [f["z0"]], [0.0])] + mg_vcycle_calls(L, lv, levels, nu, bottom, weight=w)
+
+    calls = [activate(f["z0"], coords), struct_for("FILL", leaf0, [f["r0"]], [1.0]),
+             struct_for("FILL", leaf0, [f["x"]], [0.0])]
+    calls += precondition()
+    calls += [struct_for("ADD_CONST", leaf0, [f["p"], f["z0"]], [0.0]),
+              serial("CLEAR_SCALAR", [f["zTr_old"]]), struct_for("DOT", leaf0, [f["zTr_old"], f["z0"], f["r0"]], [1.0])]
+    for _ in range(iters):
+        calls += [struct_for("STENCIL", leaf0, [f["Ap"], f["p"]]),
+                  serial("CLEAR_SCALAR", [f["pAp"]]), struct_for("DOT", leaf0, [f["pAp"], f["p"], f["Ap"]], [-1.0]),
+                  struct_for("AXPY_RATIO", leaf0, [f["x"], f["p"], f["zTr_old"], f["pAp"]], [1.0]),
+                  struct_for("AXPY_RATIO", leaf0, [f["r0"], f["Ap"], f["zTr_old"], f["pAp"]], [1.0]),
+                  serial("CLEAR_SCALAR", [f["rTr"]]), struct_for("DOT", leaf0, [f["rTr"], f["r0"], f["r0"]], [1.0])]
+        calls += precondition()
+        calls += [serial("CLEAR_SCALAR", [f["zTr_new"]]),
+                  struct_for("DOT", leaf0, [f["zTr_new"], f["z0"], f["r0"]], [1.0]),
+                  struct_for("XPAY_RATIO", leaf0, [f["p"], f["z0"], f["zTr_new"], f["zTr_old"]]),
+                  serial("COPY_SCALAR", [f["zTr_old"], f["zTr_new"]])]
+    return calls
+
+
+def mgpcg_program(n=512, levels=4, block=16, iters=10, nu=2, bottom=8, radius_frac=0.3125, passes="all"):
+    L, lv = mg_layout(n, levels, block, cg=True)
+    coords = mg_region(n, block, radius_frac)
+    calls = mgpcg_calls(L, lv, coords, iters, levels, nu, bottom)
+    calls.append(flush(passes))
+    prog = program(L, calls, name="MGPCG")
+    prog["levels"] = lv
+    return prog
 
 
 def mg_program(n=512, levels=4, block=16, cycles=10, nu=2, bottom=8, radius_frac=0.3125, passes="all"):
