@@ -53,8 +53,10 @@ def coarse_mask(m, block):
 def dense_vcycle(z, r, masks, l, nu=2, bottom=8, w=0.5):
     m = masks[l]
     if l == len(masks) - 1:
-        for _ in range(bottom):
+        for _ in range(bottom // 2):
             z = rb_half_sweep(rb_half_sweep(z, r, m, 0), r, m, 1)
+        for _ in range(bottom - bottom // 2):
+            z = rb_half_sweep(rb_half_sweep(z, r, m, 1), r, m, 0)
         return z
     for _ in range(nu):
         z = rb_half_sweep(rb_half_sweep(z, r, m, 0), r, m, 1)

@@ -438,8 +438,12 @@ def mg_vcycle_calls(L, lv, levels=4, nu=2, bottom=8, weight=1.0):
             calls += smooth(l)
         calls += [clear_values(r[l + 1]), clear_values(z[l + 1])]
         calls.append(struct_for("RESTRICT", leaf[l], [r[l + 1], r[l], z[l]], [weight], [True]))
-    for _ in range(bottom):
+    # bottom: (red, black) sweeps then (black, red) sweeps -- a symmetric smoother,
+    # so the V-cycle is a symmetric preconditioner for MGPCG
+    for _ in range(bottom // 2):
         calls += smooth(levels - 1)
+    for _ in range(bottom - bottom // 2):
+        calls += smooth(levels - 1, (1, 0))
     for l in reversed(range(levels - 1)):
         calls.append(struct_for("PROLONG", leaf[l], [z[l], z[l + 1]]))
         for _ in range(nu):
