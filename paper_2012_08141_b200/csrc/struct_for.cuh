@@ -52,6 +52,7 @@ struct SFTile {
   int org[SF_MAXE][3];
   uint32_t nbr[SF_MAXE][6];
   int32_t slot[SF_MAXE];      // HALO_PACK: record slot of each block, -1 = not packed
+  uint32_t aux[SF_MAXE];      // RESTRICT / PROLONG: the coarse block (field slot 0) of each block
   uint32_t ne;
 };
 
@@ -430,6 +431,28 @@ __device__ __forceinline__ Q4<V> nbr_sum4(const NbrLoads<V, ND>& L, const Q4<V>&
   return s;
 }
 
+// Per-lane fallback of the QUAD path: each active lane through apply_cell.
+template <typename V, int ND>
+__device__ __forceinline__ void run_lanes(const SFArgs& A, const DOp& op, int o, const SFTile& tile, uint32_t* P,
+                                          uint32_t nq, uint32_t lq, bool chunked, uint32_t jbase, uint64_t fs,
+                                          const QG& g) {
+  V acc = V(0);
+  for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+    QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+    if (x.off == SG_NO_BLOCK) continue;
+    for (int k = 0; k < 4; k++) {
+      if (!((x.amask >> k) & 1u)) continue;
+      CellCtx c;
+      c.T = &A.T; c.tile = &tile; c.P = P; c.e = x.e; c.j = x.j0 + k; c.fstride = fs;
+#pragma unroll
+      for (int a = 0; a < 3; a++) c.c[a] = tile.org[x.e][a] + x.r[a];
+      c.c[ND - 1] += k;
+      acc += apply_cell<V>(A, op, c);
+    }
+  }
+  if (op.op == SG_OP_RESID_NORM2 || op.op == SG_OP_DOT) warp_add<V>(o, acc);
+}
+
 template <typename V, int ND, bool PAIR, int GL>
 __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int nops, const SFTile& tile, uint32_t* P,
                                           uint32_t nq, uint32_t lq, bool chunked, uint32_t jbase, uint64_t fs) {
@@ -507,6 +530,141 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int n
           }
         }
       } break;
+      case SG_OP_SMOOTH_RB:
+      case SG_OP_RESID_NORM2: {
+        // red-black half sweep in place (the updated colour reads only the other
+        // colour, so concurrent quads never see a value they depend on change),
+        // or the squared residual r - A z (reduction)
+        const bool rb = op.op == SG_OP_SMOOTH_RB;
+        const V inv = V(1) / (V)(2 * ND);
+        const uint32_t* __restrict__ zsrc = P + (rb ? s0 : s2);
+        const uint32_t* __restrict__ rsrc = P + s1;
+        V acc = V(0);
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || !x.amask) continue;
+          const Q4<V> c = ld4<V>(zsrc + x.off), r = ld4<V>(rsrc + x.off);
+          NbrLoads<V, ND> L;
+          nbr_load<V, ND>(g, tile, zsrc, x, L);
+          const Q4<V> sn = nbr_sum4<V, ND>(L, c);
+          if (rb) {
+            int par = 0;
+#pragma unroll
+            for (int a = 0; a < ND; a++) par += tile.org[x.e][a] + x.r[a];
+            Q4<V> out;
+#pragma unroll
+            for (int k = 0; k < 4; k++) out.v[k] = (((par + k) & 1) == (int)op.p[0]) ? (r.v[k] + sn.v[k]) * inv : c.v[k];
+            st4<V>(P + s0 + x.off, out, x.amask);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+              if ((x.amask >> k) & 1u) {
+                const V res = r.v[k] - ((V)(2 * ND) * c.v[k] - sn.v[k]);
+                acc += res * res;
+              }
+          }
+        }
+        if (!rb) warp_add<V>(o, acc);
+      } break;
+      case SG_OP_DOT: {
+        V acc = V(0);
+        const V p0 = (V)op.p[0];
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || !x.amask) continue;
+          const Q4<V> a = ld4<V>(P + s1 + x.off), b = ld4<V>(P + s2 + x.off);
+#pragma unroll
+          for (int k = 0; k < 4; k++)
+            if ((x.amask >> k) & 1u) acc += p0 * a.v[k] * b.v[k];
+        }
+        warp_add<V>(o, acc);
+      } break;
+      case SG_OP_AXPY_RATIO:
+      case SG_OP_XPAY_RATIO: {
+        const V ratio = scalar_of<V>(A, op.f[2]) / scalar_of<V>(A, op.f[3]);
+        const V p0 = (V)op.p[0];
+        const bool axpy = op.op == SG_OP_AXPY_RATIO;
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || !x.amask) continue;
+          const Q4<V> a = ld4<V>(P + s1 + x.off), o0 = ld4<V>(P + s0 + x.off);
+          Q4<V> out;
+#pragma unroll
+          for (int k = 0; k < 4; k++) out.v[k] = axpy ? o0.v[k] + p0 * ratio * a.v[k] : a.v[k] + ratio * o0.v[k];
+          st4<V>(P + s0 + x.off, out, x.amask);
+        }
+      } break;
+      case SG_OP_RESTRICT:
+      case SG_OP_PROLONG: {
+        // the coarse cells of one block lie in ONE coarse block (coarse blocks
+        // at least half as wide): resolve it once per block, not per cell
+        const bool restrict_ = op.op == SG_OP_RESTRICT;
+        const int cf = restrict_ ? 0 : 1;
+        const DField& CF = A.C.fields[op.f[cf]];
+        const DTree& T2 = A.C.trees[CF.tree];
+        bool fast = !T2.leaf_bitmasked && T2.driving >= 0 && T2.nd == ND;
+#pragma unroll
+        for (int a = 0; a < ND; a++) fast = fast && T2.lev[T2.driving].lbelow[a] + 1 >= g.lb[a];
+        if (!fast) {
+          run_lanes<V, ND>(A, op, o, tile, P, nq, lq, chunked, jbase, fs, g);
+          break;
+        }
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < tile.ne; e += SF_TPB) {
+          uint32_t off = SG_NO_BLOCK;
+          if (tile.blk[e] != SG_NO_BLOCK) {
+            const int h[3] = {tile.org[e][0] >> 1, tile.org[e][1] >> 1, tile.org[e][2] >> 1};
+            uint32_t idx;
+            uint32_t* cont;
+            if (restrict_ && (op.act & 1u)) cont = activate_walk(A.C, T2, h, idx, A.task);
+            else cont = locate(T2, h, idx);
+            if (cont) off = (uint32_t)(cont - T2.seg[T2.nseg - 1].base) + T2.payload_off + (idx & ~((1u << T2.lblk) - 1u));
+            else if (restrict_ && A.C.debug) set_err(A.C, SG_ERR_DEMOTION_TRAP, A.task);
+          }
+          const_cast<SFTile&>(tile).aux[e] = off;
+        }
+        __syncthreads();
+        uint32_t* cpool = T2.seg[T2.nseg - 1].base + ((uint64_t)CF.slot << T2.ln_leaf);
+        const uint32_t* __restrict__ zsrc = P + s2;
+        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
+          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
+          if (x.off == SG_NO_BLOCK || !x.amask) continue;
+          const uint32_t cb = tile.aux[x.e];
+          int h[3];
+#pragma unroll
+          for (int a = 0; a < 3; a++) h[a] = (tile.org[x.e][a] + x.r[a]) >> 1;
+          if (restrict_) {
+            if (cb == SG_NO_BLOCK) continue;
+            const Q4<V> r = ld4<V>(P + s1 + x.off), c = ld4<V>(zsrc + x.off);
+            NbrLoads<V, ND> L;
+            nbr_load<V, ND>(g, tile, zsrc, x, L);
+            const Q4<V> sn = nbr_sum4<V, ND>(L, c);
+            V res[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+              res[k] = ((x.amask >> k) & 1u) ? (V)op.p[0] * (r.v[k] - ((V)(2 * ND) * c.v[k] - sn.v[k])) : V(0);
+            // lanes (0,1) and (2,3) share a coarse cell along the fast axis
+#pragma unroll
+            for (int pr = 0; pr < 2; pr++) {
+              int hc[3] = {h[0], h[1], h[2]};
+              hc[ND - 1] = (tile.org[x.e][ND - 1] + x.r[ND - 1] + 2 * pr) >> 1;
+              if ((x.amask >> (2 * pr)) & 3u)
+                atomic_add_v(cpool + cb + inblock_idx(T2, hc), res[2 * pr] + res[2 * pr + 1]);
+            }
+          } else {
+            Q4<V> out = ld4<V>(P + s0 + x.off);
+#pragma unroll
+            for (int pr = 0; pr < 2; pr++) {
+              int hc[3] = {h[0], h[1], h[2]};
+              hc[ND - 1] = (tile.org[x.e][ND - 1] + x.r[ND - 1] + 2 * pr) >> 1;
+              const V cv = cb == SG_NO_BLOCK ? V(0) : ldv<V>(cpool + cb + inblock_idx(T2, hc));
+              out.v[2 * pr] += cv;
+              out.v[2 * pr + 1] += cv;
+            }
+            st4<V>(P + s0 + x.off, out, x.amask);
+          }
+        }
+      } break;
       case SG_OP_REDUCE_SUM: {
         V acc = V(0);
         for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
@@ -538,24 +696,10 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int n
                 *reinterpret_cast<const uint4*>(P + (uint64_t)op.slot[k] * fs + x.off);
         }
       } break;
-      default: {
-        // per-lane ops (DOWNSAMPLE, JITTER, GRID_OP, multigrid)
-        V acc = V(0);
-        for (uint32_t i = threadIdx.x; i < nq; i += SF_TPB) {
-          QuadCtx x = quad_ctx<ND>(A, g, tile, P, i, lq, chunked, jbase);
-          if (x.off == SG_NO_BLOCK) continue;
-          for (int k = 0; k < 4; k++) {
-            if (!((x.amask >> k) & 1u)) continue;
-            CellCtx c;
-            c.T = &A.T; c.tile = &tile; c.P = P; c.e = x.e; c.j = x.j0 + k; c.fstride = fs;
-#pragma unroll
-            for (int a = 0; a < 3; a++) c.c[a] = tile.org[x.e][a] + x.r[a];
-            c.c[ND - 1] += k;
-            acc += apply_cell<V>(A, op, c);
-          }
-        }
-        if (op.op == SG_OP_RESID_NORM2 || op.op == SG_OP_DOT) warp_add<V>(o, acc);
-      } break;
+      default:
+        // per-lane ops (DOWNSAMPLE, JITTER, GRID_OP)
+        run_lanes<V, ND>(A, op, o, tile, P, nq, lq, chunked, jbase, fs, g);
+        break;
     }
   }
 }
