@@ -62,7 +62,7 @@ def jac_xl(iters=10, radius=288.0):
             "frac": ach / peak, "launches": n}
 
 
-def lg_xl(reps=10, p_ptr=0.25, p_bit=0.10, seed=0):
+def lg_xl(reps=15, p_ptr=0.25, p_bit=0.10, seed=0):
     L = W.Layout()
     lv = L.chain([("pointer", (64,) * 3), ("bitmasked", (32,) * 3)], [("m", "f32")])
     gen = torch.Generator(device="cuda").manual_seed(seed)
@@ -86,14 +86,22 @@ def lg_xl(reps=10, p_ptr=0.25, p_bit=0.10, seed=0):
         total += co.shape[0]
     g.sync()
     flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    sg.set_profiling(g, True)
+    # per-repetition device time (events around the flush, L2 flushed before
+    # each); the median is reported -- single launches of this kernel vary
+    times = []
+    stream = torch.cuda.current_stream()
     for _ in range(reps):
         flush_buf.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g.listgen(lv[-1])
+        e0.record(stream)
         g.flush("all")
-    prof = sg.profile_read(g)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
     g.sync()
-    ms, n = prof[200 + lv[-1]]
+    times.sort()
+    ms, n = times[len(times) // 2] * reps, reps
     import ctypes
     cnt = ctypes.c_int64()
     sg._check(sg._lib.sg_export_list(g.h, lv[-1], None, 0, ctypes.byref(cnt)))
@@ -103,7 +111,8 @@ def lg_xl(reps=10, p_ptr=0.25, p_bit=0.10, seed=0):
     ach = nbytes / (ms / n / 1e3) / 1e9
     return {"variant": "LG-XL", "containers": n_act, "active_cells": n_out, "activate_requests": total,
             "bytes_per_launch": nbytes, "avg_launch_us": ms / n * 1e3, "achieved_GBps": ach, "peak_GBps": peak,
-            "peak_source": kind, "frac": ach / peak, "launches": n}
+            "peak_source": kind, "frac": ach / peak, "launches": n,
+            "min_us": times[0] * 1e3, "max_us": times[-1] * 1e3}
 
 
 if __name__ == "__main__":
