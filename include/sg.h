@@ -195,6 +195,9 @@ sg_status sg_activate(sg_grid* g, int32_t field, const int32_t* dev_coords, int6
 sg_status sg_listgen(sg_grid* g, int32_t snode);
 /* Enqueue one kernel-level task (struct-for / range-for / serial). */
 sg_status sg_struct_for(sg_grid* g, const sg_task* t);
+/* Enqueue n tasks (host array, borrowed for the call) in order: the same as n
+ * sg_struct_for calls, one library call (a solver loop re-submitted each step). */
+sg_status sg_struct_for_batch(sg_grid* g, const sg_task* tasks, int32_t n);
 
 enum { SG_CLEAR_VALUES = 0, SG_DEACTIVATE = 1 };
 /* Enqueue: SG_CLEAR_VALUES: target = field id, store 0 on every active cell.
@@ -202,7 +205,10 @@ enum { SG_CLEAR_VALUES = 0, SG_DEACTIVATE = 1 };
  *          and below becomes inactive, payload zeroed, pointer children freed. */
 sg_status sg_clear(sg_grid* g, int32_t target, int32_t mode);
 
-/* Pass toggles: */
+/* Pass toggles.  sg_flush replays a cached plan as a CUDA
+ * graph from its second run on; when the flush window and its device pointers
+ * are identical to the graph's last capture, the graph is relaunched without
+ * re-capturing (one cudaGraphLaunch). */
 enum {
   SG_PASS_LISTGEN_REMOVAL = 1,   /* section 6.2 */
   SG_PASS_ACT_DEMOTION = 2,      /* section 6.3 */
@@ -247,6 +253,11 @@ sg_status sg_export_mask(sg_grid* g, int32_t snode, int32_t* host_coords, int64_
 sg_status sg_export_list(sg_grid* g, int32_t snode, int32_t* host_coords, int64_t cap, int64_t* count);
 /* Dense bounding array of a field (row-major, last axis fastest); inactive -> 0. */
 sg_status sg_read_field(sg_grid* g, int32_t field, void* host_dense, int64_t bytes);
+/* Enqueue (no flush, no sync) the device-to-host copy of a 0-D field's 4 bytes
+ * into host_dst, ordered after everything flushed so far on the grid's stream.
+ * host_dst should be pinned (else the copy is synchronous); it is valid once
+ * the stream reaches this point (sg_sync, or an event the caller records). */
+sg_status sg_read_scalar_async(sg_grid* g, int32_t field, void* host_dst);
 /* State handoff: overwrite the values of the ACTIVE cells of a field from a
  * dense host array (inactive entries ignored). */
 sg_status sg_load_field(sg_grid* g, int32_t field, const void* host_dense, int64_t bytes);

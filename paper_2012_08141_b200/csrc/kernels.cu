@@ -280,13 +280,39 @@ struct ActArgs {
   int task;
 };
 
+// Explicit activation: the activating walk with warp-aggregated
+// mask updates -- lanes whose cells share a mask word (__match_any_sync on the
+// word address) OR their bits together (__reduce_or_sync) and one lane issues
+// the atomicOr, skipped when every bit is already set.
+__device__ uint32_t* activate_walk_agg(const DevCtx& C, const DTree& T, const int c[3], int task) {
+  uint32_t* cont = T.seg[0].base;
+  uint32_t idx = 0;
+  for (int l = 0; l < T.nlev; l++) {
+    const DLevel& L = T.lev[l];
+    idx = (idx << L.lE) | local_lin(L, c);
+    if (L.kind == SG_BITMASKED) {
+      uint32_t* w = cont + L.mask_off + (idx >> 5);
+      const uint32_t b = 1u << (idx & 31);
+      const unsigned am = __activemask();
+      const unsigned peers = __match_any_sync(am, (unsigned long long)w);
+      const uint32_t bits = __reduce_or_sync(peers, b);
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && (ld_volatile(w) & bits) != bits) atomicOr(w, bits);
+    } else if (L.kind == SG_POINTER) {
+      int32_t s = acquire_child(C, T, L, cont, idx, c, task);
+      if (s < 0) return nullptr;
+      cont = cont_ptr(T, L.seg + 1, (uint32_t)s);
+      idx = 0;
+    }
+  }
+  return cont;
+}
+
 __global__ void __launch_bounds__(256) k_activate(const __grid_constant__ ActArgs a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
     int c[3] = {0, 0, 0};
     for (int d = 0; d < a.T.nd; d++) c[d] = a.coords[i * a.T.nd + d];
     if (!in_domain(a.T, c)) { set_err(a.C, SG_ERR_RANGE, a.task); continue; }
-    uint32_t idx;
-    activate_walk(a.C, a.T, c, idx, a.task);
+    activate_walk_agg(a.C, a.T, c, a.task);
   }
 }
 

@@ -377,6 +377,51 @@ _lib.sg_set_array_count.argtypes = [_vp, ctypes.c_int32, _vp]
 _lib.sg_set_array_count.restype = ctypes.c_int32
 EXPORTS += ["sg_set_profiling", "sg_profile_read", "sg_set_array_count"]
 
+_lib.sg_struct_for_batch.argtypes = [_vp, _vp, ctypes.c_int32]
+_lib.sg_struct_for_batch.restype = ctypes.c_int32
+_lib.sg_read_scalar_async.argtypes = [_vp, ctypes.c_int32, _vp]
+_lib.sg_read_scalar_async.restype = ctypes.c_int32
+EXPORTS += ["sg_struct_for_batch", "sg_read_scalar_async"]
+
+
+class Batch:
+    """A marshalled task list submitted with one library call (sg_struct_for_batch):
+    for loops that re-enqueue the same tasks every step."""
+
+    def __init__(self, tasks):
+        self.n = len(tasks)
+        self.arr = (Task * max(1, self.n))(*tasks)
+
+
+def make_batch(grid, calls):
+    """Marshal workloads-style task calls (struct_for / range_for / serial) into a Batch."""
+    tasks = []
+    for c in calls:
+        k = c["call"]
+        kind = {"struct_for": TASK_STRUCT_FOR, "range_for": TASK_RANGE_FOR, "serial": TASK_SERIAL}[k]
+        t = Task()
+        t.kind = kind
+        t.op = OPS[c["op"]]
+        t.snode = c.get("snode", -1) if k == "struct_for" else -1
+        t.range_n = c.get("n", 0) if k == "range_for" else 0
+        fields, arrays, params = c.get("fields", []), c.get("arrays", []), c.get("params", [])
+        for i in range(8):
+            t.fields[i] = fields[i] if i < len(fields) else -1
+            t.arrays[i] = arrays[i] if i < len(arrays) else -1
+            t.params[i] = params[i] if i < len(params) else 0.0
+        t.activating = sum(1 << i for i, a in enumerate(c.get("activating", [])) if a)
+        tasks.append(t)
+    return Batch(tasks)
+
+
+def submit(grid, batch):
+    _check(_lib.sg_struct_for_batch(grid.h, ctypes.cast(batch.arr, _vp), batch.n))
+
+
+def read_scalar_async(grid, field, pinned):
+    """Enqueue the D2H copy of a 0-D field into a pinned torch tensor (4 bytes)."""
+    _check(_lib.sg_read_scalar_async(grid.h, field, _vp(pinned.data_ptr())))
+
 
 def set_array_count(grid, array_id, count_tensor):
     """Attach a device int32 count (a torch tensor element) to a registered array."""
