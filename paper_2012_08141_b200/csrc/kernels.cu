@@ -368,6 +368,57 @@ __device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint3
   return ((uint64_t)(epoch & 0x3FFFFFFFu) << 34) | ((uint64_t)flag << 32) | v;
 }
 
+// Single-pass decoupled look-back (deterministic tile order), run by one full
+// warp: lane l inspects tiles j-l-32m (m < K), i.e. 32K predecessors per step,
+// until the nearest one carrying an inclusive prefix (flag 2).  Returns the
+// exclusive prefix of `tile`.  Descriptors of an older epoch read as "not yet
+// published".  The inclusive frontier advances at most 32K tiles per L2 round
+// trip, so many small tiles in flight need K > 1 (k_listgen_warp).
+template <int K = 1, int kSleepNs = 0>
+__device__ __forceinline__ uint32_t lb_lookback(const uint64_t* st, uint32_t tile, uint32_t epoch, int lane) {
+  uint32_t prefix = 0;
+  int64_t j = (int64_t)tile - 1;
+  while (j >= 0) {
+    uint64_t s[K];
+    uint32_t fl[K];
+#pragma unroll
+    for (int m = 0; m < K; m++) {
+      const int64_t q = j - lane - 32 * m;
+      s[m] = 0;
+      fl[m] = 2u;                             // beyond tile 0: acts as an inclusive zero
+      if (q >= 0) {
+        s[m] = ld_volatile64(&st[q]);
+        fl[m] = ((uint32_t)(s[m] >> 34) == epoch) ? (uint32_t)(s[m] >> 32) & 3u : 0u;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < K; m++) {
+      const int64_t q = j - lane - 32 * m;
+      while (fl[m] == 0u) {
+        if (kSleepNs) __nanosleep(kSleepNs);   // a spinning warp leaves its issue slots to the others
+        s[m] = ld_volatile64(&st[q]);
+        fl[m] = ((uint32_t)(s[m] >> 34) == epoch) ? (uint32_t)(s[m] >> 32) & 3u : 0u;
+      }
+    }
+    int stop = 32 * K;                        // order index l + 32m of the nearest inclusive
+#pragma unroll
+    for (int m = K - 1; m >= 0; m--) {
+      const uint32_t incl = __ballot_sync(0xffffffffu, fl[m] == 2u);
+      if (incl) stop = 32 * m + __ffs(incl) - 1;
+    }
+    uint32_t v = 0;
+#pragma unroll
+    for (int m = 0; m < K; m++)
+      if (lane + 32 * m <= stop && j - lane - 32 * m >= 0) v += (uint32_t)s[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (stop < 32 * K) break;
+    j -= 32 * K;
+  }
+  return prefix;
+}
+
 __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGArgs a) {
   __shared__ uint32_t s_warp[LG_TPB / 32];
   __shared__ uint32_t s_tile, s_base, s_total, s_epoch, s_run;
@@ -511,30 +562,8 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       if (threadIdx.x == 0) s_base = (uint32_t)a.out.status[tile];   // scanned by k_listgen_scan
     } else if (warp == 0) {
       const uint32_t total = s_total;
-      // single-pass decoupled look-back (deterministic tile order), one warp
-      // inspecting 32 predecessors per step
       uint64_t* st = a.out.status;
-      uint32_t prefix = 0;
-      int64_t j = (int64_t)tile - 1;
-      while (j >= 0) {
-        const int64_t q = j - lane;               // lane l inspects tile j-l
-        uint64_t s = 0;
-        uint32_t fl = 2u;                         // beyond tile 0: acts as an inclusive zero
-        if (q >= 0) {
-          do {
-            s = ld_volatile64(&st[q]);
-            fl = ((uint32_t)(s >> 34) == epoch) ? (uint32_t)(s >> 32) & 3u : 0u;
-          } while (fl == 0u);
-        }
-        const uint32_t incl = __ballot_sync(0xffffffffu, fl == 2u);
-        const int stop = incl ? __ffs(incl) - 1 : 31;   // nearest inclusive predecessor
-        uint32_t v = (lane <= stop && q >= 0) ? (uint32_t)s : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        prefix += v;
-        if (incl) break;
-        j -= 32;
-      }
+      const uint32_t prefix = lb_lookback(st, tile, epoch, lane);
       if (lane == 0) {
         if (tile != 0)
           atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, prefix + total));
@@ -641,6 +670,240 @@ __global__ void __launch_bounds__(1024) k_listgen_scan(const __grid_constant__ L
     if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
     *a.out.count = n;
     a.out.ctl[4] = 0u;   // the block table (if any) is stale until a struct-for rebuilds it
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-tile listgen for big bitmasked lists (LG-XL).  Same set as
+// k_listgen, in a deterministic order (chunk order, highest bit first within a
+// word, reading R2), but every warp is an independent tile of LGW_SUB
+// consecutive sub-tiles, each 32 lanes x LGW_WPL mask words:
+//   * no CTA barriers: a warp grabs its tile, loads all its words up front
+//     (two 16-byte loads per lane per sub-tile), scans the sub-tile counts
+//     with shuffles, publishes the tile aggregate and runs one decoupled
+//     look-back for the whole tile (one look-back per 1024 words: with
+//     thousands of warps in flight a per-256-word look-back walked ~5 x 32
+//     descriptors back, measured);
+//   * the set bits of a lane's 8 words are extracted in ONE loop whose trip
+//     count is the lane's own count (not one loop per word run to the
+//     per-word maximum over the warp); advancing to the next non-empty word
+//     is a single predicated shared load from a per-lane compacted copy;
+//   * the staged entries are stored at the destination's 16-byte phase, so
+//     the copy to the list is one 16-byte load + one 16-byte store per 4
+//     entries.
+// Sub-tiles denser than the staging buffer write their entries straight to
+// the list (correct, uncoalesced).
+// ---------------------------------------------------------------------------
+constexpr int LGW_MIN_HINT = 64;   // CTA tiles (2048 chunks) below which the CTA-tile kernel runs
+constexpr int LGW_TPB = 128, LGW_WARPS = LGW_TPB / 32, LGW_WPL = 8, LGW_SUBTILE = 32 * LGW_WPL, LGW_SUB = 4,
+              LGW_TILE = LGW_SUB * LGW_SUBTILE, LGW_CAP = 1024, LGW_LB = 1, LGW_SLEEP = 128;
+
+__device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {   // index of the highest set bit
+  uint32_t r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+
+// dst[0, cnt): the lane's set bits, word by word, highest bit first.  b/hi:
+// the first word and its entry base; the lane's other non-empty words are
+// compacted at rec[n * 32] = (word, entry base), so advancing to the next word
+// is always exactly one predicated 8-byte shared load.  (Two interleaved
+// streams per lane to overlap that load measured slower: 1.5x the
+// instructions, 350 vs 287 us on LG-XL.)
+__device__ __forceinline__ void lgw_extract(uint32_t* dst, uint32_t cnt, uint32_t b, uint32_t hi, const uint2* rec) {
+#pragma unroll 4   // (8 measured slower: 297 vs 287 us)
+  for (uint32_t i = 0; i < cnt; i++) {
+    if (b == 0u) {
+      const uint2 r = *rec;
+      rec += 32;
+      b = r.x;
+      hi = r.y;
+    }
+    const uint32_t t = bfind_u32(b);
+    dst[i] = hi + t;
+    b ^= 1u << t;
+  }
+}
+
+// Container and entry base of word-chunk ch0 (lcpp >= 3: the chunk's parent
+// entry also holds the next 7 chunks).
+__device__ __forceinline__ const uint32_t* lgw_decode(const LGArgs& a, uint64_t ch0, uint32_t& hi) {
+  const DLevel& S = a.T.lev[a.ls];
+  const DLevel& P = a.T.lev[a.lp < 0 ? 0 : a.lp];
+  const uint32_t p = (uint32_t)(ch0 >> a.lcpp), sub = (uint32_t)(ch0 & ((1u << a.lcpp) - 1u));
+  const uint32_t* cont = nullptr;
+  uint32_t c0 = 0, f0 = sub * 32u;
+  if (a.mode == 0) {
+    cont = a.T.seg[0].base;
+  } else {
+    const uint32_t e = a.pentries[p];
+    const uint32_t ps = e >> P.ln, pidx = e & ((1u << P.ln) - 1u);
+    if (a.mode == 1) {
+      c0 = ps; f0 = (pidx << a.lratio) + sub * 32u; cont = cont_ptr(a.T, S.seg, ps);
+    } else {
+      const uint32_t v = cont_ptr(a.T, P.seg, ps)[P.slot_off + pidx];
+      const bool ok = v != SG_SLOT_NULL && v != SG_SLOT_BUSY;
+      c0 = ok ? v - 1u : 0u; cont = ok ? cont_ptr(a.T, S.seg, c0) : nullptr;
+    }
+  }
+  hi = (c0 << S.ln) | f0;
+  return cont ? cont + S.mask_off + (f0 >> 5) : nullptr;
+}
+
+// Loads all LGW_SUB sub-tiles of warp tile `tile`: for sub-tile r this lane's
+// LGW_WPL consecutive word-chunks and their entry base.  When one parent entry
+// spans the whole tile (lcpp >= 10, e.g. LG-XL's 32^3 leaf containers) the
+// parent is decoded once per tile instead of once per sub-tile.
+__device__ __forceinline__ void lgw_load_tile(const LGArgs& a, uint64_t nchunks, uint32_t tile, int lane,
+                                              uint4 (&w)[LGW_SUB][2], uint32_t (&hi)[LGW_SUB]) {
+  const uint64_t t0 = (uint64_t)tile * LGW_TILE;
+  if ((1u << a.lcpp) >= (uint32_t)LGW_TILE && t0 + LGW_TILE <= nchunks) {
+    uint32_t h;
+    const uint32_t* m = lgw_decode(a, t0, h);   // same parent for every lane and sub-tile
+#pragma unroll
+    for (int r = 0; r < LGW_SUB; r++) {
+      const uint32_t off = (uint32_t)(r * LGW_SUBTILE) + (uint32_t)lane * LGW_WPL;
+      hi[r] = h + 32u * off;
+      if (m) {
+        const uint4* q = reinterpret_cast<const uint4*>(m + off);
+        w[r][0] = q[0];
+        w[r][1] = q[1];
+      } else {
+        w[r][0] = make_uint4(0u, 0u, 0u, 0u);
+        w[r][1] = w[r][0];
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < LGW_SUB; r++) {
+    const uint64_t ch0 = t0 + (uint32_t)(r * LGW_SUBTILE) + (uint32_t)lane * LGW_WPL;
+    hi[r] = 0;
+    w[r][0] = make_uint4(0u, 0u, 0u, 0u);
+    w[r][1] = w[r][0];
+    if (ch0 < nchunks) {
+      const uint32_t* m = lgw_decode(a, ch0, hi[r]);
+      if (m) {
+        const uint4* q = reinterpret_cast<const uint4*>(m);
+        w[r][0] = q[0];
+        w[r][1] = q[1];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t popc8(const uint4& w0, const uint4& w1) {
+  return __popc(w0.x) + __popc(w0.y) + __popc(w0.z) + __popc(w0.w) +
+         __popc(w1.x) + __popc(w1.y) + __popc(w1.z) + __popc(w1.w);
+}
+
+__global__ void __launch_bounds__(LGW_TPB, 8) k_listgen_warp(const __grid_constant__ LGArgs a) {
+  __shared__ __align__(16) uint32_t s_out[LGW_WARPS][LGW_CAP + 4];
+  __shared__ uint2 s_rec[LGW_WARPS][LGW_WPL * 32];   // compacted non-empty words 1..7 per lane
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t epoch = ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu;
+  const uint32_t nparent = a.mode == 0 ? 1u : *a.pcount;
+  const uint64_t nchunks = (uint64_t)nparent << a.lcpp;
+  const uint32_t ntiles = (uint32_t)((nchunks + LGW_TILE - 1) / LGW_TILE);
+  uint2* rec = s_rec[warp];
+  uint32_t* so = s_out[warp];
+  uint64_t* st = a.out.status;
+  while (true) {
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(&a.out.ctl[0], 1u);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= ntiles) break;
+    uint4 w[LGW_SUB][2];
+    uint32_t hi[LGW_SUB], cnt[LGW_SUB], inc[LGW_SUB], tot[LGW_SUB];
+    lgw_load_tile(a, nchunks, tile, lane, w, hi);
+    uint32_t agg = 0;
+#pragma unroll
+    for (int r = 0; r < LGW_SUB; r++) {
+      cnt[r] = popc8(w[r][0], w[r][1]);
+      inc[r] = cnt[r];
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int r = 0; r < LGW_SUB; r++) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc[r], o);
+        if (lane >= o) inc[r] += t;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < LGW_SUB; r++) {
+      tot[r] = __shfl_sync(0xffffffffu, inc[r], 31);
+      agg += tot[r];
+    }
+    if (lane == 0)
+      atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, agg));
+    uint32_t base = lb_lookback<LGW_LB, LGW_SLEEP>(st, tile, epoch, lane);
+    if (lane == 0) {
+      if (tile != 0)
+        atomicExch((unsigned long long*)&st[tile], (unsigned long long)lb_pack(epoch, 2u, base + agg));
+      if (tile == ntiles - 1) {
+        uint32_t n = base + agg;
+        if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
+        *a.out.count = n;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < LGW_SUB; r++) {
+      const uint32_t total = tot[r];
+      if (total != 0u) {
+        // non-empty words 1..7 of the sub-tile, compacted per lane (word 0
+        // starts in a register)
+        {
+          const uint32_t wv[7] = {w[r][0].y, w[r][0].z, w[r][0].w, w[r][1].x, w[r][1].y, w[r][1].z, w[r][1].w};
+          uint32_t n = 0;
+#pragma unroll
+          for (int k = 0; k < 7; k++) {
+            if (wv[k]) { rec[n * 32u + lane] = make_uint2(wv[k], hi[r] + 32u * (k + 1)); n++; }
+          }
+        }
+        const uint32_t my0 = inc[r] - cnt[r];
+        __syncwarp();
+        if (total <= (uint32_t)LGW_CAP) {
+          const uint32_t shift = base & 3u;
+          lgw_extract(so + shift + my0, cnt[r], w[r][0].x, hi[r], rec + lane);
+          __syncwarp();
+          // [base, base + total) <- so[shift, shift + total): 16-byte groups at
+          // the destination's phase; the partial head / tail groups element-wise
+          const uint32_t end = min(base + total, a.out.capacity);
+          const uint32_t ga = (base + 3u) & ~3u, gb = end & ~3u;   // full groups: [ga, gb)
+          uint32_t* ent = a.out.entries;
+          if (ga < gb) {
+            uint4* dst = reinterpret_cast<uint4*>(ent + ga);
+            const uint4* src = reinterpret_cast<const uint4*>(so + shift + (ga - base));
+            const uint32_t ng = (gb - ga) >> 2;
+            for (uint32_t j = lane; j < ng; j += 32u) dst[j] = src[j];
+            if (lane < ga - base) ent[base + lane] = so[shift + lane];            // head (< 4)
+            if (lane < end - gb) ent[gb + lane] = so[shift + (gb - base) + lane];  // tail (< 4)
+          } else if (lane < end - min(base, end)) {
+            ent[base + lane] = so[shift + lane];                                   // < 8 entries
+          }
+        } else {
+          // dense sub-tile: straight to the list (entries past the capacity are
+          // dropped; the overflow is reported with the count)
+          const uint32_t o = base + my0, cap = a.out.capacity;
+          lgw_extract(a.out.entries + o, o >= cap ? 0u : min(cnt[r], cap - o), w[r][0].x, hi[r], rec + lane);
+        }
+        __syncwarp();
+        base += total;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.out.ctl[1], 1u) == gridDim.x - 1) {
+      if (ntiles == 0) *a.out.count = 0;
+      a.out.ctl[0] = 0;
+      a.out.ctl[1] = 0;
+      a.out.ctl[2] = a.out.ctl[2] + 1u;
+      a.out.ctl[4] = 0u;   // the block table (if any) is stale until a struct-for rebuilds it
+      __threadfence();
+    }
   }
 }
 
@@ -900,6 +1163,23 @@ int launch_listgen(const DevCtx& c, const DTree& t, int, int level, int parent_l
     k_listgen_scan<<<1, 1024, 0, st>>>(a);
     a.pass = 2;
     k_listgen<<<resident, LG_TPB, 0, st>>>(a);
+    return check_launch();
+  }
+  // big bitmasked lists: warp tiles (k_listgen_warp).  SG_LG_WARP=0 forces the
+  // CTA-tile kernel, =1 the warp-tile kernel wherever it applies.
+  static const int lg_warp_env = getenv("SG_LG_WARP") ? atoi(getenv("SG_LG_WARP")) : -1;
+  if (a.fast8 && (lg_warp_env == 1 || (lg_warp_env != 0 && grid_hint >= LGW_MIN_HINT))) {
+    static int wres = 0;
+    if (!wres) {
+      int per_sm = 0;
+      cudaFuncSetAttribute(k_listgen_warp, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_listgen_warp, LGW_TPB, 0);
+      wres = num_sms() * std::max(1, per_sm);
+    }
+    // grid_hint counts 1024-chunk units of the parent list's capacity; tiles
+    // are LGW_TILE chunks; a launch never exceeds one resident wave
+    const int64_t wt = ((int64_t)grid_hint * 1024 / LGW_TILE + LGW_WARPS - 1) / LGW_WARPS;
+    k_listgen_warp<<<(int)std::max<int64_t>(1, std::min<int64_t>(wt, wres)), LGW_TPB, 0, (cudaStream_t)stream>>>(a);
     return check_launch();
   }
   grid = max(1, min(grid, resident));

@@ -342,7 +342,7 @@ static sg_status alloc_list(sg_grid* g, int tid, int k) {
   else if (T.lev[pk].seg == T.lev[k].seg) lratio = T.lev[k].ln - T.lev[pk].ln;
   else lratio = T.lev[k].ln;
   uint64_t cpp = lratio > 5 ? (1ull << (lratio - 5)) : 1;
-  uint64_t max_tiles = (pcap * cpp + 1023) / 1024 + 1;
+  uint64_t max_tiles = (pcap * cpp + 255) / 256 + 1;   // look-back descriptors: tiles of >= 256 chunks
   Ls.capacity = (uint32_t)cap;
   Ls.max_tiles = (uint32_t)std::min<uint64_t>(max_tiles, 0xFFFFFFFFull);
   if (k == T.driving) {

@@ -86,19 +86,23 @@ def lg_xl(reps=15, p_ptr=0.25, p_bit=0.10, seed=0):
         total += co.shape[0]
     g.sync()
     flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    # per-repetition device time (events around the flush, L2 flushed before
-    # each); the median is reported -- single launches of this kernel vary
+    # per-launch device time: the library's CUDA events around the listgen
+    # kernel itself on the grid's stream (sg_set_profiling), L2 flushed before
+    # each repetition; the median is reported -- single launches vary
     times = []
-    stream = torch.cuda.current_stream()
+    if os.environ.get("SG_PROFILE_FROM_HERE"):
+        torch.cuda.profiler.start()   # ncu --profile-from-start off: skip the setup launches
+    sg.set_profiling(g, True)
+    key = 200 + lv[-1]
     for _ in range(reps):
         flush_buf.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sg.profile_read(g)            # drains (and clears) earlier events
         g.listgen(lv[-1])
-        e0.record(stream)
         g.flush("all")
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
+        ms1, n1 = sg.profile_read(g).get(key, (0.0, 0))
+        assert n1 == 1, (ms1, n1)
+        times.append(ms1)
+    sg.set_profiling(g, False)
     g.sync()
     times.sort()
     ms, n = times[len(times) // 2] * reps, reps
