@@ -6,7 +6,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # C2 JACOBI with warm L2 (the timed step's condition after the first iteration)
 timeout 900 ncu --set full --cache-control none --clock-control none --import-source on -k regex:k_jacobi8 -s 60 -c 1 -o gpurun_out/prof/c2_jacobi python scripts/prof_c2.py 3 > /dev/null 2>&1; echo c2 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_jacobi8 -s 6 -c 1 -o gpurun_out/prof/jac_xl python scripts/xl_bench.py jac > /dev/null 2>&1; echo jacxl rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_listgen -s 1 -c 1 -o gpurun_out/prof/lg_xl python scripts/xl_bench.py lg > /dev/null 2>&1; echo lgxl rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_listgen -s 1 -c 1 -o gpurun_out/prof/lg_xl env SG_PROFILE_FROM_HERE=1 python scripts/xl_bench.py lg > /dev/null 2>&1; echo lgxl rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_p2g_bin|k_g2p_bin" -s 2 -c 2 -o gpurun_out/prof/c3_mpm python scripts/prof_c3.py 1 > /dev/null 2>&1; echo c3 rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_g2p_adj_bin|k_p2g_adj_bin" -s 4 -c 2 -o gpurun_out/prof/c4_adj python scripts/prof_c4.py 4 1 > /dev/null 2>&1; echo c4 rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_c4.csv python scripts/prof_c4.py 8 2 > /dev/null 2>&1; echo c4 launches rc=$?
