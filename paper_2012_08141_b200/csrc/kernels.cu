@@ -907,6 +907,103 @@ __global__ void __launch_bounds__(LGW_TPB, 8) k_listgen_warp(const __grid_consta
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-list listgen (parent capacity x chunks <= 1024 words: the configs'
+// lists, SURVEY 8d.4 "latency-bound").  One CTA of 1024 threads; every thread
+// owns ONE unit per pass -- one child slot of a pointer level (a coalesced
+// 4-byte load) or one 32-child mask word of a bitmasked level -- so a pass is a
+// single round of independent loads (parent entry -> slot -> word) followed by
+// one block scan and the writes.  The CTA-tile kernel gave each thread 8 chunks
+// (a pointer-level chunk being 32 sequential slot loads) and walked its tiles
+// in series: 12-16 us per config listgen.  Entries in unit order, highest bit
+// first within a word (reading R2); count, capacity check and the table flag as
+// in k_listgen.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_listgen_small(const __grid_constant__ LGArgs a) {
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  const DLevel& S = a.T.lev[a.ls];
+  const bool ptr = S.kind != SG_BITMASKED;
+  const uint32_t nparent = a.mode == 0 ? 1u : *a.pcount;
+  const uint64_t nchunks = (uint64_t)nparent << a.lcpp;
+  const uint32_t lnb = ptr ? (uint32_t)__ffs(a.nbits) - 1u : 0u;   // units per chunk = 2^lnb
+  const uint64_t nunits = nchunks << lnb;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lnS = S.ln;
+  uint32_t carry = 0;
+  for (uint64_t u0 = 0; u0 < nunits; u0 += 1024) {
+    const uint64_t u = u0 + threadIdx.x;
+    uint32_t bits = 0, hi = 0;
+    if (u < nunits) {
+      const uint64_t chunk = u >> lnb;
+      const uint32_t k = (uint32_t)(u & ((1u << lnb) - 1u));
+      const uint32_t p = (uint32_t)(chunk >> a.lcpp), sub = (uint32_t)(chunk & ((1u << a.lcpp) - 1u));
+      const uint32_t* cont = nullptr;
+      uint32_t cslot = 0, first = sub * 32u;
+      if (a.mode == 0) {
+        cont = a.T.seg[0].base;
+      } else {
+        const DLevel& P = a.T.lev[a.lp];
+        const uint32_t e = a.pentries[p];
+        const uint32_t ps = e >> P.ln, pidx = e & ((1u << P.ln) - 1u);
+        if (a.mode == 1) {
+          cslot = ps; first = (pidx << a.lratio) + sub * 32u; cont = cont_ptr(a.T, S.seg, ps);
+        } else {
+          const uint32_t v = cont_ptr(a.T, P.seg, ps)[P.slot_off + pidx];
+          if (v != SG_SLOT_NULL && v != SG_SLOT_BUSY) { cslot = v - 1u; cont = cont_ptr(a.T, S.seg, cslot); }
+        }
+      }
+      if (cont) {
+        if (ptr) {
+          bits = cont[S.slot_off + first + k] != SG_SLOT_NULL ? 1u : 0u;
+          first += k;
+        } else {
+          const uint32_t wd = cont[S.mask_off + (first >> 5)];
+          bits = a.nbits == 32 ? wd : ((wd >> (first & 31u)) & ((1u << a.nbits) - 1u));
+        }
+      }
+      hi = (cslot << lnS) | first;
+    }
+    const uint32_t cnt = __popc(bits);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t v = s_w[lane];
+      uint32_t vi = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, vi, o);
+        if (lane >= o) vi += t;
+      }
+      s_w[lane] = vi - v;
+      if (lane == 31) s_carry = vi;
+    }
+    __syncthreads();
+    uint32_t o = carry + s_w[w] + inc - cnt;
+    const uint32_t cap = a.out.capacity;
+    while (bits) {
+      const uint32_t t = 31u - __clz(bits);
+      bits ^= 1u << t;
+      if (o < cap) a.out.entries[o] = hi + t;
+      o++;
+    }
+    carry += s_carry;
+    __syncthreads();   // s_w / s_carry reused by the next pass
+  }
+  if (threadIdx.x == 0) {
+    uint32_t n = carry;
+    if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
+    *a.out.count = n;
+    a.out.ctl[4] = 0u;   // the block table (if any) is stale until a struct-for rebuilds it
+  }
+}
+
 __global__ void k_clear_list(uint32_t* count) { *count = 0; }
 
 #include "mpm_ops.cuh"
@@ -1183,6 +1280,13 @@ int launch_listgen(const DevCtx& c, const DTree& t, int, int level, int parent_l
     return check_launch();
   }
   grid = max(1, min(grid, resident));
+  // small lists (one CTA tile of parent capacity): k_listgen_small;
+  // SG_LG_SMALL=0 keeps the single-CTA path of k_listgen (measurement switch)
+  static const bool lg_small = !(getenv("SG_LG_SMALL") && atoi(getenv("SG_LG_SMALL")) == 0);
+  if (grid == 1 && lg_small) {
+    k_listgen_small<<<1, 1024, 0, (cudaStream_t)stream>>>(a);
+    return check_launch();
+  }
   k_listgen<<<grid, LG_TPB, 0, (cudaStream_t)stream>>>(a);
   return check_launch();
 }
