@@ -104,3 +104,38 @@ def test_repeat_listgen_is_stable_across_epochs():
         first = first or got
         assert got == first
     assert len(first) == len({tuple(c) for c in cells.tolist()})
+
+
+def test_lg_xl_full_size_exact_set():
+    """LG-XL at the size bench.py times (2048^3 bound, pointer(64^3) -> bitmasked(32^3),
+    25% of the containers, 10% of their bits): the list must be exactly the set of
+    activated cells -- listgen's definition with no
+    deactivation in between -- compared as sorted 64-bit cell keys on the device."""
+    L = W.Layout()
+    lv = L.chain([("pointer", (64,) * 3), ("bitmasked", (32,) * 3)], [("m", "f32")])
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    n_ptr = 64 ** 3
+    ptr_on = torch.randperm(n_ptr, device="cuda", generator=gen)[: n_ptr // 4]
+    n_act = ptr_on.numel()
+    cells_per = int(32768 * 0.10)
+    g = sg.Grid(L.desc(), pool_capacity=n_act, list_capacity=int(n_act * cells_per * 1.05) + 1024)
+    keys = []
+    for s in range(0, n_act, 4096):
+        pc = ptr_on[s:s + 4096]
+        px, py, pz = pc // 4096, (pc // 64) % 64, pc % 64
+        loc = torch.randint(0, 32768, (pc.numel(), cells_per), device="cuda", generator=gen)
+        co = torch.stack([px[:, None] * 32 + loc // 1024, py[:, None] * 32 + (loc // 32) % 32,
+                          pz[:, None] * 32 + loc % 32], -1).reshape(-1, 3).to(torch.int32).contiguous()
+        g.activate(0, co)
+        g.flush("all")
+        c64 = co.to(torch.int64)
+        keys.append((c64[:, 0] << 22) | (c64[:, 1] << 11) | c64[:, 2])
+    g.sync()
+    want = torch.unique(torch.cat(keys))
+    del keys
+    g.listgen(lv[-1])
+    g.flush("all")
+    got = torch.as_tensor(g.list(lv[-1])).cuda().to(torch.int64)
+    assert got.shape[0] == want.numel()
+    gk = torch.sort((got[:, 0] << 22) | (got[:, 1] << 11) | got[:, 2]).values
+    assert torch.equal(gk, want)
