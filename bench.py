@@ -625,7 +625,7 @@ def main():
             import xl_bench
             extra = {}
             for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3), ("c4", measure_c4), ("mg", measure_mg), ("mgpcg", measure_mgpcg),
-                             ("jac_xl", xl_bench.jac_xl), ("lg_xl", xl_bench.lg_xl)):
+                             ("jac_xl", xl_bench.jac_xl), ("lg_xl", xl_bench.lg_xl), ("act_xl", xl_bench.act_xl)):
                 try:
                     extra[name] = fn()
                 except Exception as e:  # keep the main line even if an extra fails

@@ -295,8 +295,16 @@ __device__ uint32_t* activate_walk_agg(const DevCtx& C, const DTree& T, const in
       const uint32_t b = 1u << (idx & 31);
       const unsigned am = __activemask();
       const unsigned peers = __match_any_sync(am, (unsigned long long)w);
-      const uint32_t bits = __reduce_or_sync(peers, b);
-      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && (ld_volatile(w) & bits) != bits) atomicOr(w, bits);
+      if (peers == (1u << (threadIdx.x & 31))) {
+        // alone on its word (random coordinates): no aggregation.  The OR
+        // reduction over a partial mask is a loop over the warp's distinct
+        // groups (REDUX per group), which made a random-coordinate warp pay 32
+        // reductions (ACT-XL: 7.3% of instructions each on the loop's lines)
+        if (!(ld_volatile(w) & b)) atomicOr(w, b);
+      } else {
+        const uint32_t bits = __reduce_or_sync(peers, b);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && (ld_volatile(w) & bits) != bits) atomicOr(w, bits);
+      }
     } else if (L.kind == SG_POINTER) {
       int32_t s = acquire_child(C, T, L, cont, idx, c, task);
       if (s < 0) return nullptr;

@@ -119,9 +119,56 @@ def lg_xl(reps=15, p_ptr=0.25, p_bit=0.10, seed=0):
             "min_us": times[0] * 1e3, "max_us": times[-1] * 1e3}
 
 
+def act_xl(p_ptr=0.25, p_bit=0.10, seed=0):
+    """ACT-XL: the LG-XL activation (214.7M random cell coordinates, 25% of the
+    64^3 pointer cells, 10% of each 32^3 container) as ONE sg_activate launch,
+    first touch into a fresh grid (pointer CAS + pool pops + atomicOr), then the
+    same buffer again (every bit already set: the read-before-atomic path).
+    Device time of the k_activate launch from the library's events."""
+    L = W.Layout()
+    lv = L.chain([("pointer", (64,) * 3), ("bitmasked", (32,) * 3)], [("m", "f32")])
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    n_ptr = 64 ** 3
+    ptr_on = torch.randperm(n_ptr, device="cuda", generator=gen)[: int(n_ptr * p_ptr)]
+    n_act = ptr_on.numel()
+    cells_per = int(32768 * p_bit)
+    px, py, pz = ptr_on // 4096, (ptr_on // 64) % 64, ptr_on % 64
+    loc = torch.randint(0, 32768, (n_act, cells_per), device="cuda", generator=gen)
+    co = torch.stack([px[:, None] * 32 + loc // 1024, py[:, None] * 32 + (loc // 32) % 32,
+                      pz[:, None] * 32 + loc % 32], -1).reshape(-1, 3).to(torch.int32).contiguous()
+    del loc
+    # 10 mask-word lines and the pointer slot per request at most; order of the
+    # requests is random (no two lanes of a warp share a container, typically)
+    g = sg.Grid(L.desc(), pool_capacity=n_act, list_capacity=int(n_act * cells_per * 1.05) + 1024)
+    # one request first: the pools are allocated and zeroed by the first flush,
+    # outside the timed launches
+    g.activate(0, co[:1].clone())
+    g.flush(0)
+    g.sync()
+    sg.set_profiling(g, True)
+    out = {"variant": "ACT-XL", "requests": int(co.shape[0]), "containers": n_act}
+    for name in ("first_touch", "again"):
+        sg.profile_read(g)
+        g.activate(0, co)
+        g.flush(0)
+        ms, n = sg.profile_read(g).get(0, (0.0, 0))
+        assert n == 1, (ms, n)
+        out[name] = {"us": ms * 1e3, "requests_per_s": co.shape[0] / (ms / 1e3),
+                     "coord_GBps": co.numel() * 4 / (ms / 1e3) / 1e9}
+    import ctypes
+    cnt = ctypes.c_int64()
+    g.listgen(lv[-1])
+    g.flush("all")
+    sg._check(sg._lib.sg_export_list(g.h, lv[-1], None, 0, ctypes.byref(cnt)))
+    out["active_cells"] = cnt.value
+    return out
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["jac", "lg"]
     if "jac" in which:
         print(json.dumps(jac_xl()), flush=True)
     if "lg" in which:
         print(json.dumps(lg_xl()), flush=True)
+    if "act" in which:
+        print(json.dumps(act_xl()), flush=True)
