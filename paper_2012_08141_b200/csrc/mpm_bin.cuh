@@ -302,16 +302,22 @@ __device__ __forceinline__ void stage_tile(const DTree& T, const DOp& op, int sl
 // Warp-private scatter tiles + per-warp particle records.
 //   rec: w[3][3] (9), fx (3), coefficient vector q (12), base offset in the tile (as float bits)
 constexpr int MB_REC = 25;
+// Scatter tiles use padded strides (node (i, j, k) at i*43 + j*7 + k): the 27
+// stencil offsets a*43 + b*7 + c (a, b, c < 3) fall in 27 distinct banks, so a
+// warp's 27 lanes update their nodes without shared-memory bank conflicts
+// (the dense 6x6x6 layout put 2 lanes on one bank for 9 of the offsets).
+constexpr int MB_SI = 43, MB_SJ = 7, MB_TP = 6 * MB_SI;
+__device__ __forceinline__ int tile_pad(int q) { return (q / 36) * MB_SI + ((q / 6) % 6) * MB_SJ + q % 6; }
 struct MbScatter {
-  float tile[MB_WARPS][4][MB_NODES];
+  float tile[MB_WARPS][4][MB_TP];
   float rec[MB_WARPS][MB_REC][32];
   uint32_t need;
   uint32_t off[8];
 };
 
 __device__ __forceinline__ void zero_tiles(MbScatter& S, int nf) {
-  for (int k = threadIdx.x; k < MB_WARPS * 4 * MB_NODES; k += MB_TPB) {
-    const int f = (k / MB_NODES) & 3;
+  for (int k = threadIdx.x; k < MB_WARPS * 4 * MB_TP; k += MB_TPB) {
+    const int f = (k / MB_TP) & 3;
     if (f < nf) (&S.tile[0][0][0])[k] = 0.0f;
   }
 }
@@ -326,7 +332,7 @@ __device__ __forceinline__ void put_record(MbScatter& S, const MpmKernel& k, con
   for (int a = 0; a < 3; a++) S.rec[w][9 + a][l] = k.fx[a];
 #pragma unroll
   for (int j = 0; j < 12; j++) S.rec[w][12 + j][l] = q[j];
-  S.rec[w][24][l] = __int_as_float((r[0] * 6 + r[1]) * 6 + r[2]);
+  S.rec[w][24][l] = __int_as_float(r[0] * MB_SI + r[1] * MB_SJ + r[2]);
 }
 
 // Warp walk over its `m` records: lane l < 27 adds, for node l = (a, b, c) of
@@ -336,7 +342,7 @@ __device__ __forceinline__ void warp_scatter(MbScatter& S, int m, float dx, floa
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l >= 27) return;
   const int a = l / 9, b = (l / 3) % 3, c = l % 3;
-  const int dq = (a * 6 + b) * 6 + c;
+  const int dq = a * MB_SI + b * MB_SJ + c;
   float* t0 = S.tile[w][0];
   float* t1 = S.tile[w][1];
   float* t2 = S.tile[w][2];
@@ -355,8 +361,9 @@ __device__ __forceinline__ void warp_scatter(MbScatter& S, int m, float dx, floa
 
 __device__ __forceinline__ float tile_sum(const MbScatter& S, int f, int q) {
   float v = 0.0f;
+  const int pq = tile_pad(q);
 #pragma unroll
-  for (int w = 0; w < MB_WARPS; w++) v += S.tile[w][f][q];
+  for (int w = 0; w < MB_WARPS; w++) v += S.tile[w][f][pq];
   return v;
 }
 
