@@ -526,7 +526,7 @@ struct MbAdj {
   uint32_t offg[8];
 };
 
-__global__ void __launch_bounds__(MB_TPB, 2) k_g2p_adj_bin(const __grid_constant__ MpmBinArgs A) {
+__global__ void __launch_bounds__(MB_TPB, 3) k_g2p_adj_bin(const __grid_constant__ MpmBinArgs A) {
   __shared__ MbAdj Z;
   MbScatter& S = Z.S;
   const DevCtx& C = A.C;
