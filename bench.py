@@ -393,7 +393,7 @@ def measure_c3(steps=20, warmup=3, n=1_000_000):
         if k in names:
             per[names[k]] = t / max(c, 1) * 1e3
     return {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
-            "avg_us_per_launch_kind": per, "particles": n}
+            "binning_kernels_per_step": st["aux_kernels"], "avg_us_per_launch_kind": per, "particles": n}
 
 
 def _enqueue_calls(g, sg, calls):
@@ -436,6 +436,7 @@ def measure_c4(steps=5, warmup=3, n=100_000, T=64):
             per[names[k]] = {"us": round(t / max(c, 1) * 1e3, 2), "launches": c / 2}
     loss = float(g.field(prog["layout"].fields["loss"]).reshape(-1)[0])
     return {"iterations_per_s": 1000.0 / ms, "ms_per_iteration": ms, "launches_per_iteration": st["launches"],
+            "binning_kernels_per_iteration": st["aux_kernels"],
             "tasks_lowered": st["tasks_lowered"], "dead_removed": st["dead_removed"],
             "avg_us_per_launch_kind": per, "particles": n, "substeps": T, "loss": loss}
 
@@ -513,7 +514,7 @@ def run_c5(args, rank, world, local):
         a.record(stream)
         for _ in range(args.steps):
             st = sim.step()
-            launches += sum(s["launches"] for s in st)
+            launches += sum(s["launches"] + s["aux_kernels"] for s in st)
         b.record(stream)
         torch.cuda.synchronize()
     ms = a.elapsed_time(b)

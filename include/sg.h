@@ -226,7 +226,7 @@ enum {
 
 typedef struct {
   int64_t tasks_lowered;        /* tasks in the eager lowering of this flush */
-  int64_t launches;             /* kernels launched by this flush */
+  int64_t launches;             /* task launches of this flush (one per launch group) */
   int64_t listgen_launched;
   int64_t clear_list_launched;
   int64_t listgens_removed;
@@ -238,6 +238,9 @@ typedef struct {
   double plan_us;               /* host planning time of this flush */
   int64_t tasks_chained;        /* SG_PASS_CHAIN: struct-for groups merged into chains */
   int64_t launches_chained;     /* SG_PASS_CHAIN: cooperative chain launches */
+  int64_t aux_kernels;          /* extra kernels inside task launches: particle binning for the
+                                   binned MPM ops (5 per binning; a binning is reused while the
+                                   positions and the bin geometry are unchanged) */
 } sg_stats;
 
 /* Optimize and launch the queue.  passes = 0 launches one kernel per lowered

@@ -57,6 +57,7 @@ struct sg_grid {
   cudaStream_t user_stream = nullptr;
   cudaStream_t cap_stream = nullptr;
   std::unordered_map<uint64_t, cudaGraphExec_t> gexec;
+  std::unordered_map<uint64_t, int64_t> gaux;   // aux kernels captured in each plan's graph
   std::unordered_map<uint64_t, uint64_t> gsig;   // launch-argument signature of each exec's last capture
   std::unordered_map<uint64_t, int> plan_runs;
   int num_sms = 148;
@@ -72,7 +73,8 @@ struct sg_grid {
   int64_t bin_cap = 0;
   uint32_t bin_keys_cap = 0;
   bool bin_valid = false;
-  int bin_xarr = -1, bin_tree = -1;
+  int bin_xarr = -1, bin_nb[3] = {0, 0, 0};
+  float bin_inv_dx = 0.0f;
   uint64_t bin_epoch = 0;
   int64_t bin_n = 0;
   const int32_t* bin_dcount = nullptr;
@@ -573,8 +575,12 @@ static bool tree_lb2(const DTree& t) {
 }
 
 // Bins of the particles in position array xa over tree `tree` (4^3 leaf
-// blocks); rebuilt unless the cache holds the same (array, epoch, tree, range).
-static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t n, const int32_t* dcount) {
+// blocks); rebuilt unless the cache holds the same (array, epoch, range) over
+// the same bin geometry (blocks per axis, cell size).  The geometry, not the
+// tree id: C4's adjoint tree has the grid tree's shape, so P2G, G2P_ADJ and
+// P2G_ADJ of one substep share one binning of its positions.
+static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t n, const int32_t* dcount,
+                             int64_t& aux) {
   const DTree& T = g->dtrees[tree];
   const DLevel& leaf = T.lev[T.nlev - 1];
   int nb[3];
@@ -604,13 +610,17 @@ static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t
   }
   g->bins.nkeys = nkeys;
   for (int a = 0; a < 3; a++) g->bins.nb[a] = nb[a];
-  if (g->bin_valid && g->bin_xarr == xa && g->bin_epoch == g->arr_epoch[xa] && g->bin_tree == tree &&
-      g->bin_n == n && g->bin_dcount == dcount)
+  if (g->bin_valid && g->bin_xarr == xa && g->bin_epoch == g->arr_epoch[xa] && g->bin_nb[0] == nb[0] &&
+      g->bin_nb[1] == nb[1] && g->bin_nb[2] == nb[2] && g->bin_inv_dx == inv_dx && g->bin_n == n &&
+      g->bin_dcount == dcount)
     return SG_OK;
   if (launch_bin(g->bins, (const float*)g->arrays[xa].ptr, g->arrays[xa].n, n, dcount, inv_dx, g->stream))
     return fail(SG_ERR_CUDA, std::string("binning launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  aux += BIN_KERNELS;
   g->bin_valid = true;
-  g->bin_xarr = xa; g->bin_epoch = g->arr_epoch[xa]; g->bin_tree = tree; g->bin_n = n; g->bin_dcount = dcount;
+  g->bin_xarr = xa; g->bin_epoch = g->arr_epoch[xa]; g->bin_n = n; g->bin_dcount = dcount;
+  for (int a = 0; a < 3; a++) g->bin_nb[a] = nb[a];
+  g->bin_inv_dx = inv_dx;
   return SG_OK;
 }
 
@@ -734,7 +744,8 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       const DBins* bp = nullptr;
       const bool mpm_op = tk.op == SG_OP_P2G || tk.op == SG_OP_G2P || tk.op == SG_OP_G2P_ADJ || tk.op == SG_OP_P2G_ADJ;
       if (n > 0 && nops == 1 && mpm_op && gt && !g->no_bin && tree_lb2(*gt) && (!gt2 || tree_lb2(*gt2))) {
-        if ((rc = ensure_bins(g, g->L.field_tree[tk.fields[0]], tk.arrays[0], ops[0].p[1], n, dcount))) return rc;
+        if ((rc = ensure_bins(g, g->L.field_tree[tk.fields[0]], tk.arrays[0], ops[0].p[1], n, dcount, st.aux_kernels)))
+          return rc;
         bp = &g->bins;
       }
       rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt, gt2, bp);
@@ -840,6 +851,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         if (t.type == TT_CLEAR_LIST) st.clear_list_launched++;
         if (plan->phase_ends[gi].size() > 1) st.launches_chained++;
       }
+      st.aux_kernels = g->gaux[key];
       sg_status rc2 = SG_OK;
       if (cudaGraphLaunch(ex->second, g->stream) != cudaSuccess) rc2 = fail(SG_ERR_CUDA, "graph launch failed");
       g->eager.clear();
@@ -906,7 +918,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         rc = fail(SG_ERR_CUDA, "graph instantiation failed");
       }
       if (ex && cudaGraphLaunch(ex, g->stream) != cudaSuccess) rc = fail(SG_ERR_CUDA, "graph launch failed");
-      if (ex) g->gsig[key] = sig;
+      if (ex) { g->gsig[key] = sig; g->gaux[key] = st.aux_kernels; }
       cudaGraphDestroy(graph);
     }
   }

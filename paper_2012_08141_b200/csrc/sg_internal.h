@@ -174,6 +174,7 @@ int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DO
                      const DBins* bins);
 // Bin the particles of position array x (3 comps, component stride xs) by the
 // leaf blocks of a tree with 4^3 blocks (nb blocks per axis).
+constexpr int BIN_KERNELS = 5;   // kernels one launch_bin issues (count, tiles, top, apply, scatter)
 int launch_bin(const DBins& b, const float* x, int64_t xs, int64_t n, const int32_t* dcount, float inv_dx,
                void* stream);
 uint32_t bin_ntiles(uint32_t nkeys);

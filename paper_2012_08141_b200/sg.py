@@ -66,7 +66,8 @@ class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "tasks_lowered", "launches", "listgen_launched", "clear_list_launched", "listgens_removed",
         "demotions", "tasks_fused", "dead_removed", "plan_cache_hits", "plan_cache_misses")] + [
-        ("plan_us", ctypes.c_double), ("tasks_chained", ctypes.c_int64), ("launches_chained", ctypes.c_int64)]
+        ("plan_us", ctypes.c_double), ("tasks_chained", ctypes.c_int64), ("launches_chained", ctypes.c_int64),
+        ("aux_kernels", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
