@@ -337,7 +337,6 @@ struct LGArgs {
   const uint32_t* pcount;
   DList out;
   int task;
-  int pass;             // 0: single pass (look-back, or one CTA); 1: count per tile; 2: write from scanned tile prefixes
 };
 
 constexpr int LG_TPB = 256, LG_CPT = 8, LG_TILE = LG_TPB * LG_CPT, LG_STAGE = 8192;
@@ -435,9 +434,8 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
   // solo: one CTA walks the tiles in order with a running prefix -- no tile
   // counter, no look-back, no finisher atomics (small lists are a chain of
   // dependent memory round trips, so every one removed counts)
-  const bool solo = gridDim.x == 1 && a.pass == 0;
-  const bool twopass = a.pass != 0;   // large lists: tile counts, a separate scan, then the writes
-  uint32_t solo_tile = 0, static_iter = 0;
+  const bool solo = gridDim.x == 1;
+  uint32_t solo_tile = 0;
   if (threadIdx.x == 0) { s_epoch = solo ? 0u : ld_volatile(&a.out.ctl[2]) & 0x3FFFFFFFu; s_run = 0u; }
   uint32_t nparent = a.mode == 0 ? 1u : *a.pcount;
   uint64_t nchunks = (uint64_t)nparent << a.lcpp;
@@ -449,8 +447,6 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
     uint32_t tile;
     if (solo) {
       tile = solo_tile++;
-    } else if (twopass) {
-      tile = blockIdx.x + (static_iter++) * gridDim.x;
     } else {
       if (threadIdx.x == 0) s_tile = atomicAdd(&a.out.ctl[0], 1u);
       __syncthreads();
@@ -524,15 +520,13 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
       uint32_t total = __shfl_sync(0xffffffffu, wi, LG_TPB / 32 - 1);
       if (lane == 0) {
         s_total = total;
-        if (a.pass == 1) a.out.status[tile] = total;   // two-pass: the tile's count only
         // publish the aggregate now, so successors can look back while we stage
-        if (!solo && !twopass)
+        if (!solo)
           atomicExch((unsigned long long*)&a.out.status[tile],
                      (unsigned long long)lb_pack(epoch, tile == 0 ? 2u : 1u, total));
       }
     }
     __syncthreads();
-    if (a.pass == 1) continue;
     // stage the tile's first LG_STAGE entries in shared memory (tile-local
     // offsets need no prefix) while warp 0 runs the look-back
     const uint32_t my0 = s_warp[warp] + (inc - cnt);
@@ -566,8 +560,6 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
     }
     if (solo) {
       if (threadIdx.x == 0) s_base = s_run;
-    } else if (twopass) {
-      if (threadIdx.x == 0) s_base = (uint32_t)a.out.status[tile];   // scanned by k_listgen_scan
     } else if (warp == 0) {
       const uint32_t total = s_total;
       uint64_t* st = a.out.status;
@@ -613,7 +605,6 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
     }
     if (solo && threadIdx.x == 0) s_run = base + total;
   }
-  if (twopass) return;   // count and table flag: k_listgen_scan
   if (solo) {
     if (threadIdx.x == 0) {
       uint32_t n = s_run;
@@ -636,50 +627,6 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
   }
 }
 
-// Two-pass listgen, middle step: exclusive scan of the per-tile counts (one CTA).
-__global__ void __launch_bounds__(1024) k_listgen_scan(const __grid_constant__ LGArgs a) {
-  __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_carry;
-  const uint32_t nparent = a.mode == 0 ? 1u : *a.pcount;
-  const uint64_t nchunks = (uint64_t)nparent << a.lcpp;
-  const uint32_t ntiles = (uint32_t)((nchunks + LG_TILE - 1) / LG_TILE);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < ntiles; base += 1024) {
-    const uint32_t t = base + threadIdx.x;
-    const uint32_t c = t < ntiles ? (uint32_t)a.out.status[t] : 0u;
-    uint32_t inc = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t p = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += p;
-    }
-    if (lane == 31) s_w[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-      uint32_t v = s_w[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t p = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += p;
-      }
-      s_w[lane] = v;
-    }
-    __syncthreads();
-    const uint32_t carry = s_carry, wp = w ? s_w[w - 1] : 0u;
-    if (t < ntiles) a.out.status[t] = carry + wp + inc - c;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = carry + wp + inc;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    uint32_t n = s_carry;
-    if (n > a.out.capacity) { set_err(a.C, SG_ERR_LIST_OVERFLOW, a.task); n = a.out.capacity; }
-    *a.out.count = n;
-    a.out.ctl[4] = 0u;   // the block table (if any) is stale until a struct-for rebuilds it
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Warp-tile listgen for big bitmasked lists (LG-XL).  Same set as
@@ -1258,18 +1205,6 @@ int launch_listgen(const DevCtx& c, const DTree& t, int, int level, int parent_l
   a.pcount = parent ? parent->count : nullptr;
   int grid = grid_hint > 0 ? grid_hint : 1;
   const int resident = num_sms() * 4;
-  a.pass = 0;
-  if (grid_hint > 4 * resident && getenv("SG_LG_TWOPASS") != nullptr) {
-    // experiment (opt-in): count, scan the tile counts, write -- measured 1.8x
-    // slower than the single pass on LG-XL (profiles/r01_*), so not the default
-    cudaStream_t st = (cudaStream_t)stream;
-    a.pass = 1;
-    k_listgen<<<resident, LG_TPB, 0, st>>>(a);
-    k_listgen_scan<<<1, 1024, 0, st>>>(a);
-    a.pass = 2;
-    k_listgen<<<resident, LG_TPB, 0, st>>>(a);
-    return check_launch();
-  }
   // big bitmasked lists: warp tiles (k_listgen_warp).  SG_LG_WARP=0 forces the
   // CTA-tile kernel, =1 the warp-tile kernel wherever it applies.
   static const int lg_warp_env = getenv("SG_LG_WARP") ? atoi(getenv("SG_LG_WARP")) : -1;

@@ -562,9 +562,7 @@ static void make_op(const sg_grid* g, const PTask& t, uint32_t act, int loop_tre
 }
 
 static int grid_hint_struct(const sg_grid* g, const DTree& T) {
-  if (T.driving < 0) return g->num_sms * 8;
-  uint64_t cap = g->lists.empty() ? 1 : 1;
-  (void)cap;
+  (void)T;
   return g->num_sms * 8;
 }
 
