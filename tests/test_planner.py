@@ -435,3 +435,16 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(sg.EXPORTS)
+
+
+def test_stats_struct_matches_header():
+    import ctypes
+    """The ctypes sg_stats mirror has the header's fields, in order, with the
+    header's types (a drifted mirror would corrupt memory on every flush)."""
+    import re
+    hdr = open(sg.LIB_PATH.replace("paper_2012_08141_b200/libsg.so", "include/sg.h")).read()
+    body = hdr[: hdr.index("} sg_stats;")]
+    body = body[body.rindex("typedef struct {"):]
+    fields = re.findall(r"^\s*(int64_t|double|int32_t)\s+(\w+);", body, re.M)
+    ctype = {"int64_t": ctypes.c_int64, "double": ctypes.c_double, "int32_t": ctypes.c_int32}
+    assert [(n, ctype[t]) for t, n in fields] == [(n, t) for n, t in sg.Stats._fields_]
