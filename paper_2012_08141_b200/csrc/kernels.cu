@@ -1381,7 +1381,7 @@ int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DO
     MpmBinArgs m;
     m.T = *grid_tree; m.TG = tree2 ? *tree2 : *grid_tree; m.C = c; m.op = ops[0]; m.B = *bins; m.task = task;
     // (bin, chunk) grid: x strides over the non-empty bins, y over a bin's chunks
-    const dim3 grid((unsigned)num_sms() * 2, MB_CHUNKS_Y);
+    const dim3 grid((unsigned)num_sms() * MB_BINS_X, MB_CHUNKS_Y);
     switch (ops[0].op) {
       case SG_OP_P2G: k_p2g_bin<<<grid, MB_TPB, 0, s>>>(m); break;
       case SG_OP_G2P: k_g2p_bin<<<grid, MB_TPB, 0, s>>>(m); break;

@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(BIN_TPB) k_bin_scatter(const __grid_constant__
 // Binned kernels
 // ---------------------------------------------------------------------------
 constexpr int MB_WARPS = MB_TPB / 32;
-constexpr int MB_CHUNKS_Y = 8;   // gridDim.y: chunk slots per bin (grid-strided)
+constexpr int MB_CHUNKS_Y = 4;   // gridDim.y: chunk slots per bin (grid-strided)
+constexpr int MB_BINS_X = 6;     // gridDim.x = MB_BINS_X x SMs: bin slots (grid-strided)
 
 struct MpmBinArgs {
   DTree T;      // grid tree (P2G target / G2P source / G2P_ADJ forward grid)
