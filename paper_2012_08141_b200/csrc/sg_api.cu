@@ -826,7 +826,18 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
     sig = 1469598103934665603ull;
     auto mix = [&](uint64_t v) { sig ^= v; sig *= 1099511628211ull; };
     mix(key);
-    for (const PTask& t : g->eager) { mix((uint64_t)(uintptr_t)t.coords); mix((uint64_t)t.n); }
+    // task params are baked into the captured kernels' __grid_constant__ op
+    // tables (the plan key ignores them: passes never depend on them)
+    for (const PTask& t : g->eager) {
+      mix((uint64_t)(uintptr_t)t.coords);
+      mix((uint64_t)t.n);
+      mix((uint64_t)t.t.activating);
+      for (int i = 0; i < 8; i++) {
+        uint32_t b;
+        std::memcpy(&b, &t.t.params[i], 4);
+        mix(b);
+      }
+    }
     mix((uint64_t)(uintptr_t)g->d_arrays);
     mix((uint64_t)g->arrays.size());
     for (const DArray& a : g->arrays) { mix((uint64_t)(uintptr_t)a.ptr); mix((uint64_t)a.n); mix((uint64_t)(uintptr_t)a.dcount); }
