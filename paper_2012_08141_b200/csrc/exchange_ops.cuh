@@ -204,12 +204,14 @@ __global__ void __launch_bounds__(256) k_migrate_append(const __grid_constant__ 
   const DOp& op = A.op;
   const DArray X = C.arrays[op.a[0]], Vv = C.arrays[op.a[1]], Cm = C.arrays[op.a[2]], Jj = C.arrays[op.a[3]],
                Id = C.arrays[op.a[4]], Lb = C.arrays[op.a[5]], Rb = C.arrays[op.a[6]];
-  const uint32_t n0 = *X.dcount, cl = *Lb.dcount, cr = *Rb.dcount;
-  const uint64_t capl = Lb.n / PREC_WORDS;
+  // received counts are clamped to the buffers' record capacity: a sender whose
+  // buffer overflowed latched SG_ERR_LIST_OVERFLOW and kept counting
+  const uint32_t n0 = *X.dcount;
+  const uint32_t cl = (uint32_t)min((uint64_t)*Lb.dcount, (uint64_t)Lb.n / PREC_WORDS);
+  const uint32_t cr = (uint32_t)min((uint64_t)*Rb.dcount, (uint64_t)Rb.n / PREC_WORDS);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cl + cr; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t* rec = i < cl ? (const uint32_t*)Lb.ptr + i * PREC_WORDS
                                  : (const uint32_t*)Rb.ptr + (i - cl) * PREC_WORDS;
-    (void)capl;
     const uint64_t dst = n0 + i;
     if (dst >= (uint64_t)X.n) { set_err(C, SG_ERR_LIST_OVERFLOW, 0); continue; }
     float* x = (float*)X.ptr;

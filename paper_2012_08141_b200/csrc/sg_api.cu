@@ -774,8 +774,22 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
   return SG_OK;
 }
 
+// Makes the grid's device current for the scope of a call (lazy allocations
+// and launches inside sg_flush), restoring the caller's device afterwards.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const sg_grid* g) {
+    if (g->plan_only) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; return; }
+    if (prev == g->opts.device) prev = -1;
+    else cudaSetDevice(g->opts.device);
+  }
+  ~DeviceScope() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
 extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observed, int32_t n_observed, sg_stats* out) {
   if (!g) return fail(SG_ERR_ARG, "null grid");
+  DeviceScope dev_scope(g);
   sg_stats st;
   std::memset(&st, 0, sizeof(st));
   auto t0 = std::chrono::steady_clock::now();

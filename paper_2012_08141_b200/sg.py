@@ -127,12 +127,14 @@ def passes_mask(p):
 _torch_alloc_keep = []
 
 
-def _torch_allocators():
+def _torch_allocators(device):
     import torch
 
     @ALLOC_FN
     def _alloc(ctx, nbytes, stream):
-        return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream)
+        # the grid's own device, not the caller's current one (lazy allocations
+        # inside sg_flush of a grid on another device)
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device, stream)
 
     @FREE_FN
     def _free(ctx, ptr, stream):
@@ -170,7 +172,7 @@ class Grid:
                 stream = torch.cuda.current_stream(device).cuda_stream
             o.stream = stream
             if torch_alloc:
-                a, f = _torch_allocators()
+                a, f = _torch_allocators(device)
                 o.alloc, o.free = a, f
         self.plan_only = plan_only
         h = _vp()
