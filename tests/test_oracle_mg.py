@@ -43,14 +43,16 @@ def rb_half_sweep(z, r, m, parity):
 
 
 def coarse_mask(m, block):
+    """Active cells of the next coarser level: coarse blocks (of `block` cells)
+    that contain the image of an active fine cell."""
     n = m.shape[0] // 2
     mc = m.reshape(n, 2, n, 2).max(axis=(1, 3))
-    b = min(block, n)
+    b = max(1, min(block, n))
     nb = n // b
     return np.kron(mc.reshape(nb, b, nb, b).max(axis=(1, 3)), np.ones((b, b)))
 
 
-def dense_vcycle(z, r, masks, l, nu=2, bottom=8, w=0.5):
+def dense_vcycle(z, r, masks, l, nu=2, bottom=W.MG_BOTTOM, w=W.mg_weight(2)):
     m = masks[l]
     if l == len(masks) - 1:
         for _ in range(bottom // 2):
@@ -75,8 +77,8 @@ def dense_masks():
     for x, y in W.mg_region(N, BLOCK, RADIUS):
         m0[x:x + BLOCK, y:y + BLOCK] = 1.0
     masks = [m0]
-    for _ in range(LEVELS - 1):
-        masks.append(coarse_mask(masks[-1], BLOCK))
+    for l in range(1, LEVELS):
+        masks.append(coarse_mask(masks[-1], BLOCK >> l))
     return masks
 
 
@@ -97,8 +99,7 @@ def test_mg_vcycles_match_dense_textbook(cycles):
     for l in range(1, LEVELS):
         leaf = prog["levels"][l][-1]
         act = o.mask(prog["levels"][l][0])
-        n = N >> l
-        b = min(BLOCK, n)
+        b = max(1, BLOCK >> l)
         want = {(x // b, y // b) for x, y in zip(*np.nonzero(masks[l]))}
         assert {tuple(c) for c in np.asarray(act).reshape(-1, 2)} == want, l
         del leaf
@@ -111,7 +112,7 @@ def test_restriction_and_prolongation_are_adjoint():
     f = L.fields
     coords = W.mg_region(N, BLOCK, RADIUS)
     rng = np.random.default_rng(1)
-    w = 0.5
+    w = W.mg_weight(2)
     o = Oracle(L.desc())
     o.set_exact(True)
     o.call(W.activate(f["z0"], coords))
@@ -124,7 +125,7 @@ def test_restriction_and_prolongation_are_adjoint():
     o.call(W.struct_for("PROLONG", lv[0][-1], [f["z0"], f["z1"]]))
     Pv = o.field(f["z0"])
     m0 = dense_masks()[0]
-    m1 = coarse_mask(m0, BLOCK)
+    m1 = coarse_mask(m0, BLOCK >> 1)
     lhs = (Ru * v * m1).sum()
     rhs = w * (u * m0 * Pv).sum()
     assert lhs == pytest.approx(rhs, rel=1e-12)
@@ -195,3 +196,117 @@ def test_cg_ops_closed_form():
     np.testing.assert_allclose(o.field(f["x"]), (want_p + (dot_aa / dot_ab) * a) * m, rtol=1e-12, atol=1e-12)
     o.call(W.serial("COPY_SCALAR", [f["rTr"], f["pAp"]]))
     assert float(o.field(f["rTr"]).reshape(-1)[0]) == pytest.approx(dot_aa, rel=1e-15)
+
+
+# ---- bench size (512^2, 4 levels): the V-cycle is an SPD preconditioner and
+# MGPCG converges (VERDICT r1 "make N1 actually solve") -----
+NB, LB, BB, RB = 512, 4, 16, 0.3125
+
+
+def bench_masks():
+    m0 = np.zeros((NB, NB))
+    for x, y in W.mg_region(NB, BB, RB):
+        m0[x:x + BB, y:y + BB] = 1.0
+    masks = [m0]
+    for l in range(1, LB):
+        masks.append(coarse_mask(masks[-1], BB >> l))
+    return masks
+
+
+def masked_laplacian(m):
+    from scipy.sparse import csr_matrix
+    n = m.shape[0]
+    act = np.argwhere(m > 0)
+    idx = -np.ones(m.shape, dtype=np.int64)
+    idx[tuple(act.T)] = np.arange(len(act))
+    rows, cols, vals = [np.arange(len(act))], [np.arange(len(act))], [np.full(len(act), 4.0)]
+    for di, dj in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+        ii, jj = act[:, 0] + di, act[:, 1] + dj
+        ok = (ii >= 0) & (ii < n) & (jj >= 0) & (jj < n)
+        nb = np.full(len(act), -1)
+        nb[ok] = idx[ii[ok], jj[ok]]
+        sel = nb >= 0
+        rows.append(np.arange(len(act))[sel]); cols.append(nb[sel]); vals.append(np.full(sel.sum(), -1.0))
+    A = csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(len(act),) * 2)
+    return A, act
+
+
+def oracle_vcycle(u):
+    """z = M u: one oracle V-cycle (f64) from z0 = 0 with r0 = u."""
+    L, lv = W.mg_layout(NB, LB, BB)
+    f = L.fields
+    o = Oracle(L.desc())
+    o.set_exact(True)
+    o.call(W.activate(f["z0"], W.mg_region(NB, BB, RB)))
+    o.load_field(f["r0"], u)
+    o.call(W.struct_for("FILL", lv[0][-1], [f["z0"]], [0.0]))
+    for c in W.mg_vcycle_calls(L, lv, LB, 2, W.MG_BOTTOM, W.mg_weight(2)):
+        o.call(c)
+    return o.field(f["z0"])
+
+
+def test_vcycle_is_spd_at_bench_size():
+    masks = bench_masks()
+    m = masks[0]
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal((NB, NB)) * m
+    v = rng.standard_normal((NB, NB)) * m
+    Mu, Mv = oracle_vcycle(u), oracle_vcycle(v)
+    # the oracle's V-cycle is the textbook one at full size as well
+    np.testing.assert_allclose(Mu, dense_vcycle(np.zeros((NB, NB)), u, masks, 0), rtol=1e-11, atol=1e-11)
+    uMv, vMu = (u * Mv).sum(), (v * Mu).sum()
+    assert abs(uMv - vMu) <= 1e-11 * np.sqrt((u * Mu).sum() * (v * Mv).sum())
+    assert (u * Mu).sum() > 0 and (v * Mv).sum() > 0
+    # positive on a smooth vector too (where a wrong coarse scaling goes negative)
+    ii, jj = np.meshgrid(np.arange(NB), np.arange(NB), indexing="ij")
+    s = np.sin(np.pi * ii / NB) * np.sin(np.pi * jj / NB) * m
+    assert (s * oracle_vcycle(s)).sum() > 0
+
+
+def _scipy_pcg(iters):
+    """scipy's CG on the masked 5-point system, preconditioned by the textbook
+    V-cycle above (both independent of the oracle).  Returns rTr per iteration."""
+    from scipy.sparse.linalg import LinearOperator, cg
+    masks = bench_masks()
+    A, act = masked_laplacian(masks[0])
+    sel = tuple(act.T)
+
+    def prec(r):
+        d = np.zeros((NB, NB))
+        d[sel] = r
+        return dense_vcycle(np.zeros((NB, NB)), d, masks, 0)[sel]
+
+    b = np.ones(len(act))
+    hist = [float(b @ b)]
+
+    def cb(xk):
+        r = b - A @ xk
+        hist.append(float(r @ r))
+
+    cg(A, b, x0=np.zeros(len(act)), M=LinearOperator(A.shape, prec), maxiter=iters, rtol=1e-30, atol=0.0,
+       callback=cb)
+    return hist
+
+
+def test_mgpcg_reduces_residual_1e3_in_the_timed_iterations():
+    hist = _scipy_pcg(10)
+    assert hist[-1] <= 1e-3 * hist[0], hist
+
+
+def test_oracle_mgpcg_tracks_scipy_pcg_at_bench_size():
+    iters = 3
+    hist = _scipy_pcg(iters)
+    prog = W.mgpcg_program(n=NB, levels=LB, block=BB, iters=iters, radius_frac=RB)
+    o = run_exact(prog)
+    rtr = float(np.asarray(o.field(prog["layout"].fields["rTr"])).reshape(-1)[0])
+    assert rtr == pytest.approx(hist[-1], rel=1e-6), (rtr, hist)
+
+
+def test_mg_reduces_residual_at_bench_size():
+    masks = bench_masks()
+    r = masks[0].copy()
+    z = np.zeros((NB, NB))
+    res0 = (r * r).sum()
+    for _ in range(10):
+        z = dense_vcycle(z, r, masks, 0)
+    assert ((r - lap_apply(z, masks[0])) ** 2).sum() < 0.05 * res0

@@ -388,12 +388,20 @@ def c4_program(n_grid=64, n_particles=100_000, T=64, seed=0, passes="all", comp=
 # Gauss-Seidel smoothing, residual restriction with activate-on-write on the
 # coarse level (demoted after the first cycle), prolongation.
 # ----------------------------------------------------------------------------
+MG_BOTTOM = 32   # red-black sweeps on the coarsest level (reading R36)
+
+
 def mg_layout(n=512, levels=4, block=16, cg=False):
+    """Level l is a two-level sparse grid pointer(n/block) -> dense(block >> l)
+    ("for each level we use a two-level sparse grid"): a coarse
+    block is exactly the image of one fine block, so the coarse active region
+    that restriction activates (block granularity) is exactly the image of the
+    fine region (reading R36)."""
     L = Layout()
     lv = []
     for l in range(levels):
         nl = n >> l
-        b = min(block, nl)
+        b = max(1, block >> l)
         fields = [(f"z{l}", "f32"), (f"r{l}", "f32")]
         if cg and l == 0:
             fields += [("x", "f32"), ("p", "f32"), ("Ap", "f32")]
@@ -423,7 +431,7 @@ def mg_region(n=512, block=16, radius_frac=0.3125, center=(0.5, 0.5)):
     return np.asarray(out, dtype=np.int32)
 
 
-def mg_vcycle_calls(L, lv, levels=4, nu=2, bottom=8, weight=1.0):
+def mg_vcycle_calls(L, lv, levels=4, nu=2, bottom=MG_BOTTOM, weight=1.0):
     f = L.fields
     z = [f[f"z{l}"] for l in range(levels)]
     r = [f[f"r{l}"] for l in range(levels)]
@@ -451,30 +459,35 @@ def mg_vcycle_calls(L, lv, levels=4, nu=2, bottom=8, weight=1.0):
     return calls
 
 
-def mg_solve_calls(L, lv, coords, cycles=10, levels=4, nu=2, bottom=8, dim=2, with_residual=True):
+def mg_weight(dim=2):
+    """Restriction weight 4 / 2^dim (= 1 in 2-D): the re-discretized coarse
+    operator (the h^2 scaling of the coarse grid, 4, times the average over the
+    2^dim children).  Reading R36."""
+    return 4.0 / (1 << dim)
+
+
+def mg_solve_calls(L, lv, coords, cycles=10, levels=4, nu=2, bottom=MG_BOTTOM, dim=2, with_residual=True):
     """Activate the finest level, r0 = 1 (the right-hand side), z0 = 0, then
-    `cycles` V-cycles; finally res = ||r0 - A z0||^2.  Restriction weight
-    4 / 2^dim (= 1 in 2-D): the h^2 scaling of the coarse operator times the
-    average over the 2^dim children."""
+    `cycles` V-cycles; finally res = ||r0 - A z0||^2."""
     f = L.fields
     calls = [activate(f["z0"], coords), struct_for("FILL", lv[0][-1], [f["r0"]], [1.0]),
              struct_for("FILL", lv[0][-1], [f["z0"]], [0.0])]
     for _ in range(cycles):
-        calls += mg_vcycle_calls(L, lv, levels, nu, bottom, weight=2.0 / (1 << dim))
+        calls += mg_vcycle_calls(L, lv, levels, nu, bottom, weight=mg_weight(dim))
     if with_residual:
         calls += [serial("CLEAR_SCALAR", [f["res"]]),
                   struct_for("RESID_NORM2", lv[0][-1], [f["res"], f["r0"], f["z0"]])]
     return calls
 
 
-def mgpcg_calls(L, lv, coords, iters=10, levels=4, nu=2, bottom=8, dim=2):
+def mgpcg_calls(L, lv, coords, iters=10, levels=4, nu=2, bottom=MG_BOTTOM, dim=2):
     """Conjugate gradients preconditioned by one V-cycle (MGPCG, PAPER.md:438-441
     after hu2019taichi): solve A x = b (b = 1 on the active region).  The
     V-cycle works on (z0, r0), so r0 doubles as the CG residual.  STENCIL gives
     -A p, so pAp = -<p, STENCIL p> and r -= alpha A p becomes r += alpha (-A p)."""
     f = L.fields
     leaf0 = lv[0][-1]
-    w = 2.0 / (1 << dim)
+    w = mg_weight(dim)
 
     def precondition():
         return [struct_for("FILL", leaf0, [f["z0"]], [0.0])] + mg_vcycle_calls(L, lv, levels, nu, bottom, weight=w)
@@ -498,7 +511,7 @@ def mgpcg_calls(L, lv, coords, iters=10, levels=4, nu=2, bottom=8, dim=2):
     return calls
 
 
-def mgpcg_program(n=512, levels=4, block=16, iters=10, nu=2, bottom=8, radius_frac=0.3125, passes="all"):
+def mgpcg_program(n=512, levels=4, block=16, iters=10, nu=2, bottom=MG_BOTTOM, radius_frac=0.3125, passes="all"):
     L, lv = mg_layout(n, levels, block, cg=True)
     coords = mg_region(n, block, radius_frac)
     calls = mgpcg_calls(L, lv, coords, iters, levels, nu, bottom)
@@ -508,7 +521,7 @@ def mgpcg_program(n=512, levels=4, block=16, iters=10, nu=2, bottom=8, radius_fr
     return prog
 
 
-def mg_program(n=512, levels=4, block=16, cycles=10, nu=2, bottom=8, radius_frac=0.3125, passes="all"):
+def mg_program(n=512, levels=4, block=16, cycles=10, nu=2, bottom=MG_BOTTOM, radius_frac=0.3125, passes="all"):
     L, lv = mg_layout(n, levels, block)
     coords = mg_region(n, block, radius_frac)
     calls = mg_solve_calls(L, lv, coords, cycles, levels, nu, bottom)
