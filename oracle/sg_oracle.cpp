@@ -735,10 +735,19 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
         Kernel k = kernel_of(ar[0], i);
         double J = A_(g, ar[3], 0, i);
         double stress = -dt * 4.0 * E * pv * (J - 1.0) * idx * idx;
-        double aff[3][3], v[3];
+        // shadow magnitudes (reading R15: the sum of the absolute values of
+        // every term the value is computed from, inputs at their own shadow
+        // magnitude): |stress| counts |J| + 1, the momentum |p_mass v| +
+        // sum_d |aff_rd dpos_d| term by term (they may cancel)
+        const double stress_m = dt * 4.0 * E * pv * (M_(g, ar[3], 0, i) + 1.0) * idx * idx;
+        double aff[3][3], affm[3][3], v[3], vm[3];
         for (int r = 0; r < 3; r++) {
           v[r] = A_(g, ar[1], r, i);
-          for (int c = 0; c < 3; c++) aff[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? stress : 0.0);
+          vm[r] = M_(g, ar[1], r, i);
+          for (int c = 0; c < 3; c++) {
+            aff[r][c] = pm * A_(g, ar[2], 3 * r + c, i) + (r == c ? stress : 0.0);
+            affm[r][c] = pm * M_(g, ar[2], 3 * r + c, i) + (r == c ? stress_m : 0.0);
+          }
         }
         for (int a = 0; a < 3 && !rc; a++)
           for (int b = 0; b < 3 && !rc; b++)
@@ -747,9 +756,12 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
               node_w(k, a, b, c, W, gW, dpos);
               Coord node{k.base[0] + a, k.base[1] + b, k.base[2] + c};
               for (int r = 0; r < 3 && !rc; r++) {
-                double mom = pm * v[r];
-                for (int d = 0; d < 3; d++) mom += aff[r][d] * dpos[d];
-                rc = atomic_add(g, f[r], node, W * mom, act_bit(activating, r));
+                double mom = pm * v[r], momm = pm * vm[r];
+                for (int d = 0; d < 3; d++) {
+                  mom += aff[r][d] * dpos[d];
+                  momm += affm[r][d] * std::fabs(dpos[d]);
+                }
+                rc = atomic_add_m(g, f[r], node, W * mom, std::fabs(W) * momm, act_bit(activating, r));
               }
               if (!rc) rc = atomic_add(g, f[3], node, W * pm, act_bit(activating, 3));
             }

@@ -2,11 +2,12 @@
 
 * one backward substep, both sides fed the same seeded state and adjoint seed:
   grid-adjoint tree masks exact, grid adjoints and particle adjoints within
-  1e-4 of the oracle's shadow magnitude M (reading R32), at a small size and at
-  the full 64^3 / 100K-particle size;
-* a whole small forward + backward window (T = 4, all passes): loss 1e-5,
-  final state and gradient within 1e-3 of M (the f32 rounding of each substep
-  feeds the next, reading R17);
+  1e-5 of the oracle's shadow magnitude M (readings R15, R32), at a small size
+  and at the full 64^3 / 100K-particle size;
+* a whole small forward + backward window (T = 4, all passes): the loss within
+  1e-5, and every forward and backward substep of the window by single-step
+  handoff (reading R17): the oracle's own state (and adjoint) entering the
+  substep is loaded on both sides, one substep runs, everything within 1e-5 of M;
 * full size (T = 64): the gradient is finite and its directional derivative
   along the initial velocity matches f32 central differences of the GPU loss.
 """
@@ -57,7 +58,7 @@ def one_substep_program(n_grid, n, seed, dt=2e-4):
     return W.program(L, calls, arrays=arrays, name="C4-1"), L, lg
 
 
-def check_one_substep(prog, L, lg, tol=1e-4):
+def check_one_substep(prog, L, lg, tol=1e-5):
     o = oracle.run_program(prog)
     g, arrs, st = gpu_run(prog)
     for s in lg:
@@ -88,22 +89,74 @@ def test_c4_one_backward_substep_full_size():
     check_one_substep(prog, L, lg)
 
 
+def handoff_backward_program(n_grid, state, adj, prm):
+    """One backward substep (recompute P2G, G2P_ADJ, P2G_ADJ) entering from a
+    given particle state s and adjoint of state s+1 (both f32 on both sides)."""
+    L, lv, lg = W.c4_layout(n_grid)
+    n = state["x"].shape[1]
+    arrays = W.c4_arrays(n, 1, n_grid)
+    for k in ("x", "v", "C", "J"):
+        arrays[f"{k}0"] = np.ascontiguousarray(state[k], dtype=np.float32)
+        arrays[f"adjA_{k}"] = np.ascontiguousarray(adj[k], dtype=np.float32)
+    calls = W.c4_backward_calls(L, lv, lg, n, 1, prm)[1:] + [W.flush()]
+    return W.program(L, calls, arrays=arrays, name="C4-handoff"), L, lg
+
+
+def handoff_forward_program(n_grid, state, prm):
+    """One forward substep (DEACTIVATE, grad clears, P2G, GRID_OP, G2P) from a
+    given particle state."""
+    L, lv, lg = W.c4_layout(n_grid)
+    n = state["x"].shape[1]
+    arrays = W.c4_arrays(n, 1, n_grid)
+    for k in ("x", "v", "C", "J"):
+        arrays[f"{k}0"] = np.ascontiguousarray(state[k], dtype=np.float32)
+    calls = W.c4_forward_calls(L, lv, lg, n, 1, prm)[:-2] + [W.flush()]
+    return W.program(L, calls, arrays=arrays, name="C4-fwd-handoff"), L
+
+
 @pytest.mark.parametrize("passes", [0, "all"])
 def test_c4_small_window(passes):
-    T = 4
-    prog = W.c4_program(n_grid=32, n_particles=4000, T=T, seed=13, passes="all")
+    T, ng, n = 4, 32, 4000
+    prog = W.c4_program(n_grid=ng, n_particles=n, T=T, seed=13, passes="all")
+    prm = prog["params"]
     o = oracle.run_program(prog)
     g, arrs, st = gpu_run(prog, passes)
     L = prog["layout"]
     loss = float(g.field(L.fields["loss"]).reshape(-1)[0])
-    want = float(o.field(L.fields["loss"]).reshape(-1)[0])
-    assert loss == pytest.approx(want, rel=1e-5)
-    names = list(prog["arrays"])
-    for i in list(range(4 * T, 4 * T + 4)) + prog["result_arrays"]:
-        want, mag = o.array(i, with_mag=True)
-        close(arrs[names[i]].cpu().numpy(), want, mag, 1e-3, names[i], floor=1e-5)
+    want, mag = o.field(L.fields["loss"], with_mag=True)
+    close(loss, want, mag, 1e-5, "loss")
     if passes == "all":
         assert st[0]["dead_removed"] == 8 * T
+    names = list(prog["arrays"])
+    keys = ("x", "v", "C", "J")
+
+    def ostate(oo, s):
+        return {k: oo.array(4 * s + i) for i, k in enumerate(keys)}
+
+    # forward substeps s -> s+1 from the oracle's state s
+    for s in range(T):
+        p1, L1 = handoff_forward_program(ng, ostate(o, s), prm)
+        o1 = oracle.run_program(p1)
+        g1, a1, _ = gpu_run(p1, passes)
+        n1 = list(p1["arrays"])
+        for i in range(4, 8):
+            want, mag = o1.array(i, with_mag=True)
+            close(a1[n1[i]].cpu().numpy(), want, mag, 1e-5, f"forward substep {s}: {n1[i]}")
+        for name in ("px", "py", "pz", "m"):
+            want, mag = o1.field(L1.fields[name], with_mag=True)
+            close(g1.field(L1.fields[name]), want, mag, 1e-5, f"forward substep {s}: grid {name}")
+    # backward substeps: the oracle's adjoint of state s+1 (after ADJ_INIT and the
+    # backward substeps T-1 .. s+1 of the eager program) and its state s
+    n_fwd = len(W.c4_forward_calls(L, *W.c4_layout(ng)[1:], n, T, prm))
+    A = [4 * (T + 1) + k for k in range(4)]
+    B = [4 * (T + 1) + 4 + k for k in range(4)]
+    for j, s in enumerate(reversed(range(T))):
+        op = oracle.run_program(prog, upto=n_fwd + 1 + 5 * j)
+        src = A if j % 2 == 0 else B
+        adj = {k: op.array(src[i]) for i, k in enumerate(keys)}
+        p1, L1, lg1 = handoff_backward_program(ng, ostate(o, s), adj, prm)
+        check_one_substep(p1, L1, lg1)
+    del names
 
 
 def test_c4_full_size_gradient_properties():

@@ -1,9 +1,10 @@
 """GPU parity of the multigrid workload against the oracle (-m gpu).
 
 Masks of every level exact (the coarse levels are activated by RESTRICT's
-activate-on-write, demoted after the first cycle); z and r of every level and
-the residual norm within 1e-4 of the oracle's shadow magnitude M (several
-Gauss-Seidel sweeps and restrictions compound the f32 rounding, reading R29).
+activate-on-write, demoted after the first cycle); z and r of every level, the
+CG vectors and scalars and the residual norm within 1e-5 of the oracle's shadow
+magnitude M (reading R15) -- whole solves, no handoff needed: the shadow
+magnitudes carry every sweep's terms.
 """
 import numpy as np
 import pytest
@@ -20,7 +21,7 @@ from paper_2012_08141_b200 import sg  # noqa: E402
 from test_gpu_parity import as_set  # noqa: E402
 
 
-def compare(g, o, prog, tol=1e-4):
+def compare(g, o, prog, tol=1e-5):
     L = prog["layout"]
     for lv in prog["levels"]:
         for s in lv:
@@ -65,46 +66,42 @@ def test_mg_full_size_one_cycle_and_replay():
 
 
 def test_mg_full_size_ten_cycles_converge():
-    res = []
-    for cycles in (2, 10):
-        prog = W.mg_program(n=512, cycles=cycles)
-        g = sg.Grid(prog["desc"])
-        sg.replay(g, prog, device="cuda")
-        g.sync()
-        res.append(float(np.asarray(g.field(prog["layout"].fields["res"])).reshape(-1)[0]))
-    # (4 levels down to a 64^2 bottom grid smoothed 8 times: a slow V-cycle on
-    # its own -- the paper wraps it in CG -- but the residual must keep falling)
-    assert np.isfinite(res).all() and res[1] < 0.9 * res[0]
+    """The bench's MG solve (512^2, 4 levels, 10 V-cycles): oracle parity of
+    every level and ||r||^2 below 5% of its initial 88,064 (a V-cycle with
+    piecewise-constant prolongation on its own converges slowly; MGPCG below is
+    the paper's solver)."""
+    prog = W.mg_program(n=512, cycles=10)
+    o = oracle.run_program(prog)
+    g = sg.Grid(prog["desc"])
+    sg.replay(g, prog, device="cuda")
+    g.sync()
+    compare(g, o, prog)
+    res = float(np.asarray(g.field(prog["layout"].fields["res"])).reshape(-1)[0])
+    assert res < 0.05 * 88064.0, res
 
 
 def test_mgpcg_small():
-    """MGPCG: two CG iterations on 64^2 -- every field within 1e-3 of M (CG
-    divides by device-computed dot products; reading R32's multi-step bound)."""
+    """MGPCG: two CG iterations on 64^2 (CG divides by device-computed dot
+    products; the oracle's shadow magnitudes carry them)."""
     prog = W.mgpcg_program(n=64, levels=3, block=8, iters=2, radius_frac=0.3)
     o = oracle.run_program(prog)
     g = sg.Grid(prog["desc"])
     sg.replay(g, prog, device="cuda")
     g.sync()
-    compare(g, o, prog, tol=1e-3)
+    compare(g, o, prog)
 
 
-def test_mgpcg_full_size():
-    """512^2, 4 levels: x after 2 CG iterations within 1e-3 of M of the oracle's;
-    10 iterations stay finite and track the oracle's residual (at this size the
-    V-cycle with a 64^2 bottom grid is a weak preconditioner: the oracle's own
-    rTr goes 88,064 -> 645,019 over 10 iterations, CG's residual is not monotone)."""
-    L = W.mgpcg_program(n=512, iters=2)["layout"]
-    prog2 = W.mgpcg_program(n=512, iters=2)
-    o = oracle.run_program(prog2)
-    g2 = sg.Grid(prog2["desc"])
-    sg.replay(g2, prog2, device="cuda")
-    g2.sync()
-    want, mag = o.field(L.fields["x"], with_mag=True)
-    got = np.asarray(g2.field(L.fields["x"]), dtype=np.float64)
-    assert (np.abs(got - want) <= 1e-3 * np.maximum(np.abs(want), mag)).all()
-    prog = W.mgpcg_program(n=512, iters=10)
+@pytest.mark.parametrize("iters", [2, 10])
+def test_mgpcg_full_size(iters):
+    """512^2, 4 levels, the bench's 10 CG iterations: every field within 1e-5
+    of M, and rTr down by >= 1e3 from 88,064 (the preconditioner is SPD,
+    tests/test_oracle_mg.py)."""
+    prog = W.mgpcg_program(n=512, iters=iters)
+    o = oracle.run_program(prog)
     g = sg.Grid(prog["desc"])
     sg.replay(g, prog, device="cuda")
     g.sync()
-    rTr = float(np.asarray(g.field(L.fields["rTr"])).reshape(-1)[0])
-    assert np.isfinite(rTr) and 0.5 * 645019.0 < rTr < 2.0 * 645019.0
+    compare(g, o, prog)
+    rTr = float(np.asarray(g.field(prog["layout"].fields["rTr"])).reshape(-1)[0])
+    if iters == 10:
+        assert np.isfinite(rTr) and rTr < 1e-3 * 88064.0, rTr

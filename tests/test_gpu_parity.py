@@ -176,3 +176,22 @@ def test_c2_full_size_properties():
     for name in ("x1", "s"):
         want, mag = o1.field(L1.fields[name], with_mag=True)
         assert_field_close(g1.field(L1.fields[name]), want, mag, "f32", f"C2 full size, 1 iteration, {name}")
+
+
+@pytest.mark.parametrize("iters", [2, 3])
+def test_c2_full_size_unfused_jacobi(iters):
+    """BASELINE configs[1] at full size (256^3, 3,280 8^3 blocks): `iters`
+    JACOBI sweeps with no reduction after them, so every sweep is a lone JACOBI
+    group and runs in k_jacobi8 -- the bench's dominant kernel, in the launch
+    configuration bench.py times (grid-stride over 6,560 half blocks, the
+    block-table path) -- compared element by element with the oracle at 1e-5."""
+    coords = W.block_ball_coords(32, 8, 68.0)
+    L, lv = W.c2_layout()
+    calls, _ = W.c2_solve_calls(L, lv, coords, iters=iters, reduce_result=False)
+    prog = W.program(L, calls + [W.flush()])
+    g, st = sg.run_program(prog)
+    o = oracle.run_program(prog)
+    for name in ("x0", "x1", "b"):
+        want, mag = o.field(L.fields[name], with_mag=True)
+        assert_field_close(g.field(L.fields[name]), want, mag, "f32", f"C2 full size, {iters} sweeps, {name}")
+    assert st[0]["launches"] == 4 + iters   # activate, 2 listgens, FILL b + FILL x0, the sweeps

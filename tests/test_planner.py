@@ -253,7 +253,10 @@ def test_mg_demotion_and_listgen_removal():
     assert s["listgen_launched"] == 7         # 4 levels' lists once, coarse ones after cycle 1
     assert s["tasks_fused"] == 31             # the two coarse clears per level, FILL r0 + FILL z0
     st0, _ = plan_counts(prog, passes=0)
-    assert st0[0]["launches"] == s["tasks_lowered"] == 1048
+    # eager: per cycle 2 x (4 pre + 4 post) + 64 bottom half sweeps, 3 restrictions, 3
+    # prolongations (a listgen + a body each), 6 clears, + setup / residual
+    assert st0[0]["launches"] == s["tasks_lowered"] == 2008
+    assert s["launches"] == 981
     nodem, _ = plan_counts(prog, passes=15 & ~2)
     assert nodem[0]["demotions"] == 0 and nodem[0]["listgen_launched"] == 34
     assert nodem[0]["launches"] > s["launches"]
@@ -265,7 +268,7 @@ def test_mgpcg_counts():
     # overwritten before it is observed except in the last iteration: DSE
     prog = W.mgpcg_program(n=512, iters=10)
     s = plan_counts(prog)[0][0]
-    assert (s["tasks_lowered"], s["launches"], s["listgen_launched"]) == (1356, 599, 7)
+    assert (s["tasks_lowered"], s["launches"], s["listgen_launched"]) == (2412, 1127, 7)
     assert s["dead_removed"] == 2 * 9 and s["demotions"] == 30
     nodem = plan_counts(prog, passes=15 & ~2)[0][0]
     assert nodem["listgen_launched"] == 37
