@@ -121,7 +121,7 @@ def test_c3_full_size_properties_and_handoff():
     L = prog["layout"]
     f = L.fields
     m = g.field(f["m"]).astype(np.float64)
-    np.testing.assert_allclose(m.sum(), n * prm["p_mass"], rtol=1e-4)
+    np.testing.assert_allclose(m.sum(), n * prm["p_mass"], rtol=1e-5)
     v = arrs["v"].cpu().numpy()
     np.testing.assert_allclose(v[1], -prm["dt"] * prm["gravity"], rtol=1e-5)   # free fall from rest
     assert np.abs(v[0]).max() < 1e-9 and np.abs(arrs["C"].cpu().numpy()).max() < 1e-4
