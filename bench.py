@@ -288,7 +288,44 @@ def cpu_baseline(args, max_seconds=30.0):
     return {"value": 1.0 / t_solve, "unit": "solves/s", "cores": 1, "kind": "oracle",
             "sample": f"C2 full grid, 1 and 2 Jacobi iterations timed ({times[0]:.1f}s, {times[1]:.1f}s); "
                       f"{args.iters}-iteration solve extrapolated = {t_solve:.1f}s",
-            "host_cpus": os.cpu_count()}
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "oracle_threads": 1}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_c5(args, thick=2):
+    """The oracle on a bounded sample of C5: one unpartitioned step of a
+    `thick`-cell x-slice of the bar at the full particle density (the same
+    per-particle and per-block work), scaled to the 460-cell bar."""
+    import oracle
+    n_full, length = args.c5_particles, 460
+    ns = int(round(n_full * thick / length))
+    rng = np.random.default_rng(0)
+    dx, c = 1.0 / 512, 256.0
+    x = np.empty((3, ns), np.float32)
+    x[0] = ((c - thick / 2) + rng.random(ns) * thick) * dx
+    x[1:] = ((c - 33) + rng.random((2, ns)) * 66) * dx
+    arrays = {"x": x, "v": np.zeros((3, ns), np.float32), "C": np.zeros((9, ns), np.float32),
+              "J": np.ones((1, ns), np.float32)}
+    L, lv = W.c5_layout(512, 16)
+    prm = W.mpm_params(512)
+    prog = W.program(L, W.c3_step_calls(L, lv, ns, prm) + [W.flush()], arrays=arrays)
+    t0 = time.perf_counter()
+    oracle.run_program(prog)
+    t = time.perf_counter() - t0
+    scale = length / thick
+    return {"value": 1.0 / (t * scale), "unit": "steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"one C5 step of a {thick}-cell x-slice of the bar at full density ({ns} particles): "
+                      f"{t:.1f}s, x{scale:.0f} slices",
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "oracle_threads": 1}
 
 
 def _timed_flushes(grid, enqueue, steps, warmup, l2=None, after_warmup=None):
@@ -502,21 +539,24 @@ def measure_mgpcg(steps=5, warmup=3, iters=10):
             "final_rTr": rtr}
 
 
-def run_c5(args, rank, world, local):
-    """C5: 512^3 sparse MPM, 16M particles in an x-spanning bar, sharded in x
-    slabs over the ranks (strong scaling); NCCL P2P halo / migration."""
+def c5_sim(args, rank, world, local, uid=None):
     import torch
     from paper_2012_08141_b200 import parallel
-    torch.cuda.set_device(local)
     n = args.c5_particles
     prm = W.mpm_params(512)
-    parts = W.c5_particles(n, 512, seed=0)
-    transport = parallel.DistTransport() if world > 1 else parallel.LocalTransport()
-    sim = parallel.SlabMPM(512, 16, parts, world, [rank], transport, prm, lambda r: torch.device("cuda", local),
-                           halo_cap=4096, mig_cap=65536)
+    # halo capacity: ~2x the active blocks of one 4-cell ghost layer across the
+    # bar's 66x66-cell section (17 x 17 blocks, 2 fields' worth of slack);
+    # migration: a generous bound on particles crossing one face per step
+    return parallel.SlabMPM(512, 16, lambda r: W.c5_rank_particles(n, r, world), world, [rank], prm,
+                            lambda r: torch.device("cuda", local), halo_cap=1024, mig_cap=65536, n_total=n,
+                            nccl_uid=uid, connect="nccl" if world > 1 else "local")
+
+
+def time_c5(sim, args, local, world):
+    import torch
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        st = sim.step()
+        st = sim.step(fused=True)
     torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
@@ -526,7 +566,7 @@ def run_c5(args, rank, world, local):
     with ClockSampler(local) as clk:
         a.record(stream)
         for _ in range(args.steps):
-            st = sim.step()
+            st = sim.step(fused=True)
             launches += sum(s["launches"] + s["aux_kernels"] for s in st)
         b.record(stream)
         torch.cuda.synchronize()
@@ -536,9 +576,46 @@ def run_c5(args, rank, world, local):
         t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    return ms / args.steps, launches, clk.summary(), st
+
+
+def run_c5(args, rank, world, local):
+    """C5: 512^3 sparse MPM, 16M particles in an x-spanning bar, sharded in x
+    slabs over the ranks (strong scaling).  Exchanges run inside libsg
+    (sg_dist_init with an NCCL id broadcast over torch.distributed: peer
+    memory over NVLink when the GPUs can map each other, else ncclSend/Recv);
+    every rank builds only its own slabs' particles."""
+    import torch
+    torch.cuda.set_device(local)
+    single = None
+    if world > 1:
+        import torch.distributed as dist
+        if rank == 0:   # the same workload on one GPU, in the same run, for the scaling context
+            sim1 = c5_sim(args, 0, 1, local)
+            ms1, _, _, _ = time_c5(sim1, args, local, 1)
+            single = {"value": 1000.0 / ms1, "ms_per_step": ms1, "unit": "steps/s"}
+            del sim1
+            torch.cuda.empty_cache()
+        uid = [None]
+        if rank == 0:
+            from paper_2012_08141_b200 import sg
+            uid = [sg.nccl_unique_id()]
+        dist.broadcast_object_list(uid, src=0)
+        sim = c5_sim(args, rank, world, local, uid[0])
+    else:
+        sim = c5_sim(args, rank, world, local)
+    ms, launches, clocks, st = time_c5(sim, args, local, world)
     me = sim.ranks[rank]
-    return {"ms_per_step": ms / args.steps, "launches": launches, "clocks": clk.summary(), "n_local": me.n(),
-            "launches_per_step_rank0": sum(s["launches"] for s in st)}
+    return {"ms_per_step": ms, "launches": launches, "clocks": clocks, "n_local": me.n(),
+            "launches_per_step_rank0": sum(s["launches"] for s in st), "transport": me.transport,
+            "single_gpu": single}
+
+
+def c5_config(args, world):
+    return {"workload": f"C5: 512^3 sparse MLS-MPM, {args.c5_particles} particles in a 460x66x66-cell bar "
+                        "with x-velocity shear; pointer(16^3)->bitmasked(8^3)->dense(4^3); one step = "
+                        "DEACTIVATE, P2G, halo reduce, GRID_OP, halo fill, G2P + migration",
+            "parallelism": f"x-slabs{world}", "l2": "inputs (1 GB of particles) larger than L2"}
 
 
 def main():
@@ -550,13 +627,16 @@ def main():
     ap.add_argument("--impl", default="sg", choices=["sg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C1/C3 lines and the XL rooflines")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--workload", default=None, choices=["c2", "c5"],
+                    help="default: c2 on one GPU (BASELINE configs[1]), c5 (the sharded config) on N > 1")
     ap.add_argument("--c5-particles", type=int, default=16_000_000)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload is None:
+        args.workload = "c2" if world == 1 else "c5"
 
     base_cfg = {"workload": "C2: 3D sparse Jacobi 256^3, pointer(8^3)->bitmasked(4^3)->dense(8^3), "
                             "block-ball R=68 (3280 of 32768 leaf blocks, 10.0%), 50 iterations + reduction",
@@ -567,13 +647,17 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_baseline(args)
-        cb_line = dict(cb)
-        out = {"metric": "sparse-grid steps/s (C2 solves/s)", "value": cb["value"], "unit": "solves/s",
+        if args.workload == "c5":
+            cb = cpu_baseline_c5(args)
+            metric, unit, cfg = "sparse-grid steps/s (C5 MPM steps/s)", "steps/s", c5_config(args, world)
+        else:
+            cb = cpu_baseline(args)
+            metric, unit, cfg = "sparse-grid steps/s (C2 solves/s)", "solves/s", base_cfg
+        out = {"metric": metric, "value": cb["value"], "unit": unit,
                "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-               "higher_is_better": True, "dtype": "f64", "data": "synthetic", "config": base_cfg,
-               "cpu_baseline": cb_line,
-               "e2e": {"value": cb["value"], "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+               "higher_is_better": True, "dtype": "f64", "data": "synthetic", "config": cfg,
+               "cpu_baseline": dict(cb),
+               "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return
 
@@ -588,11 +672,10 @@ def main():
                    "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                    "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
                    "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                   "config": {"workload": f"C5: 512^3 sparse MLS-MPM, {args.c5_particles} particles in a "
-                                          "460x66x66-cell bar with x-velocity shear; pointer(16^3)->bitmasked(8^3)"
-                                          "->dense(4^3)", "parallelism": f"x-slabs{world}",
-                              "l2": "inputs (1 GB of particles) larger than L2"},
+                   "config": c5_config(args, world),
                    "gpu_launches": r["launches"], "launches_per_step_rank0": r["launches_per_step_rank0"],
+                   "transport": r["transport"],
+                   "single_gpu_same_run": r["single_gpu"],
                    "clocks": r["clocks"]}
             print(json.dumps(out))
         if world > 1:

@@ -50,7 +50,8 @@ enum {
   SG_ERR_OVERFLOW = -7,        /* reserved */
   SG_ERR_POOL_EXHAUSTED = -8,  /* device: pointer pool has no free container */
   SG_ERR_LIST_OVERFLOW = -9,   /* device: element list exceeded its capacity */
-  SG_ERR_STATE = -10           /* call not valid in this state (e.g. plan-only grid) */
+  SG_ERR_STATE = -10,          /* call not valid in this state (e.g. plan-only grid) */
+  SG_ERR_TIMEOUT = -11         /* device: a neighbour rank's exchange signal never arrived */
 };
 
 /* --- SNode tree (Fig. 2 caption; section 4) ---------- */
@@ -87,18 +88,36 @@ typedef struct {
   void* alloc_ctx;
   int64_t pool_capacity;   /* max containers per pointer level; 0 = every pointer cell */
   int64_t list_capacity;   /* max entries of any element list; 0 = derived from pools */
+  /* multi-GPU exchange buffers (sg_dist_init), in 4-byte words per buffer
+   * including a 4-word header (word 0 = record count): halo buffers (kinds 0, 1)
+   * and particle-migration buffers (kind 2); 0 = 4 + 1 Mi words */
+  int64_t dist_halo_words;
+  int64_t dist_part_words;
 } sg_opts;
 
 typedef struct sg_grid sg_grid;
 
-/* Validates the tree, derives the container layout and allocates: per pointer
- * level a pool of containers (zeroed: zero-on-free invariant), per sparse level
- * a list buffer with a device-side count, and the device error word. */
+/* Validates the tree (power-of-two extents, places only at
+ * leaves, one ndim per chain), derives the container layout (PAPER.md:148
+ * Fig. 2, "dense, bitmasked, pointer") and allocates: per pointer
+ * level a pool of containers (zeroed: the zero-on-free reading of PAPER.md:157
+ * "zero-fill the initial data"), per sparse level a list buffer with a
+ * device-side count (PAPER.md:143 element lists), and the device error word.
+ * The memory allocator is a state of the program ("Allocator").
+ * nodes: n host rows (read during the call).  *out receives the grid; on error
+ * *out = NULL and nothing is allocated.  Errors: SG_ERR_LAYOUT (invalid tree,
+ * sg_last_error says which rule), SG_ERR_CUDA (allocation). */
 sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_opts* opts, sg_grid** out);
+/* Waits for the grid's stream and frees everything the grid allocated (pools,
+ * lists, cached plans and CUDA graphs, exchange buffers; mapped peer buffers
+ * are unmapped).  Borrowed buffers are not touched.  NULL is a no-op. */
 sg_status sg_destroy(sg_grid* g);
 
 /* Registers an external SoA particle array (ncomp components of n elements,
- * component c at dev_ptr + c*n) as a Value state usable by range-for ops. */
+ * component c at dev_ptr + c*n, 4-byte elements, device memory, borrowed) as a
+ * Value state usable by range-for ops ("Value" states of the
+ * state-flow graph; particles are range-for operands, PAPER.md:444 MPM).
+ * *id receives the array id.  Errors: SG_ERR_ARG. */
 sg_status sg_register_array(sg_grid* g, void* dev_ptr, int64_t n, int32_t dtype, int32_t ncomp, int32_t* id);
 /* Gives array `id` a device-resident element count (int32 at dev_count,
  * borrowed; <= the registered n, which becomes the capacity).  Range-for tasks
@@ -171,7 +190,8 @@ enum {
   SG_OP_HALO_PACK = 23, SG_OP_HALO_UNPACK = 24, SG_OP_G2P_MIGRATE = 25, SG_OP_MIGRATE_APPEND = 26,
   SG_OP_LOSS_MEAN = 27, SG_OP_ADJ_INIT = 28, SG_OP_G2P_ADJ = 29, SG_OP_P2G_ADJ = 30,
   SG_OP_SMOOTH_RB = 31, SG_OP_RESTRICT = 32, SG_OP_PROLONG = 33, SG_OP_RESID_NORM2 = 34,
-  SG_OP_DOT = 35, SG_OP_AXPY_RATIO = 36, SG_OP_XPAY_RATIO = 37, SG_OP_COPY_SCALAR = 38
+  SG_OP_DOT = 35, SG_OP_AXPY_RATIO = 36, SG_OP_XPAY_RATIO = 37, SG_OP_COPY_SCALAR = 38,
+  SG_OP_DIST_SIGNAL = 40, SG_OP_DIST_WAIT = 41   /* exchange tasks (sg_dist_init) */
 };
 
 typedef struct {
@@ -193,16 +213,22 @@ sg_status sg_activate(sg_grid* g, int32_t field, const int32_t* dev_coords, int6
 /* Enqueue: generate the element lists of every sparse level from the top of
  * snode's chain down to snode. */
 sg_status sg_listgen(sg_grid* g, int32_t snode);
-/* Enqueue one kernel-level task (struct-for / range-for / serial). */
+/* Enqueue one kernel-level task (PAPER.md:138-143 struct-for over the active
+ * elements of a leaf; range-for and serial tasks, "kernels are
+ * decomposed into tasks").  t is read during the call; operand device buffers
+ * (registered arrays) are borrowed.  Validation errors (unknown op, operand
+ * count, dtype or tree mismatch) return SG_ERR_ARG at enqueue time. */
 sg_status sg_struct_for(sg_grid* g, const sg_task* t);
 /* Enqueue n tasks (host array, borrowed for the call) in order: the same as n
  * sg_struct_for calls, one library call (a solver loop re-submitted each step). */
 sg_status sg_struct_for_batch(sg_grid* g, const sg_task* tasks, int32_t n);
 
 enum { SG_CLEAR_VALUES = 0, SG_DEACTIVATE = 1 };
-/* Enqueue: SG_CLEAR_VALUES: target = field id, store 0 on every active cell.
+/* Enqueue: SG_CLEAR_VALUES: target = field id, store 0 on every active cell
+ *          (a complete overwrite: earlier stores become dead).
  *          SG_DEACTIVATE:   target = sparse snode id, every cell of that level
- *          and below becomes inactive, payload zeroed, pointer children freed. */
+ *          and below becomes inactive, payload zeroed, pointer children freed
+ *          (PAPER.md:166 deactivation, PAPER.md:200 allocator state). */
 sg_status sg_clear(sg_grid* g, int32_t target, int32_t mode);
 
 /* Pass toggles.  sg_flush replays a cached plan as a CUDA
@@ -243,35 +269,51 @@ typedef struct {
                                    positions and the bin geometry are unchanged) */
 } sg_stats;
 
-/* Optimize and launch the queue.  passes = 0 launches one kernel per lowered
- * task in program order (the eager baseline).  observed: field ids whose final
+/* Optimize and launch the queue (section 7.1: the queued
+ * tasks form the state-flow graph, the passes of section 6 run, the plan is
+ * cached by the stream's hash like the IR bank).  passes = 0 launches one
+ * kernel per lowered task in program order (the eager baseline).  Returns
+ * after enqueueing (no synchronization).  observed: field ids whose final
  * values the caller will read (NULL / n_observed < 0: every field and array);
  * masks are always observed.  out may be NULL. */
 sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observed, int32_t n_observed, sg_stats* out);
-/* Wait for the grid's stream; report a latched device error. */
+/* Synchronization point ("until synchronization"): waits for the
+ * grid's stream and reports a latched device error (SG_ERR_POOL_EXHAUSTED,
+ * SG_ERR_LIST_OVERFLOW, SG_ERR_DEMOTION_TRAP, SG_ERR_RANGE, SG_ERR_TIMEOUT)
+ * with the launch index of the task that raised it (sg_last_error). */
 sg_status sg_sync(sg_grid* g);
 
-/* Exports (flush + sync).  Coordinates are level-global (row-major n x ndim). */
+/* Exports (flush + sync: "anything we need to output" is a sync point,
+ * PAPER.md:390).  Coordinates are level-global (row-major n x ndim, host
+ * memory of cap rows; *count = the full count even when it exceeds cap).
+ * The mask export is the set of active cells of a sparse level (PAPER.md:152
+ * activation), the list export the element list, both compared
+ * as sorted sets (reading R1/R2). */
 sg_status sg_export_mask(sg_grid* g, int32_t snode, int32_t* host_coords, int64_t cap, int64_t* count);
 sg_status sg_export_list(sg_grid* g, int32_t snode, int32_t* host_coords, int64_t cap, int64_t* count);
-/* Dense bounding array of a field (row-major, last axis fastest); inactive -> 0. */
+/* Dense bounding array of a field (row-major, last axis fastest, bytes = 4 x
+ * cells); inactive -> 0 (PAPER.md:195 reads of inactive cells return 0). */
 sg_status sg_read_field(sg_grid* g, int32_t field, void* host_dense, int64_t bytes);
 /* Enqueue (no flush, no sync) the device-to-host copy of a 0-D field's 4 bytes
  * into host_dst, ordered after everything flushed so far on the grid's stream.
  * host_dst should be pinned (else the copy is synchronous); it is valid once
  * the stream reaches this point (sg_sync, or an event the caller records). */
 sg_status sg_read_scalar_async(sg_grid* g, int32_t field, void* host_dst);
-/* State handoff: overwrite the values of the ACTIVE cells of a field from a
- * dense host array (inactive entries ignored). */
+/* State handoff (SURVEY.md s8c reading 17, sg_load_state): overwrite the
+ * values of the ACTIVE cells of a field from a dense host array (inactive
+ * entries ignored; masks unchanged).  Flushes and synchronizes first. */
 sg_status sg_load_field(sg_grid* g, int32_t field, const void* host_dense, int64_t bytes);
 
-/* The launch plan of the last flush, for host-side tests: `count` records of
- * 6 int32 {group, task_type, call_index, snode, activating, flags}.  task_type:
+/* The launch plan of the last flush (the optimized SFG's launch order,
+ * PAPER.md:212-254), for host-side tests: `count` records of
+ * 6 int32 {group, task_type, call_index, snode, activating, op} (op: the
+ * sg_task op of struct-for / range-for / serial tasks, else 0).  task_type:
  * 0 activate, 1 listgen, 2 clear_list, 3 struct_for, 4 range_for, 5 serial,
  * 6 deactivate.  call_index = index of the enqueue call within the flush window. */
 sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count);
 
-/* Launch profiling for benchmarks: when on, sg_flush records a CUDA event pair
+/* Launch profiling for benchmarks (launch counts and times are the quantities
+ * PAPER.md:411-424 Table 1 reports): when on, sg_flush records a CUDA event pair
  * on the grid's stream around every launch group.  sg_profile_read waits for
  * the stream and returns, per launch kind, the summed device time (ms) and the
  * number of launches since the last read (kinds: 0 activate, 1 listgen,
@@ -281,10 +323,65 @@ sg_status sg_last_plan(sg_grid* g, int32_t* out, int64_t cap, int64_t* count);
 sg_status sg_set_profiling(sg_grid* g, int32_t on);
 sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int32_t n_kinds);
 
-/* Device pointer of the payload pool / counters, for benchmarks (read-only). */
+/* Device pointers of the leaf payload pools (the SNode layout of PAPER.md:148),
+ * for benchmarks (read-only): out[0] = number of trees, then 4 values per tree
+ * (pool base, stride words, capacity, payload offset words). */
 sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
 
+/* Thread-local message of the last failing call on this thread (SPEC.md:50,
+ * :59, :78 error conventions). */
 const char* sg_last_error(void);
+
+/* --- multi-GPU data plane (BASELINE north_star "partitioned
+ * ... into spatial slabs ... with boundary-block halo exchange"; N3 peer
+ * memory over NVLink).  The paper itself is single-device.
+ *
+ * sg_dist_init makes the grid rank `rank` of `world` ranks partitioned along
+ * `axis` (0 = x); its neighbours are rank-1 (left) and rank+1 (right).  It
+ * allocates the exchange arena (sizes from sg_opts.dist_*_words), registers 12
+ * arrays (send and receive buffer per exchange kind x side, each with a device
+ * count in its header word; ids from sg_dist_info) and connects the
+ * neighbours:
+ *   nccl_uid != NULL: a 128-byte ncclUniqueId shared by every rank (the caller
+ *     broadcasts it, e.g. over torch.distributed).  The library creates the
+ *     NCCL communicator, exchanges IPC handles of the arenas over it and maps
+ *     each neighbour's arena when the devices can access each other (NVLink /
+ *     NVSwitch): the PEER transport -- packing kernels store their records and
+ *     counts straight into the neighbour's receive buffer, so exactly the
+ *     packed bytes move and no host ever sees a count.  Otherwise (or with
+ *     SG_DIST_TRANSPORT=nccl) the NCCL transport: ncclSend/ncclRecv of whole
+ *     buffers on the grid's stream.
+ *   nccl_uid == NULL: no NCCL.  Either an in-process group (virtual ranks,
+ *     e.g. several grids on one GPU): grids calling sg_dist_init with ranks
+ *     0..world-1 in order form a group and map each other's arenas directly
+ *     (peer transport) -- or, one rank per process, the caller exchanges the
+ *     256-byte sg_dist_peer_info blobs over any process group (e.g. gloo) and
+ *     passes all of them to sg_dist_connect (peer transport through CUDA IPC).
+ * Exchange tasks (serial ops, never fused or removed by the passes):
+ *   SG_OP_DIST_SIGNAL  p0 = kind: release the neighbours (their receive buffer
+ *     of that kind is complete); arrays [sendL, sendR, recvL, recvR].
+ *   SG_OP_DIST_WAIT    p0 = kind: wait until both neighbours signalled that kind
+ *     (device-side spin, SG_ERR_TIMEOUT after 30 s); NCCL transport: the
+ *     send/recv of that kind.  Same arrays.
+ * Every rank must enqueue the same exchange sequence (SPMD).  Virtual ranks on
+ * one stream must flush after each SIGNAL and enqueue every rank's SIGNAL of a
+ * kind before any rank's WAIT of it.  Errors: SG_ERR_ARG, SG_ERR_STATE (called
+ * twice), SG_ERR_NCCL, SG_ERR_CUDA. */
+sg_status sg_dist_init(sg_grid* g, int32_t rank, int32_t world, const void* nccl_uid, int32_t axis);
+/* out (n >= 16 int32): [0] transport (0 none, 1 peer, 2 nccl), [1] rank,
+ * [2] world, [3] axis, [4 + 2k + s] send array id of kind k side s,
+ * [10 + 2k + s] receive array id (on a side without a neighbour the arrays
+ * exist but nothing arrives: counts stay 0). */
+sg_status sg_dist_info(sg_grid* g, int32_t* out, int32_t n);
+/* ncclGetUniqueId into out (128 bytes), for rank 0 to broadcast. */
+sg_status sg_nccl_unique_id(void* out);
+/* This rank's 256-byte connection blob (IPC handle of its exchange arena,
+ * PCI bus id, host, pid) after sg_dist_init(nccl_uid = NULL). */
+sg_status sg_dist_peer_info(sg_grid* g, void* out);
+/* Connects the neighbours from every rank's blob (world x 256 bytes, rank
+ * order): maps their arenas (peer transport).  SG_ERR_CUDA when a neighbour
+ * cannot be mapped (other host, same process, no peer access). */
+sg_status sg_dist_connect(sg_grid* g, const void* all_infos);
 
 #ifdef __cplusplus
 }

@@ -7,8 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsg.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["kernels.cu", "sg_api.cu", "planner.cpp"]
-DEPS = SOURCES + ["sg_internal.h", "planner.h", "mpm_ops.cuh", "struct_for.cuh", "exchange_ops.cuh", "mpm_adj.cuh", "mpm_bin.cuh", "../../include/sg.h"]
+SOURCES = ["kernels.cu", "sg_api.cu", "planner.cpp", "dist.cu"]
+DEPS = SOURCES + ["grid.h", "sg_internal.h", "planner.h", "mpm_ops.cuh", "struct_for.cuh", "exchange_ops.cuh", "mpm_adj.cuh", "mpm_bin.cuh", "../../include/sg.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -40,7 +40,7 @@ def build(force=False, verbose=False):
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", LIB] + objs
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -144,6 +144,12 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
       for (int i = 0; i < 5; i++) A(i, R_RW, AC_DATA);
       A(5, R_READ, AC_DATA); A(6, R_READ, AC_DATA);
       break;
+    case SG_OP_DIST_SIGNAL:   // send buffers complete -> the neighbours' receive buffers
+      A(0, R_READ, AC_DATA); A(1, R_READ, AC_DATA); A(2, R_WRITE, AC_DATA); A(3, R_WRITE, AC_DATA);
+      break;
+    case SG_OP_DIST_WAIT:
+      A(0, R_READ, AC_DATA); A(1, R_READ, AC_DATA); A(2, R_RW, AC_DATA); A(3, R_RW, AC_DATA);
+      break;
     default: break;
   }
   return u;
@@ -163,6 +169,7 @@ static int op_min_fields(int op) {
     case SG_OP_AXPY: case SG_OP_JACOBI: return 3;
     case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: case SG_OP_G2P_MIGRATE: return 4;
     case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: return 0;
+    case SG_OP_DIST_SIGNAL: case SG_OP_DIST_WAIT: return 0;
     case SG_OP_LOSS_MEAN: return 1;
     case SG_OP_SMOOTH_RB: case SG_OP_PROLONG: return 2;
     case SG_OP_RESTRICT: case SG_OP_RESID_NORM2: case SG_OP_DOT: return 3;
@@ -247,6 +254,14 @@ void task_meta(const HLayout& L, PTask& t) {
             add_activation_states(L, L.field_tree[id], t.in, t.out);
         }
       }
+      if (t.t.op == SG_OP_DIST_SIGNAL || t.t.op == SG_OP_DIST_WAIT) {
+        // every exchange task reads and writes one sequence state: the passes
+        // keep exchanges in program order on every rank (no cross-rank
+        // deadlock from a reordered wait)
+        const int64_t seq = skey(ST_ARRAY, 0x7ffffff0);
+        t.in.push_back({seq, AC_NONE, false});
+        t.out.push_back({seq, AC_NONE, false});
+      }
     } break;
     default: break;
   }
@@ -285,6 +300,11 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
   switch (t.op) {
     case SG_OP_ARRAY_COUNT:
       if (t.kind != SG_TASK_SERIAL || t.arrays[0] < 0) { err = "ARRAY_COUNT is a serial op on arrays[0]"; return SG_ERR_ARG; }
+      return SG_OK;
+    case SG_OP_DIST_SIGNAL:
+    case SG_OP_DIST_WAIT:
+      if (t.kind != SG_TASK_SERIAL) { err = "exchange tasks are serial ops"; return SG_ERR_ARG; }
+      if (!(t.params[0] == 0.0f || t.params[0] == 1.0f || t.params[0] == 2.0f)) { err = "exchange kind (p0) must be 0, 1 or 2"; return SG_ERR_ARG; }
       return SG_OK;
     case SG_OP_MIGRATE_APPEND:
     case SG_OP_HALO_UNPACK:
@@ -440,6 +460,8 @@ int lower_call(const HLayout& L, const UserCall& c, int call, bool faithful, std
         t.type = TT_RANGE_FOR; t.n = c.t.range_n;
       } else {
         t.type = TT_SERIAL;
+        // exchanges are collective with the neighbour ranks: never removed
+        t.pinned = c.t.op == SG_OP_DIST_SIGNAL || c.t.op == SG_OP_DIST_WAIT;
       }
       out.push_back(t);
     } break;
@@ -711,6 +733,9 @@ static bool pass_fusion(const HLayout& L, std::vector<PTask>& seq, PlanStats& st
                    op == SG_OP_G2P;
           };
           if (solo(A.t.op) || solo(B.t.op)) continue;
+        } else if (A.type == TT_SERIAL) {
+          auto xchg = [](int op) { return op == SG_OP_DIST_SIGNAL || op == SG_OP_DIST_WAIT; };
+          if (xchg(A.t.op) || xchg(B.t.op)) continue;
         }
         // no path of length >= 2
         bool long_path = false;

@@ -11,6 +11,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "grid.h"
 #include "planner.h"
 #include "sg_internal.h"
 
@@ -23,91 +24,13 @@ static sg_status fail(sg_status code, const std::string& msg) {
   return code;
 }
 
+void sg_internal_set_error(const char* msg) { g_err = msg; }
+
 #define CUDA_TRY(x)                                                               \
   do {                                                                            \
     cudaError_t e_ = (x);                                                         \
     if (e_ != cudaSuccess) return fail(SG_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
   } while (0)
-
-struct sg_grid {
-  sg_opts opts{};
-  cudaStream_t stream = nullptr;
-  bool plan_only = false;
-  HLayout L;
-  std::vector<DTree> dtrees;
-  std::vector<std::vector<DList>> lists;   // [tree][chain position]
-  std::vector<DArray> arrays;
-  std::vector<void*> allocs;
-  DevCtx ctx{};
-  DTree* d_trees = nullptr;
-  DField* d_fields = nullptr;
-  DArray* d_arrays = nullptr;
-  int d_arrays_cap = 0;
-  // flush window
-  std::vector<PTask> eager;
-  int ncalls = 0;
-  std::vector<std::pair<const int32_t*, int64_t>> coords_seen;
-  std::unordered_map<uint64_t, Plan> cache;
-  std::vector<PlanRecord> last_plan;
-  int64_t task_counter = 0;         // launch index inside the current flush (error reports)
-  // CUDA graphs: a plan that already ran once is captured (on a private
-  // stream), instantiated once per plan and updated in place afterwards, and
-  // replayed with one cudaGraphLaunch on the user stream
-  bool use_graphs = true;           // SG_NO_GRAPH=1 disables
-  cudaStream_t user_stream = nullptr;
-  cudaStream_t cap_stream = nullptr;
-  std::unordered_map<uint64_t, cudaGraphExec_t> gexec;
-  std::unordered_map<uint64_t, int64_t> gaux;   // aux kernels captured in each plan's graph
-  std::unordered_map<uint64_t, uint64_t> gsig;   // launch-argument signature of each exec's last capture
-  std::unordered_map<uint64_t, int> plan_runs;
-  int num_sms = 148;
-  char* chain_buf = nullptr;        // SG_PASS_CHAIN op tables
-  size_t chain_bytes = 0;
-  std::vector<char> chain_host;
-  uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
-  uint64_t mig_tiles = 0;
-  uint32_t* mig_ctl = nullptr;
-  // particle bins (binned MPM kernels) + a one-entry cache keyed by the
-  // position array, its write epoch, the tree and the range
-  DBins bins{};
-  int64_t bin_cap = 0;
-  uint32_t bin_keys_cap = 0;
-  bool bin_valid = false;
-  int bin_xarr = -1, bin_nb[3] = {0, 0, 0};
-  float bin_inv_dx = 0.0f;
-  uint64_t bin_epoch = 0;
-  int64_t bin_n = 0;
-  const int32_t* bin_dcount = nullptr;
-  bool no_bin = false;                 // SG_NO_BIN=1: per-particle kernels (A/B measurements)
-  std::vector<uint64_t> arr_epoch;     // bumped by every launched task that writes the array
-  // launch profiling (benchmarks): event pairs per launch group
-  bool profiling = false;
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
-  std::vector<cudaEvent_t> event_pool;
-  cudaEvent_t get_event() {
-    if (!event_pool.empty()) { cudaEvent_t e = event_pool.back(); event_pool.pop_back(); return e; }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    return e;
-  }
-
-  void* dev_alloc(size_t bytes) {
-    if (bytes == 0) bytes = 4;
-    void* p = nullptr;
-    if (opts.alloc) p = opts.alloc(opts.alloc_ctx, bytes, (void*)user_stream);
-    else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
-    if (p) allocs.push_back(p);
-    return p;
-  }
-  ~sg_grid() {
-    for (auto& p : prof_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
-    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
-    for (void* p : allocs) {
-      if (opts.free) opts.free(opts.alloc_ctx, p, (void*)stream);
-      else cudaFree(p);
-    }
-  }
-};
 
 static int ilog2i(int64_t v) {
   int r = 0;
@@ -444,6 +367,7 @@ extern "C" sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_o
 extern "C" sg_status sg_destroy(sg_grid* g) {
   if (!g) return SG_OK;
   if (!g->plan_only) cudaStreamSynchronize(g->stream);
+  sg_dist_destroy(g);
   for (auto& kv : g->gexec)
     if (kv.second) cudaGraphExecDestroy(kv.second);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -749,6 +673,11 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt, gt2, bp);
     } break;
     case TT_SERIAL: {
+      if (t0.t.op == SG_OP_DIST_SIGNAL || t0.t.op == SG_OP_DIST_WAIT) {
+        rc = sg_dist_launch(g, t0.t.op, (int)t0.t.params[0], task);
+        if (rc) return rc;
+        break;
+      }
       DOp ops[SG_MAXOPS];
       int nops = (int)members.size();
       for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], -1, ops[i]);
@@ -786,6 +715,10 @@ struct DeviceScope {
   }
   ~DeviceScope() { if (prev >= 0) cudaSetDevice(prev); }
 };
+
+static int plan_op(const PTask& t) {
+  return (t.type == TT_STRUCT_FOR || t.type == TT_RANGE_FOR || t.type == TT_SERIAL) ? t.t.op : 0;
+}
 
 extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observed, int32_t n_observed, sg_stats* out) {
   if (!g) return fail(SG_ERR_ARG, "null grid");
@@ -866,7 +799,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         const auto& acts = plan->acts[gi];
         for (size_t m = 0; m < mem.size(); m++) {
           const PTask& t = g->eager[mem[m]];
-          g->last_plan.push_back({(int)gi, t.type, t.call, t.snode, acts[m], 0});
+          g->last_plan.push_back({(int)gi, t.type, t.call, t.snode, acts[m], plan_op(t)});
         }
         const PTask& t = g->eager[mem[0]];
         st.launches++;
@@ -898,7 +831,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
     const auto& acts = plan->acts[gi];
     for (size_t m = 0; m < mem.size(); m++) {
       const PTask& t = g->eager[mem[m]];
-      g->last_plan.push_back({(int)gi, t.type, t.call, t.snode, acts[m], 0});
+      g->last_plan.push_back({(int)gi, t.type, t.call, t.snode, acts[m], plan_op(t)});
     }
     if (g->plan_only) {
       const PTask& t = g->eager[mem[0]];
@@ -963,7 +896,8 @@ extern "C" sg_status sg_sync(sg_grid* g) {
     const char* what = code == SG_ERR_POOL_EXHAUSTED ? "pool exhausted"
                        : code == SG_ERR_LIST_OVERFLOW ? "list overflow"
                        : code == SG_ERR_DEMOTION_TRAP ? "non-activating write to an inactive cell"
-                       : code == SG_ERR_RANGE ? "coordinate out of range" : "device error";
+                       : code == SG_ERR_RANGE ? "coordinate out of range"
+                       : code == SG_ERR_TIMEOUT ? "a neighbour rank's exchange signal never arrived" : "device error";
     return fail(code, std::string("device: ") + what + " (task " + std::to_string(e[1]) + ")");
   }
   return SG_OK;

@@ -1,25 +1,27 @@
 """x-slab partitioner for sparse MLS-MPM across GPUs.
 
 Rank g of G owns the pointer-cell x-slab [g*Px/G, (g+1)*Px/G) of the grid and
-the particles whose cell x lies in it.  Every step:
+the particles whose cell x lies in it.  Every step, in libsg tasks only:
 
   1. DEACTIVATE, P2G (activating) of the owned particles: contributions reach
      one leaf-block layer beyond each face (the ghost layers);
-     HALO_PACK of the two ghost layers.
-  2. exchange #1 (halo reduce): ghost layers go to their owners, which
-     HALO_UNPACK them with add (activating); GRID_OP; HALO_PACK of the two
-     boundary layers.
-  3. exchange #2 (halo fill): boundary layers overwrite the neighbours' ghost
-     layers (HALO_UNPACK set); G2P_MIGRATE: G2P fused with the stable in-place
-     compaction of the particles that stay, leavers packed per side.
-  4. exchange #3 (migration): MIGRATE_APPEND of the received particles.
+     HALO_PACK of the two ghost layers into the halo-reduce send buffers;
+     DIST_SIGNAL(halo reduce).
+  2. DIST_WAIT(halo reduce); HALO_UNPACK add (activating) of what the
+     neighbours packed; GRID_OP; HALO_PACK of the two boundary layers;
+     DIST_SIGNAL(halo fill).
+  3. DIST_WAIT(halo fill); HALO_UNPACK store into the ghost layers;
+     G2P_MIGRATE: G2P fused with the stable in-place compaction of the
+     particles that stay, leavers appended to the migration send buffers;
+     DIST_SIGNAL(migration).
+  4. DIST_WAIT(migration); MIGRATE_APPEND of the received particles.
 
-All of it runs in libsg kernels enqueued through the C-ABI; the only
-device-to-device traffic is the three exchanges, each a fixed-capacity buffer
-per side whose first word is the device-side record count (no host sync).
-Transports: `DistTransport` (torch.distributed P2P: NCCL over NVLink on GPUs,
-gloo on CPU) and `LocalTransport` (several virtual ranks in one process on one
-GPU, buffers copied device-to-device -- what the single-GPU tests drive).
+The library moves the bytes (sg_dist_init, include/sg.h): on the peer
+transport the send buffers ARE the neighbours' receive buffers (NVLink peer
+memory, or the same allocation for virtual ranks), so packing kernels store
+straight into the neighbour and only device flags synchronize; on the NCCL
+transport DIST_WAIT is an ncclSend/ncclRecv pair per neighbour.  This module
+holds only the partition arithmetic and the task sequence.
 """
 from __future__ import annotations
 
@@ -28,6 +30,7 @@ import numpy as np
 from . import sg
 
 PREC_WORDS = 17   # particle record: x3 v3 C9 J1 id1 (exchange_ops.cuh)
+HALO, FILL, PART = 0, 1, 2   # exchange kinds (sg_dist_init)
 
 
 class SlabPartition:
@@ -37,10 +40,12 @@ class SlabPartition:
         if ptr_cells_x % world:
             raise ValueError(f"{ptr_cells_x} pointer slabs do not split over {world} ranks")
         self.n_grid, self.world, self.block = n_grid, world, block
+        self.ptr_cells_x = ptr_cells_x
         per = ptr_cells_x // world
         cells_per_ptr = n_grid // ptr_cells_x
         self.lo = [r * per * cells_per_ptr for r in range(world)]
         self.hi = [(r + 1) * per * cells_per_ptr for r in range(world)]
+        self.ptr_slabs = [list(range(r * per, (r + 1) * per)) for r in range(world)]
 
     def owner(self, cell_x):
         cell_x = np.asarray(cell_x)
@@ -59,65 +64,42 @@ class SlabPartition:
         B = self.block
         return (self.lo[r], self.lo[r] + B), (self.hi[r] - B, self.hi[r])
 
-    def exchange_pairs(self):
-        """(src, dst, side) for one exchange: side 'L' = src's left buffer."""
-        out = []
-        for r in range(self.world):
-            left, right = self.neighbours(r)
-            if left is not None:
-                out.append((r, left, "L"))
-            if right is not None:
-                out.append((r, right, "R"))
-        return out
+    def migration_bounds(self, r):
+        """Cell-x bounds of G2P_MIGRATE: particles whose cell x leaves [lo, hi)
+        go left / right (open-ended at the outer ranks)."""
+        lo = -1e9 if r == 0 else float(self.lo[r])
+        hi = 1e9 if r == self.world - 1 else float(self.hi[r])
+        return lo, hi
 
 
-class LocalTransport:
-    """Virtual ranks in one process: each send buffer is copied into the
-    matching receive buffer of the destination rank (device to device)."""
-
-    def exchange(self, ranks, pairs, kind):
-        for src, dst, side in pairs:
-            send = ranks[src].bufs[kind]["send" + side]
-            recv = ranks[dst].bufs[kind]["recv" + ("R" if side == "L" else "L")]
-            recv.copy_(send, non_blocking=True)
-
-
-class DistTransport:
-    """One rank per process: batched P2P over torch.distributed (NCCL on GPU)."""
-
-    def __init__(self, group=None):
-        import torch.distributed as dist
-        self.dist = dist
-        self.group = group
-
-    def exchange(self, ranks, pairs, kind):
-        dist = self.dist
-        (me,) = ranks.keys()
-        st = ranks[me]
-        ops = []
-        for src, dst, side in pairs:
-            if src == me:
-                ops.append(dist.P2POp(dist.isend, st.bufs[kind]["send" + side], dst, self.group))
-            if dst == me:
-                ops.append(dist.P2POp(dist.irecv, st.bufs[kind]["recv" + ("R" if side == "L" else "L")], src,
-                                      self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+def halo_record_words(n_fields=4, block_cells=64):
+    return 4 + n_fields * block_cells
 
 
 class RankState:
-    """One rank: its grid, particle arrays with a device count, exchange buffers."""
+    """One rank: its grid (with the library's exchange buffers), particle
+    arrays with a device count."""
 
     def __init__(self, rank, part, desc, fields, grid_leaf, ptr_level, particles, capacity, halo_cap, mig_cap,
-                 device, stream=None):
-        import torch
+                 device, stream=None, plan_only=False):
         self.rank, self.part = rank, part
-        self.grid = sg.Grid(desc, device=device.index or 0, stream=stream)
+        self.halo_cap, self.mig_cap = halo_cap, mig_cap
+        self.grid = sg.Grid(desc, device=0 if plan_only else (device.index or 0), stream=stream,
+                            plan_only=plan_only,
+                            dist_halo_words=4 + halo_cap * halo_record_words(),
+                            dist_part_words=4 + mig_cap * PREC_WORDS)
         self.fields = fields
         self.leaf, self.ptr_level = grid_leaf, ptr_level
-        n = particles["x"].shape[1]
         self.capacity = capacity
+        self.plan_only = plan_only
+        g = self.grid
+        if plan_only:
+            self.a = [g.register_array_plan(capacity, nc) for nc in (3, 3, 9, 1, 1)]
+            return
+        import torch
+        n = particles["x"].shape[1]
+        if n > capacity:
+            raise ValueError(f"rank {rank}: {n} particles exceed the capacity {capacity}")
         dev = device
 
         def arr(ncomp, dtype=torch.float32):
@@ -126,39 +108,49 @@ class RankState:
         self.x, self.v, self.C, self.J = arr(3), arr(3), arr(9), arr(1)
         self.id = arr(1, torch.int32)
         self.count = torch.zeros(4, dtype=torch.int32, device=dev)
-        self.x[:, :n] = torch.as_tensor(particles["x"], device=dev)
-        self.v[:, :n] = torch.as_tensor(particles["v"], device=dev)
-        self.C[:, :n] = torch.as_tensor(particles["C"], device=dev)
-        self.J[:, :n] = torch.as_tensor(particles["J"], device=dev)
-        self.id[:, :n] = torch.as_tensor(particles["id"], device=dev)
+        for name in ("x", "v", "C", "J", "id"):
+            getattr(self, name)[:, :n] = torch.as_tensor(np.ascontiguousarray(particles[name]), device=dev)
         self.count[0] = n
-        g = self.grid
         self.a = [g.register_array(t, t.shape[0]) for t in (self.x, self.v, self.C, self.J, self.id)]
         for a in self.a:
             sg.set_array_count(g, a, self.count)
-        # exchange buffers: int32 tensors, word 0 = record count, records from word 4
-        blk_words = 4 + 4 * 64
-        self.halo_rec = blk_words
-        self.bufs = {"halo": {}, "part": {}}
-        self.buf_ids = {"halo": {}, "part": {}}
-        for kind, cap_words in (("halo", halo_cap * blk_words), ("part", mig_cap * PREC_WORDS)):
-            for name in ("sendL", "sendR", "recvL", "recvR"):
-                t = torch.zeros(4 + cap_words, dtype=torch.int32, device=dev)
-                self.bufs[kind][name] = t
-                i = g.register_array(t[4:], 1)
-                sg.set_array_count(g, i, t[:1])
-                self.buf_ids[kind][name] = i
-        self.halo_cap = halo_cap
+
+    def connect(self, world, nccl_uid=None):
+        sg.dist_init(self.grid, self.rank, world, nccl_uid)
+
+    def connect_ipc(self, world, group=None):
+        """One rank per process without NCCL: exchange the connection blobs over
+        torch.distributed (any backend) and map the neighbours' arenas."""
+        import torch.distributed as dist
+        sg.dist_init(self.grid, self.rank, world, None)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, sg.dist_peer_info(self.grid), group=group)
+        sg.dist_connect(self.grid, blobs)
+
+    def ids(self):
+        info = sg.dist_info(self.grid)
+        self.transport = info["transport"]
+        self.send, self.recv = info["send"], info["recv"]
 
     def n(self):
         return int(self.count[0].item())
 
 
 class SlabMPM:
-    """C5-style sharded MPM over G ranks (virtual or real)."""
+    """C5-style sharded MPM over G ranks.
 
-    def __init__(self, n_grid, ptr_cells, particles, world, ranks_here, transport, prm, device_of,
-                 capacity_factor=1.5, halo_cap=2048, mig_cap=16384, streams=None):
+    ranks_here: the ranks this process drives (all of them for virtual ranks on
+    one GPU, [rank] for one rank per process).  connect: "local" (every rank in
+    this process: an in-process group), "nccl" (nccl_uid = the 128-byte id
+    every rank received; the library picks peer memory or NCCL send/recv), or
+    "ipc" (one rank per process, connection blobs exchanged over the default
+    torch.distributed group, peer memory through CUDA IPC).
+    particles: the global particle dict (filtered by owner here) or a callable
+    rank -> that rank's particles (dict with an "id" row)."""
+
+    def __init__(self, n_grid, ptr_cells, particles, world, ranks_here, prm, device_of,
+                 capacity_factor=1.5, halo_cap=2048, mig_cap=16384, streams=None, nccl_uid=None,
+                 n_total=None, plan_only=False, connect=None):
         import workloads as W
         self.world = world
         self.prm = prm
@@ -167,83 +159,135 @@ class SlabMPM:
         self.L, self.lv = L, lv
         f = L.fields
         self.gf = [f["vx"], f["vy"], f["vz"], f["m"]]
-        ids = np.arange(particles["x"].shape[1], dtype=np.int32)
-        cells = np.floor(particles["x"][0].astype(np.float32) * np.float32(prm["inv_dx"])).astype(np.int64)
-        own = self.part.owner(cells)
-        n_total = particles["x"].shape[1]
+        local = {}
+        if plan_only:
+            local = {r: None for r in ranks_here}
+            n_total = n_total or 0
+        elif callable(particles):
+            for r in ranks_here:
+                local[r] = particles(r)
+            if n_total is None:
+                raise ValueError("n_total is needed with per-rank particle generators")
+        else:
+            n_total = particles["x"].shape[1]
+            ids = np.arange(n_total, dtype=np.int32)
+            cells = np.floor(particles["x"][0].astype(np.float32) * np.float32(prm["inv_dx"])).astype(np.int64)
+            own = self.part.owner(cells)
+            for r in ranks_here:
+                sel = own == r
+                p = {k: np.ascontiguousarray(v[:, sel]) for k, v in particles.items() if k != "id"}
+                p["id"] = ids[sel][None]
+                local[r] = p
         cap = int(capacity_factor * n_total / world) + mig_cap
         self.ranks = {}
         for r in ranks_here:
-            sel = own == r
-            p = {k: np.ascontiguousarray(v[:, sel]) for k, v in particles.items()}
-            p["id"] = ids[sel][None]
-            self.ranks[r] = RankState(r, self.part, L.desc(), self.gf, lv[-1], lv[0], p, cap, halo_cap, mig_cap,
-                                      device_of(r), None if streams is None else streams[r])
-        self.transport = transport
-        self.pairs = self.part.exchange_pairs()
+            self.ranks[r] = RankState(r, self.part, L.desc(), self.gf, lv[-1], lv[0], local[r], cap, halo_cap,
+                                      mig_cap, None if plan_only else device_of(r),
+                                      None if streams is None else streams[r], plan_only)
+        # the library connects the neighbours (in-process group: ranks in order)
+        if connect is None:
+            connect = "nccl" if nccl_uid is not None else ("local" if len(self.ranks) == world else "ipc")
+        self.connect_mode = connect
+        for r in sorted(self.ranks):
+            if connect == "ipc":
+                self.ranks[r].connect_ipc(world)
+            else:
+                self.ranks[r].connect(world, nccl_uid if connect == "nccl" else None)
+        for st in self.ranks.values():
+            st.ids()
 
     # --- enqueue helpers -----------------------------------------------------
-    def _pack(self, st, layers):
+    def _xchg_arrays(self, st, kind):
+        return [st.send[(kind, 0)], st.send[(kind, 1)], st.recv[(kind, 0)], st.recv[(kind, 1)]]
+
+    def _pack(self, st, kind, layers):
         """Reset the send counts and pack the given (left, right) layers."""
         g = st.grid
         nbs = self.part.neighbours(st.rank)
-        ids = st.buf_ids["halo"]
-        for side, nb, rng in (("L", nbs[0], layers[0]), ("R", nbs[1], layers[1])):
+        for side, nb, rng in ((0, nbs[0], layers[0]), (1, nbs[1], layers[1])):
             if nb is None:
                 continue
-            g.task(sg.TASK_SERIAL, "ARRAY_COUNT", arrays=[ids["send" + side]], params=[0.0])
-            g.task(sg.TASK_STRUCT_FOR, "HALO_PACK", st.leaf, self.gf, [ids["send" + side]],
+            g.task(sg.TASK_SERIAL, "ARRAY_COUNT", arrays=[st.send[(kind, side)]], params=[0.0])
+            g.task(sg.TASK_STRUCT_FOR, "HALO_PACK", st.leaf, self.gf, [st.send[(kind, side)]],
                    [float(rng[0]), float(rng[1]), float(st.halo_cap)])
 
-    def _unpack(self, st, mode):
+    def _unpack(self, st, kind, mode):
         g = st.grid
         nbs = self.part.neighbours(st.rank)
-        ids = st.buf_ids["halo"]
-        for side, nb in (("L", nbs[0]), ("R", nbs[1])):
+        for side, nb in ((0, nbs[0]), (1, nbs[1])):
             if nb is not None:
-                g.task(sg.TASK_RANGE_FOR, "HALO_UNPACK", -1, self.gf, [ids["recv" + side]], [float(mode)],
+                g.task(sg.TASK_RANGE_FOR, "HALO_UNPACK", -1, self.gf, [st.recv[(kind, side)]], [float(mode)],
                        [True] * 4, n=0)
 
-    # --- one MPM step on every local rank -------------------------------------
-    def step(self):
+    def _signal(self, st, kind):
+        if self.world > 1:
+            st.grid.task(sg.TASK_SERIAL, "DIST_SIGNAL", arrays=self._xchg_arrays(st, kind), params=[float(kind)])
+
+    def _wait(self, st, kind):
+        if self.world > 1:
+            st.grid.task(sg.TASK_SERIAL, "DIST_WAIT", arrays=self._xchg_arrays(st, kind), params=[float(kind)])
+
+    def phases(self, st):
+        """The step as 4 enqueue functions; an exchange's SIGNAL ends a phase and
+        its WAIT starts the next (virtual ranks flush between them)."""
         prm = self.prm
-        stats = []
-        # phase 1: P2G with ghost contributions, pack ghost layers
-        for st in self.ranks.values():
+
+        def p1():
             g = st.grid
             g.clear(st.ptr_level, sg.DEACTIVATE)
             g.range_for("P2G", -1, self.gf, st.a[:4],
                         [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]], [True] * 4)
-            self._pack(st, self.part.ghost_layers(st.rank))
-            stats.append(g.flush("all"))
-        self.transport.exchange(self.ranks, self.pairs, "halo")          # halo reduce
-        # phase 2: add received ghost contributions, grid update, pack boundary layers
-        for st in self.ranks.values():
+            self._pack(st, HALO, self.part.ghost_layers(st.rank))
+            self._signal(st, HALO)
+
+        def p2():
             g = st.grid
-            self._unpack(st, 0)
+            self._wait(st, HALO)
+            self._unpack(st, HALO, 0)
             g.struct_for("GRID_OP", st.leaf, self.gf, [prm["dt"], prm["gravity"], prm["bound"], prm["n_grid"]])
-            self._pack(st, self.part.boundary_layers(st.rank))
-            stats.append(g.flush("all"))
-        self.transport.exchange(self.ranks, self.pairs, "halo")          # halo fill
-        # phase 3: overwrite ghost layers, G2P + compaction + migration packing
-        for st in self.ranks.values():
+            self._pack(st, FILL, self.part.boundary_layers(st.rank))
+            self._signal(st, FILL)
+
+        def p3():
             g = st.grid
-            self._unpack(st, 1)
-            pid = st.buf_ids["part"]
-            for side in ("L", "R"):
-                g.task(sg.TASK_SERIAL, "ARRAY_COUNT", arrays=[pid["send" + side]], params=[0.0])
-            lo, hi = self.part.lo[st.rank], self.part.hi[st.rank]
-            lo_f = -1e9 if st.rank == 0 else float(lo)
-            hi_f = 1e9 if st.rank == self.world - 1 else float(hi)
-            g.task(sg.TASK_RANGE_FOR, "G2P_MIGRATE", -1, self.gf, st.a + [pid["sendL"], pid["sendR"]],
-                   [prm["dt"], prm["inv_dx"], lo_f, hi_f], n=-1)
-            stats.append(g.flush("all"))
-        if self.world > 1:
-            self.transport.exchange(self.ranks, self.pairs, "part")      # migration
+            self._wait(st, FILL)
+            self._unpack(st, FILL, 1)
+            for side in (0, 1):
+                g.task(sg.TASK_SERIAL, "ARRAY_COUNT", arrays=[st.send[(PART, side)]], params=[0.0])
+            lo_f, hi_f = self.part.migration_bounds(st.rank)
+            g.task(sg.TASK_RANGE_FOR, "G2P_MIGRATE", -1, self.gf,
+                   st.a + [st.send[(PART, 0)], st.send[(PART, 1)]], [prm["dt"], prm["inv_dx"], lo_f, hi_f], n=-1)
+            self._signal(st, PART)
+
+        def p4():
+            if self.world > 1:
+                self._wait(st, PART)
+                st.grid.task(sg.TASK_RANGE_FOR, "MIGRATE_APPEND", -1, [],
+                             st.a + [st.recv[(PART, 0)], st.recv[(PART, 1)]], n=0)
+
+        return [p1, p2, p3, p4]
+
+    # --- one MPM step on every local rank -------------------------------------
+    def step(self, fused=None):
+        """fused: one flush per step per rank (one rank per process: every
+        exchange is device-side, the whole step is one plan / one CUDA graph);
+        default for a single local rank.  Otherwise (virtual ranks sharing a
+        stream) each phase is flushed on every rank before the next starts."""
+        if fused is None:
+            fused = len(self.ranks) == 1
+        stats = []
+        if fused:
             for st in self.ranks.values():
-                pid = st.buf_ids["part"]
-                st.grid.task(sg.TASK_RANGE_FOR, "MIGRATE_APPEND", -1, [], st.a + [pid["recvL"], pid["recvR"]],
-                             n=0)
+                for ph in self.phases(st):
+                    ph()
+                stats.append(st.grid.flush("all"))
+            return stats
+        per_rank = {r: self.phases(st) for r, st in self.ranks.items()}
+        for k in range(4):
+            if k == 3 and self.world == 1:
+                break
+            for r, st in self.ranks.items():
+                per_rank[r][k]()
                 stats.append(st.grid.flush("all"))
         return stats
 

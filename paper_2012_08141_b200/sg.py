@@ -29,14 +29,15 @@ OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6
        "HALO_PACK": 23, "HALO_UNPACK": 24, "G2P_MIGRATE": 25, "MIGRATE_APPEND": 26,
        "LOSS_MEAN": 27, "ADJ_INIT": 28, "G2P_ADJ": 29, "P2G_ADJ": 30,
        "SMOOTH_RB": 31, "RESTRICT": 32, "PROLONG": 33, "RESID_NORM2": 34,
-       "DOT": 35, "AXPY_RATIO": 36, "XPAY_RATIO": 37, "COPY_SCALAR": 38}
+       "DOT": 35, "AXPY_RATIO": 36, "XPAY_RATIO": 37, "COPY_SCALAR": 38,
+       "DIST_SIGNAL": 40, "DIST_WAIT": 41}
 CLEAR_VALUES, DEACTIVATE = 0, 1
 PASS_LISTGEN_REMOVAL, PASS_ACT_DEMOTION, PASS_FUSION, PASS_DSE = 1, 2, 4, 8
 PASS_ALL = 15
 PASS_CHAIN = 16
 PASS_NAMES = {"none": 0, "all": 15, "listgen": 1, "demotion": 2, "fusion": 4, "dse": 8, "chain": 16}
 ERRORS = {0: "OK", -1: "ARG", -2: "LAYOUT", -3: "RANGE", -4: "CUDA", -5: "NCCL", -6: "DEMOTION_TRAP",
-          -7: "OVERFLOW", -8: "POOL_EXHAUSTED", -9: "LIST_OVERFLOW", -10: "STATE"}
+          -7: "OVERFLOW", -8: "POOL_EXHAUSTED", -9: "LIST_OVERFLOW", -10: "STATE", -11: "TIMEOUT"}
 TASK_TYPES = ["activate", "listgen", "clear_list", "struct_for", "range_for", "serial", "deactivate"]
 
 
@@ -53,7 +54,8 @@ class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("debug", ctypes.c_int32), ("plan_only", ctypes.c_int32),
                 ("lowering", ctypes.c_int32), ("stream", ctypes.c_void_p), ("alloc", ALLOC_FN),
                 ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p), ("pool_capacity", ctypes.c_int64),
-                ("list_capacity", ctypes.c_int64)]
+                ("list_capacity", ctypes.c_int64), ("dist_halo_words", ctypes.c_int64),
+                ("dist_part_words", ctypes.c_int64)]
 
 
 class Task(ctypes.Structure):
@@ -148,7 +150,7 @@ class Grid:
     """One sparse grid behind the C-ABI."""
 
     def __init__(self, desc, device=0, stream=None, plan_only=False, debug=False, faithful=False,
-                 pool_capacity=0, list_capacity=0, torch_alloc=True):
+                 pool_capacity=0, list_capacity=0, torch_alloc=True, dist_halo_words=0, dist_part_words=0):
         d = np.ascontiguousarray(desc, dtype=np.int32)
         self.desc = d
         rows = (SnodeDesc * len(d))()
@@ -164,6 +166,8 @@ class Grid:
         o.lowering = int(faithful)
         o.pool_capacity = pool_capacity
         o.list_capacity = list_capacity
+        o.dist_halo_words = dist_halo_words
+        o.dist_part_words = dist_part_words
         self._keep = []         # borrowed device buffers kept alive until the flush ran
         self._keep_prev = []
         if not plan_only:
@@ -203,6 +207,12 @@ class Grid:
         dt = I32 if str(tensor.dtype) == "torch.int32" else F32
         self._keep.append(tensor)
         _check(_lib.sg_register_array(self.h, _vp(tensor.data_ptr()), n, dt, ncomp, ctypes.byref(i)))
+        return i.value
+
+    def register_array_plan(self, n, ncomp):
+        """Plan-only grids: an array id without memory (planner tests)."""
+        i = ctypes.c_int32()
+        _check(_lib.sg_register_array(self.h, None, n, F32, ncomp, ctypes.byref(i)))
         return i.value
 
     def activate(self, field, coords):
@@ -445,3 +455,60 @@ def profile_read(grid):
     cnt = (ctypes.c_int64 * PROFILE_KINDS)()
     _check(_lib.sg_profile_read(grid.h, ms, cnt, PROFILE_KINDS))
     return {k: (ms[k], cnt[k]) for k in range(PROFILE_KINDS) if cnt[k]}
+
+
+# --- multi-GPU data plane (include/sg.h sg_dist_init) ---------------------------
+_lib.sg_dist_init.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32]
+_lib.sg_dist_init.restype = ctypes.c_int32
+_lib.sg_dist_info.argtypes = [_vp, _P(ctypes.c_int32), ctypes.c_int32]
+_lib.sg_dist_info.restype = ctypes.c_int32
+_lib.sg_nccl_unique_id.argtypes = [_vp]
+_lib.sg_nccl_unique_id.restype = ctypes.c_int32
+_lib.sg_dist_peer_info.argtypes = [_vp, _vp]
+_lib.sg_dist_peer_info.restype = ctypes.c_int32
+_lib.sg_dist_connect.argtypes = [_vp, _vp]
+_lib.sg_dist_connect.restype = ctypes.c_int32
+EXPORTS += ["sg_dist_init", "sg_dist_info", "sg_nccl_unique_id", "sg_dist_peer_info", "sg_dist_connect"]
+TRANSPORTS = {0: "none", 1: "peer", 2: "nccl"}
+DIST_KINDS = {"halo_reduce": 0, "halo_fill": 1, "part": 2}
+
+
+def nccl_unique_id():
+    """128 bytes (ncclGetUniqueId) for rank 0 to broadcast to the other ranks."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.sg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def dist_init(grid, rank, world, nccl_uid=None, axis=0):
+    """sg_dist_init: nccl_uid (bytes) for one rank per process, None for an
+    in-process group of virtual ranks (call for ranks 0..world-1 in order)."""
+    if nccl_uid is None:
+        _check(_lib.sg_dist_init(grid.h, rank, world, None, axis))
+    else:
+        buf = ctypes.create_string_buffer(bytes(nccl_uid), 128)
+        _check(_lib.sg_dist_init(grid.h, rank, world, buf, axis))
+
+
+def dist_peer_info(grid):
+    """256-byte connection blob of this rank (after dist_init with nccl_uid=None)."""
+    buf = ctypes.create_string_buffer(256)
+    _check(_lib.sg_dist_peer_info(grid.h, buf))
+    return buf.raw
+
+
+def dist_connect(grid, blobs):
+    """Map the neighbours' exchange arenas from every rank's blob (rank order)."""
+    data = b"".join(bytes(b) for b in blobs)
+    buf = ctypes.create_string_buffer(data, len(data))
+    _check(_lib.sg_dist_connect(grid.h, buf))
+
+
+def dist_info(grid):
+    """{'transport', 'rank', 'world', 'axis', 'send': {(kind, side): id}, 'recv': {...}}"""
+    out = (ctypes.c_int32 * 16)()
+    _check(_lib.sg_dist_info(grid.h, out, 16))
+    v = list(out)
+    return {"transport": TRANSPORTS.get(v[0], v[0]), "rank": v[1], "world": v[2], "axis": v[3],
+            "send": {(k, s): v[4 + 2 * k + s] for k in range(3) for s in range(2)},
+            "recv": {(k, s): v[10 + 2 * k + s] for k in range(3) for s in range(2)}}

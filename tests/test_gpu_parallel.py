@@ -30,7 +30,7 @@ def particles():
 
 def run_slab(world):
     prm = W.mpm_params(NG)
-    sim = parallel.SlabMPM(NG, PTR, particles(), world, list(range(world)), parallel.LocalTransport(), prm,
+    sim = parallel.SlabMPM(NG, PTR, particles(), world, list(range(world)), prm,
                            lambda r: torch.device("cuda", 0), halo_cap=1024, mig_cap=8192)
     for _ in range(STEPS):
         sim.step()
@@ -76,8 +76,9 @@ def check(sim, prog, o, tol=1e-5):
 def run_slab_from(parts, world):
     prm = W.mpm_params(NG)
     p = dict(parts)
-    sim = parallel.SlabMPM(NG, PTR, p, world, list(range(world)), parallel.LocalTransport(), prm,
+    sim = parallel.SlabMPM(NG, PTR, p, world, list(range(world)), prm,
                            lambda r: torch.device("cuda", 0), halo_cap=1024, mig_cap=8192)
+    assert all(st.transport == "peer" for st in sim.ranks.values())
     sim.step()
     return sim
 

@@ -3,9 +3,10 @@
 * SlabPartition arithmetic: ownership, ghost / boundary layers, exchange pairs;
   the ghost layers cover exactly the P2G/G2P stencil overhang of owned
   particles (base in [lo-1, hi-1], base+2 <= hi+1).
-* DistTransport over torch.distributed with the gloo backend, world size 2:
-  the send buffers of each side arrive in the neighbour's receive buffers
-  (the same code path runs NCCL over NVLink on the GPU box).
+* the library data plane's host side (sg_dist_init on plan-only grids): every
+  rank's plan of a C5 step carries the same exchange sequence, each kind's
+  signal before its wait -- in-process groups (world 1..8, phase-split or one
+  fused flush per step) and one rank per process over gloo, world size 2.
 """
 import os
 import socket
@@ -15,7 +16,7 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from paper_2012_08141_b200.parallel import DistTransport, SlabPartition
+from paper_2012_08141_b200.parallel import SlabPartition
 
 
 def test_partition_layers_cover_stencils():
@@ -36,8 +37,8 @@ def test_partition_layers_cover_stencils():
             assert (br0, br1) == p.ghost_layers(right)[0]
     cells = np.arange(512)
     assert (p.owner(cells) == cells // 64).all()
-    pairs = p.exchange_pairs()
-    assert len(pairs) == 2 * 7 and (0, 1, "R") in pairs and (1, 0, "L") in pairs
+    assert p.migration_bounds(0) == (-1e9, 64.0) and p.migration_bounds(7) == (448.0, 1e9)
+    assert p.neighbours(0) == (None, 1) and p.neighbours(7) == (6, None)
 
 
 def test_partition_rejects_uneven_split():
@@ -45,27 +46,75 @@ def test_partition_rejects_uneven_split():
         SlabPartition(512, 16, 3)
 
 
-class _FakeRank:
-    def __init__(self, r, words):
-        self.bufs = {"halo": {}}
-        for name in ("sendL", "sendR", "recvL", "recvR"):
-            t = torch.zeros(words, dtype=torch.int32)
-            if name.startswith("send"):
-                t[0] = 3 + r          # record count
-                t[4:] = 1000 * r + (1 if name == "sendR" else 2)
-            self.bufs["halo"][name] = t
+EXCHANGE_OPS = {40: "signal", 41: "wait"}
 
 
-def _worker(rank, world, port, q):
+def exchange_sequence(grid):
+    """[(signal|wait), ...] of the last flush's plan, in launch order (the
+    sg_last_plan op column), and the plan's launch count."""
+    plan = grid.last_plan()
+    seq = [EXCHANGE_OPS[int(r[5])] for r in plan if int(r[1]) == 5 and int(r[5]) in EXCHANGE_OPS]
+    return seq, len({int(r[0]) for r in plan})
+
+
+def plan_c5_step(world, ranks, fused, uid=None):
+    """Plan (no device) one sharded C5 step for `ranks` of `world`; returns
+    {rank: [per-flush exchange sequences]}."""
+    import workloads as W
+    from paper_2012_08141_b200 import parallel
+    prm = W.mpm_params(512)
+    sim = parallel.SlabMPM(512, 16, None, world, ranks, prm, None, halo_cap=64, mig_cap=256, n_total=16_000_000,
+                           plan_only=True, nccl_uid=uid, connect="nccl" if uid else None)
+    out = {}
+    for r, st in sim.ranks.items():
+        flushes = []
+        for ph in sim.phases(st):
+            ph()
+            if not fused:
+                st.grid.flush("all")
+                flushes.append(exchange_sequence(st.grid)[0])
+        if fused:
+            st.grid.flush("all")
+            flushes.append(exchange_sequence(st.grid)[0])
+        out[r] = flushes
+    return sim, out
+
+
+def check_sequences(seqs, world):
+    """Every rank enqueues the same exchanges in the same order, each kind's
+    signal before its wait (the SPMD condition under which device-side waits
+    cannot deadlock, include/sg.h)."""
+    flat = {r: [x for f in fl for x in f] for r, fl in seqs.items()}
+    ref = flat[min(flat)]
+    assert ref == ["signal", "wait"] * 3 if world > 1 else ref == []
+    for r, f in flat.items():
+        assert f == ref, (r, f)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("fused", [False, True])
+def test_exchange_plan_in_process_group(world, fused):
+    sim, seqs = plan_c5_step(world, list(range(world)), fused)
+    check_sequences(seqs, world)
+    for st in sim.ranks.values():
+        assert st.transport == ("peer" if world > 1 else "peer")
+        ids = set(st.send.values()) | set(st.recv.values())
+        assert len(ids) == 12 and all(i >= 5 for i in ids)   # after the 5 particle arrays
+
+
+def _plan_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    p = SlabPartition(64, 4, world)
-    st = _FakeRank(rank, 16)
-    DistTransport().exchange({rank: st}, p.exchange_pairs(), "halo")
-    got = {k: st.bufs["halo"][k].tolist() for k in ("recvL", "recvR")}
-    q.put((rank, got))
+    uid = [bytes(range(128)) if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)        # the id every rank receives (plumbing)
+    sim, seqs = plan_c5_step(world, [rank], fused=True, uid=uid[0])
+    seq = seqs[rank][0]
+    st = sim.ranks[rank]
+    everyone = [None] * world
+    dist.all_gather_object(everyone, (seq, st.transport))
+    q.put((rank, everyone))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -78,18 +127,21 @@ def _free_port():
     return port
 
 
-def test_dist_transport_gloo_world2():
+def test_exchange_plans_agree_gloo_world2():
+    """One rank per process (gloo, world 2), each planning its own fused C5
+    step through the library (plan-only grids, sg_dist_init with a broadcast
+    id): both ranks' plans carry the same exchange sequence."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_plan_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in procs)
+    res = dict(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # rank 0 receives rank 1's left send in its right buffer, and vice versa
-    assert res[0]["recvR"][0] == 4 and res[0]["recvR"][4] == 1002
-    assert res[1]["recvL"][0] == 3 and res[1]["recvL"][4] == 1
-    assert res[0]["recvL"] == [0] * 16 and res[1]["recvR"] == [0] * 16   # no neighbour there
+    for r in range(2):
+        seqs = [s for s, _ in res[r]]
+        assert seqs[0] == seqs[1] == ["signal", "wait"] * 3
+        assert [t for _, t in res[r]] == ["nccl", "nccl"]

@@ -557,6 +557,51 @@ def c5_particles(n, n_grid=512, length=460, width=66, seed=0, shear=2.0):
     return {"x": x, "v": v, "C": np.zeros((9, n), dtype=np.float32), "J": np.ones((1, n), dtype=np.float32)}
 
 
+def c5_slab_counts(n, n_grid=512, ptr_cells=16, length=460):
+    """Particles per pointer x-slab of the bar: proportional to the slab's
+    overlap with the bar, largest remainders first (sums to n)."""
+    dx_slab = n_grid / ptr_cells
+    lo, hi = n_grid / 2.0 - length / 2.0, n_grid / 2.0 + length / 2.0
+    ov = np.array([max(0.0, min(hi, (j + 1) * dx_slab) - max(lo, j * dx_slab)) for j in range(ptr_cells)])
+    exact = n * ov / ov.sum()
+    cnt = np.floor(exact).astype(np.int64)
+    rem = n - cnt.sum()
+    cnt[np.argsort(-(exact - cnt), kind="stable")[:rem]] += 1
+    return cnt
+
+
+def c5_slab_particles(n, j, n_grid=512, ptr_cells=16, length=460, width=66, seed=0, shear=2.0):
+    """The particles of pointer x-slab j of the C5 bar (uniform in the slab's
+    part of the bar, x-velocity shear), generated from seed (seed, j) alone:
+    any rank can build its own slabs and every world size sees the same
+    particle set.  ids are global (prefix of the slab counts)."""
+    cnt = c5_slab_counts(n, n_grid, ptr_cells, length)
+    rng = np.random.default_rng([seed, j])
+    dx = 1.0 / n_grid
+    c = n_grid / 2.0
+    x0 = max(c - length / 2.0, j * n_grid / ptr_cells)
+    x1 = min(c + length / 2.0, (j + 1) * n_grid / ptr_cells)
+    k = int(cnt[j])
+    x = np.empty((3, k), dtype=np.float32)
+    x[0] = (x0 + rng.random(k) * (x1 - x0)) * dx
+    x[1:] = ((c - width / 2.0) + rng.random((2, k)) * width) * dx
+    # keep the cell inside the slab under f32 rounding (ownership by floor(x * n))
+    top = np.float32((x1 * dx))
+    x[0] = np.minimum(x[0], np.nextafter(top, np.float32(0)))
+    v = np.zeros((3, k), dtype=np.float32)
+    v[0] = (shear * (x[1] - 0.5) / (width * dx)).astype(np.float32)
+    ids = (np.int64(cnt[:j].sum()) + np.arange(k)).astype(np.int32)[None]
+    return {"x": x, "v": v, "C": np.zeros((9, k), dtype=np.float32), "J": np.ones((1, k), dtype=np.float32),
+            "id": ids}
+
+
+def c5_rank_particles(n, rank, world, n_grid=512, ptr_cells=16, **kw):
+    """Rank `rank`'s particles under the x-slab partition (its pointer slabs)."""
+    per = ptr_cells // world
+    parts = [c5_slab_particles(n, j, n_grid, ptr_cells, **kw) for j in range(rank * per, (rank + 1) * per)]
+    return {k: np.concatenate([p[k] for p in parts], axis=1) for k in parts[0]}
+
+
 def c5_program(n_grid=512, ptr_cells=16, n_particles=16_000_000, steps=1, seed=0, **kw):
     """The unpartitioned C5 problem as a plain program (oracle / 1-GPU reference)."""
     L, lv = c5_layout(n_grid, ptr_cells)
