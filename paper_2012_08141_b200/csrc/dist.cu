@@ -221,6 +221,8 @@ static sg_status dist_register_sends(sg_grid* g) {
       if (rc) return rc;
       if (base && (rc = sg_set_array_count(g, id, (int32_t*)base))) return rc;
       D.ids_send[k][s] = id;
+      if ((int)g->L.seq_arrays.size() <= id) g->L.seq_arrays.resize(id + 1, 0);
+      g->L.seq_arrays[id] = 1;
     }
   return SG_OK;
 }

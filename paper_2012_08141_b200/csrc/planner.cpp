@@ -254,13 +254,24 @@ void task_meta(const HLayout& L, PTask& t) {
             add_activation_states(L, L.field_tree[id], t.in, t.out);
         }
       }
+      const int64_t seq = skey(ST_ARRAY, 0x7ffffff0);
       if (t.t.op == SG_OP_DIST_SIGNAL || t.t.op == SG_OP_DIST_WAIT) {
         // every exchange task reads and writes one sequence state: the passes
         // keep exchanges in program order on every rank (no cross-rank
         // deadlock from a reordered wait)
-        const int64_t seq = skey(ST_ARRAY, 0x7ffffff0);
         t.in.push_back({seq, AC_NONE, false});
         t.out.push_back({seq, AC_NONE, false});
+      } else {
+        // a write into a send buffer (pack, count reset, migration) reads the
+        // sequence: it stays after the exchange before it and before the one
+        // after it.  On the peer transport it lands in the neighbour's receive
+        // buffer, which the neighbour may still be consuming until then.
+        bool ordered = false;
+        for (const OpUse& u : op_uses(t.t)) {
+          int id = u.array ? t.t.arrays[u.slot] : -1;
+          if (id >= 0 && (u.role & R_WRITE) && id < (int)L.seq_arrays.size() && L.seq_arrays[id]) ordered = true;
+        }
+        if (ordered) t.in.push_back({seq, AC_NONE, false});
       }
     } break;
     default: break;

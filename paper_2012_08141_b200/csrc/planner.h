@@ -26,6 +26,10 @@ struct HLayout {
   std::vector<int> field_tree, field_slot, field_dtype, field_scalar;
   std::vector<int> snode_tree, snode_pos;   // tree id / chain index of each level snode
   int n_scalars = 0;
+  // arrays whose writes are ordered against the exchange sequence (the
+  // multi-GPU send buffers: on the peer transport they are the neighbours'
+  // receive buffers, so a write must stay between the same exchanges)
+  std::vector<char> seq_arrays;
   bool is_sparse(int snode) const {
     return nodes[snode].kind == SG_BITMASKED || nodes[snode].kind == SG_POINTER;
   }

@@ -145,3 +145,25 @@ def test_exchange_plans_agree_gloo_world2():
         seqs = [s for s, _ in res[r]]
         assert seqs[0] == seqs[1] == ["signal", "wait"] * 3
         assert [t for _, t in res[r]] == ["nccl", "nccl"]
+
+
+def test_send_buffer_writes_stay_between_their_exchanges():
+    """Peer transport: a send buffer is the neighbour's receive buffer, so the
+    count reset, the pack and the migration writes must not move across an
+    exchange in the optimized plan (a count reset hoisted before the previous
+    WAIT would zero a buffer the neighbour is still appending from)."""
+    sim, _ = plan_c5_step(4, list(range(4)), fused=True)
+    for st in sim.ranks.values():
+        plan = st.grid.last_plan()
+        calls = sorted({int(r[2]): int(r[5]) for r in plan}.items())   # program order: call index -> op
+        checked = 0
+        for pos, r in enumerate(plan):
+            op, call = int(r[5]), int(r[2])
+            if op not in (11, 23, 25):      # ARRAY_COUNT, HALO_PACK, G2P_MIGRATE
+                continue
+            for x in (40, 41):
+                in_plan = sum(1 for q in plan[:pos] if int(q[5]) == x)
+                in_prog = sum(1 for c, o in calls if c < call and o == x)
+                assert in_plan == in_prog, (st.rank, call, op, x, in_plan, in_prog)
+            checked += 1
+        assert checked >= 4
