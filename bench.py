@@ -209,6 +209,8 @@ def run_sg(args, rank, world, device):
         except Exception:
             traffic = None
 
+    l2_peak = measure_l2_peak()
+
     # ---- e2e: through the public API with host buffers ----
     # every step: H2D of the step's block coordinates from pinned host memory
     # into the device input buffer, the solve's tasks (one batched enqueue),
@@ -263,6 +265,7 @@ def run_sg(args, rank, world, device):
         "clocks": clk.summary(), "e2e": e2e_value, "e2e_serial": e2e_serial, "e2e_bytes": (coords.nbytes, 4),
         "s": float(s_host),
         "n_blocks": n_blocks,
+        "l2_peak": l2_peak,
     }
 
 
@@ -350,6 +353,101 @@ def _timed_flushes(grid, enqueue, steps, warmup, l2=None, after_warmup=None):
         b.synchronize()
         ms += a.elapsed_time(b)
     return ms / steps, st
+
+
+def jac_xl_traffic():
+    """ncu DRAM bytes (read + write) per JAC-XL k_jacobi8 launch, from the
+    committed capture summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "jac_xl_dram_bytes.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def measure_c5_1gpu(args):
+    """C5 (512^3, 16M particles) on this one GPU: one fused flush per step."""
+    import torch
+    a = argparse.Namespace(**vars(args))
+    a.steps, a.warmup = 10, 3
+    sim = c5_sim(a, 0, 1, torch.cuda.current_device())
+    ms, launches, _, st = time_c5(sim, a, torch.cuda.current_device(), 1)
+    return {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": launches / a.steps,
+            "particles": args.c5_particles}
+
+
+def measure_l2_peak(mb=16, reps=50):
+    """L2-resident copy bandwidth of this GPU (read + write bytes of a copy of
+    `mb` MB into another `mb` MB buffer, both far below the L2 size; best of
+    `reps`, CUDA events): the denominator of an L2-resident kernel's roofline."""
+    import torch
+    n = mb * 1024 * 1024 // 4
+    a = torch.ones(n, device="cuda")
+    b = torch.empty_like(a)
+    for _ in range(5):
+        b.copy_(a)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return 2 * n * 4 / (best / 1e3) / 1e9
+
+
+def measure_c2_variants(args, device, steps=10, warmup=3):
+    """The C2 solve in four launch modes, L2 flushed before each step: the
+    paper's passes on / off (passes = 0 is the eager one-launch-per-task
+    stream, PAPER.md:62 / Table 1) x CUDA-graph replay on / off (SURVEY.md
+    s8d.4: graphs are an orthogonal column).  solves/s each."""
+    import torch
+    from paper_2012_08141_b200 import sg
+    L, lv, coords, calls, result = c2_setup(args.iters)
+    dc = torch.as_tensor(coords).to(device)
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    out = {}
+    for graphs in (True, False):
+        old = os.environ.pop("SG_NO_GRAPH", None)
+        if not graphs:
+            os.environ["SG_NO_GRAPH"] = "1"
+        try:
+            g = sg.Grid(L.desc(), device=device)
+        finally:
+            os.environ.pop("SG_NO_GRAPH", None)
+            if old is not None:
+                os.environ["SG_NO_GRAPH"] = old
+        for passes in ("all", 0):
+            def enq():
+                enqueue_calls(g, calls, dc)
+            stream = torch.cuda.current_stream()
+            for _ in range(warmup):
+                enq()
+                g.flush(passes)
+            torch.cuda.synchronize()
+            ms = 0.0
+            for _ in range(steps):
+                l2.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                enq()
+                st = g.flush(passes)
+                b.record(stream)
+                b.synchronize()
+                ms += a.elapsed_time(b)
+            ms /= steps
+            key = f"{'optimized' if passes == 'all' else 'eager'}_{'graph' if graphs else 'direct'}"
+            out[key] = {"solves_per_s": 1000.0 / ms, "ms_per_step": ms, "launches": st["launches"]}
+        del g
+    out["speedup_passes_graph"] = out["optimized_graph"]["solves_per_s"] / out["eager_graph"]["solves_per_s"]
+    out["speedup_passes_direct"] = out["optimized_direct"]["solves_per_s"] / out["eager_direct"]["solves_per_s"]
+    out["note"] = ("eager = passes 0 (161 launches: every listgen, both fills, 50 sweeps, clear, reduce); "
+                   "direct = SG_NO_GRAPH (one cudaLaunchKernel per launch group)")
+    return out
 
 
 def measure_c2_chain(steps=20, warmup=5):
@@ -697,9 +795,12 @@ def main():
                                   "tasks_fused": st["tasks_fused"], "dead_removed": st["dead_removed"],
                                   "plan_cache_hit": bool(st["plan_cache_hits"]), "plan_us": st["plan_us"]},
             "gpu_launches": r["launches"],
-            "roofline": {"bound": "hbm", "kernel": "k_jacobi8 (JACOBI, 8^3 blocks)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "peak_source": peak_kind, "traffic": traffic,
+            "roofline": {"bound": "l2", "kernel": "k_jacobi8 (JACOBI, 8^3 blocks)",
+                         "achieved": achieved, "peak": r["l2_peak"], "unit": "GB/s", "frac": achieved / r["l2_peak"],
+                         "peak_source": "measured in this run: L2-resident copy bandwidth (16 MB -> 16 MB)",
+                         "frac_of_hbm_peak": achieved / peak, "hbm_peak": peak, "hbm_peak_source": peak_kind,
+                         "traffic": traffic,
+                         "dram_over_algorithmic": (traffic / jac_bytes) if traffic else None,
                          "algorithmic_bytes_per_launch": jac_bytes, "avg_launch_us": jac_ms * 1e3,
                          "share_of_step": jac_ms * args.iters / r["ms_per_step"],
                          "method": f"(step with {args.iters} iterations - step with 10) / {args.iters - 10}, "
@@ -707,7 +808,9 @@ def main():
                          "ms_per_step_10_iterations": ms10,
                          "direct_launch_profile": {"avg_launch_us": jac_direct_ms * 1e3, "share_of_step": direct_share,
                                                    "note": "per-launch events force direct launches (no graph)"},
-                         "note": "C2 working set (~20 MB) is L2-resident after the first iterations"},
+                         "note": "C2 working set (~20 MB) is L2-resident after the first iterations: ncu DRAM "
+                                 "traffic is a few % of the algorithmic bytes; the HBM-bound evidence for the "
+                                 "same kernel is roofline_hbm (JAC-XL, 1.27 GB per launch)"},
             "e2e": {"value": r["e2e"], "unit": "solves/s", "h2d_bytes_per_step": r["e2e_bytes"][0],
                     "d2h_bytes_per_step": r["e2e_bytes"][1],
                     "method": "public API (sg.Grid: activate from a device input buffer filled by an H2D copy "
@@ -721,8 +824,12 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "scripts"))
             import xl_bench
             extra = {}
-            for name, fn in (("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3), ("c4", measure_c4), ("mg", measure_mg), ("mgpcg", measure_mgpcg),
-                             ("jac_xl", xl_bench.jac_xl), ("lg_xl", xl_bench.lg_xl), ("act_xl", xl_bench.act_xl)):
+            for name, fn in (("c2_modes", lambda: measure_c2_variants(args, local)),
+                             ("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3),
+                             ("c4", measure_c4), ("mg", measure_mg), ("mgpcg", measure_mgpcg),
+                             ("c5_1gpu", lambda: measure_c5_1gpu(args)),
+                             ("jac_xl", xl_bench.jac_xl), ("sf_xl", xl_bench.sf_xl), ("lg_xl", xl_bench.lg_xl),
+                             ("act_xl", xl_bench.act_xl)):
                 try:
                     extra[name] = fn()
                 except Exception as e:  # keep the main line even if an extra fails
@@ -731,7 +838,14 @@ def main():
             out["roofline_xl"] = {k: {"achieved": extra[k].get("achieved_GBps"), "frac": extra[k].get("frac"),
                                       "peak": extra[k].get("peak_GBps"), "unit": "GB/s",
                                       "bytes_per_launch": extra[k].get("bytes_per_launch")}
-                                  for k in ("jac_xl", "lg_xl")}
+                                  for k in ("jac_xl", "sf_xl", "lg_xl")}
+            jx = extra.get("jac_xl", {})
+            if "frac" in jx:
+                out["roofline_hbm"] = {"bound": "hbm", "kernel": "k_jacobi8 at JAC-XL (1024^3, 206K 8^3 blocks)",
+                                       "achieved": jx["achieved_GBps"], "peak": jx["peak_GBps"], "unit": "GB/s",
+                                       "frac": jx["frac"], "peak_source": jx["peak_source"],
+                                       "traffic": jac_xl_traffic(),
+                                       "algorithmic_bytes_per_launch": jx["bytes_per_launch"]}
         if not args.no_cpu_baseline and world == 1:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out))

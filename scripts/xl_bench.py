@@ -62,6 +62,49 @@ def jac_xl(iters=10, radius=288.0):
             "frac": ach / peak, "launches": n}
 
 
+def sf_xl(iters=10, radius=288.0):
+    """SF-XL: the generic fused megakernel (k_struct_for op table) at JAC-XL
+    size: JACOBI fused with the residual-style reduction s += x1 (PAPER.md:440
+    "fuse the Jacobi smoothing and reduction kernels"), one launch per
+    iteration.  Algorithmic bytes: 12 B per active cell (read x0, b; write x1;
+    the reduction reads x1 from the thread's registers)."""
+    L, lv = W.c2_layout(ptr=32)
+    f = L.fields
+    coords = W.block_ball_coords(128, 8, radius)
+    g = sg.Grid(L.desc())
+    dc = torch.as_tensor(coords).cuda()
+    calls, _ = W.c2_solve_calls(L, lv, coords, iters=0, reduce_result=False)
+    bench.enqueue_calls(g, calls, dc)
+    g.flush("all")
+    g.sync()
+    flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    src, dst = f["x0"], f["x1"]
+
+    def solve(k):
+        nonlocal src, dst
+        flush_buf.zero_()
+        for _ in range(k):
+            g.serial("CLEAR_SCALAR", [f["s"]])
+            g.struct_for("JACOBI", lv[-1], [dst, src, f["b"]])
+            g.struct_for("REDUCE_SUM", lv[-1], [f["s"], dst])
+            src, dst = dst, src
+        st = g.flush("all")
+        return sg.profile_read(g).get(100 + sg.OPS["JACOBI"], (0.0, 0)), st
+
+    solve(2)
+    sg.set_profiling(g, True)
+    (t1, _), _ = solve(1)
+    (tk, nk), st = solve(iters + 1)
+    ms, n = tk - t1, iters
+    nbytes = len(coords) * 512 * 12
+    peak, kind = bench.hbm_peak()
+    ach = nbytes / (ms / n / 1e3) / 1e9
+    return {"variant": "SF-XL", "kernel": "k_struct_for (JACOBI+REDUCE_SUM fused)", "blocks": len(coords),
+            "cells": len(coords) * 512, "bytes_per_launch": nbytes, "avg_launch_us": ms / n * 1e3,
+            "achieved_GBps": ach, "peak_GBps": peak, "peak_source": kind, "frac": ach / peak, "launches": n,
+            "tasks_fused": st["tasks_fused"]}
+
+
 def lg_xl(reps=15, p_ptr=0.25, p_bit=0.10, seed=0):
     L = W.Layout()
     lv = L.chain([("pointer", (64,) * 3), ("bitmasked", (32,) * 3)], [("m", "f32")])
@@ -172,3 +215,5 @@ if __name__ == "__main__":
         print(json.dumps(lg_xl()), flush=True)
     if "act" in which:
         print(json.dumps(act_xl()), flush=True)
+    if "sf" in which:
+        print(json.dumps(sf_xl()), flush=True)
