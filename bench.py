@@ -378,26 +378,37 @@ def measure_c5_1gpu(args):
             "particles": args.c5_particles}
 
 
-def measure_l2_peak(mb=16, reps=50):
-    """L2-resident copy bandwidth of this GPU (read + write bytes of a copy of
-    `mb` MB into another `mb` MB buffer, both far below the L2 size; best of
-    `reps`, CUDA events): the denominator of an L2-resident kernel's roofline."""
+def measure_l2_peak(mb=24, copies=40, reps=5):
+    """L2-resident copy bandwidth of this GPU: `copies` back-to-back copies of an
+    `mb` MB buffer into another (both together far below the 126 MB L2),
+    captured in one CUDA graph so launch gaps do not count; read + write bytes
+    over the graph's device time, best of `reps`.  The denominator of an
+    L2-resident kernel's roofline (MEASURED_PEAKS.json has no L2 figure)."""
     import torch
     n = mb * 1024 * 1024 // 4
     a = torch.ones(n, device="cuda")
     b = torch.empty_like(a)
-    for _ in range(5):
-        b.copy_(a)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            b.copy_(a)
+    torch.cuda.current_stream().wait_stream(s)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for _ in range(copies):
+            b.copy_(a)
+    gr.replay()
     torch.cuda.synchronize()
     best = 1e30
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        b.copy_(a)
+        gr.replay()
         e1.record()
         e1.synchronize()
         best = min(best, e0.elapsed_time(e1))
-    return 2 * n * 4 / (best / 1e3) / 1e9
+    return copies * 2 * n * 4 / (best / 1e3) / 1e9
 
 
 def measure_c2_variants(args, device, steps=10, warmup=3):
@@ -429,17 +440,16 @@ def measure_c2_variants(args, device, steps=10, warmup=3):
                 enq()
                 g.flush(passes)
             torch.cuda.synchronize()
-            ms = 0.0
-            for _ in range(steps):
+            # device time per step, the host running ahead (as in the headline loop)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for i in range(steps):
                 l2.zero_()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
+                ev[i][0].record(stream)
                 enq()
                 st = g.flush(passes)
-                b.record(stream)
-                b.synchronize()
-                ms += a.elapsed_time(b)
-            ms /= steps
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in ev) / steps
             key = f"{'optimized' if passes == 'all' else 'eager'}_{'graph' if graphs else 'direct'}"
             out[key] = {"solves_per_s": 1000.0 / ms, "ms_per_step": ms, "launches": st["launches"]}
         del g
@@ -508,40 +518,101 @@ def measure_c1(steps=200, warmup=10):
             "note": "host-synchronous per step (events around enqueue + flush, then a sync): includes host time"}
 
 
+# MPM algorithmic bytes per particle: P2G reads x, v, C, J
+# (64 B); G2P reads x, J (16 B) and writes x, v, C, J (64 B); PERMUTE moves
+# the 4-byte id (8 B).  FP32 work per particle (counted from the kernels'
+# arithmetic, FMA = 2): P2G ~ 27 nodes x (2 weight products + 4 x 8 for the
+# affine momentum and mass) + 60 setup ~ 0.95 kflop; G2P ~ 27 x (2 + 3 x 8) +
+# 40 ~ 0.74 kflop.
+MPM_BYTES = {"P2G": 64, "G2P": 80, "PERMUTE": 8}
+MPM_FLOPS = {"P2G": 950, "G2P": 740}
+
+
+def fp32_peak_tflops():
+    """FP32 FMA peak: SMs x 128 lanes x 2 flop x max SM clock (B200_PROFILING
+    unit counts; the clock from MEASURED_PEAKS.json)."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = 1965.0
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            mhz = float(json.load(open(p)).get("sm_max_mhz", mhz))
+        except Exception:
+            pass
+    return sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
 def measure_c3(steps=20, warmup=3, n=1_000_000):
-    """C3: 3D 128^3 sparse MLS-MPM, 1M particles: DEACTIVATE, P2G, GRID_OP, G2P per step."""
+    """C3: 3D 128^3 sparse MLS-MPM, 1M particles: DEACTIVATE, P2G, GRID_OP, G2P
+    per step.  Two particle layouts: in place (G2P overwrites the state in the
+    user's order), and bin order (G2P out of place into a second state set in
+    the binned kernels' order + PERMUTE of the ids; the sets alternate), with
+    a per-kernel roofline of P2G / G2P (HBM fraction, FP32 fraction)."""
     import torch
     from paper_2012_08141_b200 import sg
-    prog = W.c3_program(n_grid=128, n_particles=n, steps=1)
-    g = sg.Grid(prog["desc"])
-    for name, a in prog["arrays"].items():
-        t = torch.as_tensor(a).cuda().contiguous()
-        g.tensors = getattr(g, "tensors", {})
-        g.tensors[name] = t
-        g.register_array(t, a.shape[0])
-    step_calls = [c for c in prog["calls"] if c["call"] != "flush"]
+    out = {"particles": n}
+    peak, _ = hbm_peak()
+    fpk = fp32_peak_tflops()
+    for variant in ("in_place", "bin_order"):
+        bo = variant == "bin_order"
+        prog = W.c3_program(n_grid=128, n_particles=n, steps=2 if bo else 1, bin_order=bo)
+        g = sg.Grid(prog["desc"])
+        g.tensors = {}
+        for name, a in prog["arrays"].items():
+            t = torch.as_tensor(a).cuda().contiguous()
+            g.tensors[name] = t
+            g.register_array(t, a.shape[0])
+        per_step = []
+        cur = []
+        for c in prog["calls"]:
+            if c["call"] == "flush":
+                per_step.append(cur)
+                cur = []
+            else:
+                cur.append(c)
+        k = [0]
 
-    def enqueue():
-        for c in step_calls:
-            if c["call"] == "clear":
-                g.clear(c["target"], sg.DEACTIVATE)
-            elif c["call"] == "range_for":
-                g.range_for(c["op"], c["n"], c["fields"], c["arrays"], c["params"], c["activating"])
-            elif c["call"] == "struct_for":
-                g.struct_for(c["op"], c["snode"], c["fields"], c["params"], c["activating"])
+        def enqueue():
+            for c in per_step[k[0] % len(per_step)]:
+                if c["call"] == "clear":
+                    g.clear(c["target"], sg.DEACTIVATE)
+                elif c["call"] == "range_for":
+                    g.range_for(c["op"], c["n"], c["fields"], c["arrays"], c["params"], c["activating"])
+                elif c["call"] == "struct_for":
+                    g.struct_for(c["op"], c["snode"], c["fields"], c["params"], c["activating"])
+            k[0] += 1
 
-    ms, st = _timed_flushes(g, enqueue, steps, warmup)   # graph-replayed flushes
-    sg.set_profiling(g, True)                           # breakdown pass: direct launches with events
-    _timed_flushes(g, enqueue, 2, 0)
-    prof = sg.profile_read(g)
-    sg.set_profiling(g, False)
-    per = {}
-    names = {0: "activate", 1: "listgen", 3: "struct_for", 4: "range_for", 6: "deactivate"}
-    for k, (t, c) in prof.items():
-        if k in names:
-            per[names[k]] = t / max(c, 1) * 1e3
-    return {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
-            "binning_kernels_per_step": st["aux_kernels"], "avg_us_per_launch_kind": per, "particles": n}
+        ms, st = _timed_flushes(g, enqueue, steps, warmup)   # graph-replayed flushes
+        sg.set_profiling(g, True)                           # breakdown pass: direct launches with events
+        _timed_flushes(g, enqueue, 4, 0)
+        prof = sg.profile_read(g)
+        sg.set_profiling(g, False)
+        per = {}
+        names = {0: "activate", 1: "listgen", 3: "struct_for", 4: "range_for", 6: "deactivate"}
+        for key, (t, c) in prof.items():
+            if key in names:
+                per[names[key]] = t / max(c, 1) * 1e3
+        kern = {}
+        for op in ("P2G", "G2P", "PERMUTE"):
+            t, c = prof.get(300 + sg.OPS[op], (0.0, 0))
+            if not c:
+                continue
+            us = t / c * 1e3
+            e = {"avg_launch_us": us, "algorithmic_bytes": MPM_BYTES[op] * n,
+                 "achieved_GBps": MPM_BYTES[op] * n / (us / 1e6) / 1e9}
+            e["hbm_frac"] = e["achieved_GBps"] / peak
+            if op in MPM_FLOPS:
+                e["fp32_tflops"] = MPM_FLOPS[op] * n / (us / 1e6) / 1e12
+                e["fp32_frac"] = e["fp32_tflops"] / fpk
+            kern[op] = e
+        out[variant] = {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
+                        "binning_kernels_per_step": st["aux_kernels"], "avg_us_per_launch_kind": per,
+                        "kernels": kern}
+        del g
+    out["steps_per_s"] = max(out["in_place"]["steps_per_s"], out["bin_order"]["steps_per_s"])
+    out["fp32_peak_tflops"] = fpk
+    return out
 
 
 def _enqueue_calls(g, sg, calls):

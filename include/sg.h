@@ -151,6 +151,14 @@ enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
  *                           stable in-place compaction of the particles whose cell x stays
  *                           in [p2, p3); leavers appended to a5 (x < p2) / a6 (x >= p3)
  *   MIGRATE_APPEND range-for particles of buffers a5, a6 appended to a0..a4
+ *   G2P out of place with p2 != 0: the new state is written in the BIN ORDER of
+ *                           the input positions (the particle the binned kernel visits
+ *                           j-th goes to index j): a permutation of the particles (the
+ *                           paper fixes no particle order), which keeps the next step's
+ *                           binned kernels' particle reads sequential.  Pair it with:
+ *   PERMUTE      range-for  a2[c][j] = a1[c][perm(j)] for every component, perm = the
+ *                           bin order of positions a0 (the same binning as G2P), f0 any
+ *                           field of the grid tree, p1 inv_dx (moves ids along)
  * Differentiable MPM (C4; "kernels and their gradients", the
  * global fields / particle states serve as checkpoints):
  *   G2P with arrays a4..a7 set: reads state a0..a3, writes the new state to
@@ -191,7 +199,8 @@ enum {
   SG_OP_LOSS_MEAN = 27, SG_OP_ADJ_INIT = 28, SG_OP_G2P_ADJ = 29, SG_OP_P2G_ADJ = 30,
   SG_OP_SMOOTH_RB = 31, SG_OP_RESTRICT = 32, SG_OP_PROLONG = 33, SG_OP_RESID_NORM2 = 34,
   SG_OP_DOT = 35, SG_OP_AXPY_RATIO = 36, SG_OP_XPAY_RATIO = 37, SG_OP_COPY_SCALAR = 38,
-  SG_OP_DIST_SIGNAL = 40, SG_OP_DIST_WAIT = 41   /* exchange tasks (sg_dist_init) */
+  SG_OP_DIST_SIGNAL = 40, SG_OP_DIST_WAIT = 41,  /* exchange tasks (sg_dist_init) */
+  SG_OP_PERMUTE = 42
 };
 
 typedef struct {

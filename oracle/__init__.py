@@ -32,7 +32,7 @@ OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6
        "P2G": 20, "GRID_OP": 21, "G2P": 22,
        "LOSS_MEAN": 27, "ADJ_INIT": 28, "G2P_ADJ": 29, "P2G_ADJ": 30,
        "SMOOTH_RB": 31, "RESTRICT": 32, "PROLONG": 33, "RESID_NORM2": 34,
-       "DOT": 35, "AXPY_RATIO": 36, "XPAY_RATIO": 37, "COPY_SCALAR": 38}
+       "DOT": 35, "AXPY_RATIO": 36, "XPAY_RATIO": 37, "COPY_SCALAR": 38, "PERMUTE": 42}
 
 ERRORS = {-1: "ARG", -2: "LAYOUT", -3: "RANGE", -6: "DEMOTION_TRAP", -7: "OVERFLOW"}
 

@@ -61,7 +61,7 @@ enum {
   OP_P2G = 20, OP_GRID_OP = 21, OP_G2P = 22,
   OP_LOSS_MEAN = 27, OP_ADJ_INIT = 28, OP_G2P_ADJ = 29, OP_P2G_ADJ = 30,
   OP_SMOOTH_RB = 31, OP_RESTRICT = 32, OP_PROLONG = 33, OP_RESID_NORM2 = 34,
-  OP_DOT = 35, OP_AXPY_RATIO = 36, OP_XPAY_RATIO = 37, OP_COPY_SCALAR = 38
+  OP_DOT = 35, OP_AXPY_RATIO = 36, OP_XPAY_RATIO = 37, OP_COPY_SCALAR = 38, OP_PERMUTE = 42
 };
 
 typedef std::array<int64_t, 3> Coord;
@@ -816,6 +816,19 @@ int range_for(Grid* g, int op, int64_t n, const int32_t* f, int nf, const int32_
       const int comp = (int)P(0);
       for (int64_t i = 0; i < n && !rc; i++)
         rc = atomic_add(g, f[0], Coord{0, 0, 0}, P(1) * A_(g, ar[0], comp, i), false);
+    } break;
+    case OP_PERMUTE: {
+      // a2 = a1 in SOME order of the particles (the method fixes none; the
+      // device uses its bin order).  The oracle takes the identity; parity
+      // tests match particles by id.
+      if (na < 3) return fail(g, E_ARG, "PERMUTE needs 3 arrays");
+      Array &src = g->arrays[ar[1]], &dst = g->arrays[ar[2]];
+      const int nc = std::min(src.ncomp, dst.ncomp);
+      for (int c = 0; c < nc; c++)
+        for (int64_t i = 0; i < n; i++) {
+          dst.val[c * dst.n + i] = src.val[c * src.n + i];
+          dst.mag[c * dst.n + i] = src.mag[c * src.n + i];
+        }
     } break;
     case OP_ADJ_INIT: {
       // adjoint of the last state: a0[p0] = p1 (d loss / d x_T), everything else 0

@@ -1377,6 +1377,14 @@ int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DO
                      const DBins* bins) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  if (nops == 1 && ops[0].op == SG_OP_PERMUTE) {
+    PermArgs m;
+    m.C = c; m.op = ops[0]; m.n = n; m.dcount = dcount; m.binned = bins != nullptr;
+    if (bins) m.B = *bins;
+    int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    k_permute<<<std::max(grid, 1), 256, 0, s>>>(m);
+    return check_launch();
+  }
   if (nops == 1 && bins) {   // binned MPM kernels (LB = 2 trees; bins built by the caller)
     MpmBinArgs m;
     m.T = *grid_tree; m.TG = tree2 ? *tree2 : *grid_tree; m.C = c; m.op = ops[0]; m.B = *bins; m.task = task;

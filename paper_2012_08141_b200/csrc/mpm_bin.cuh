@@ -55,12 +55,24 @@ __device__ __forceinline__ uint32_t bin_key_of(const DBins& B, const float* x, i
   return ((uint32_t)b[0] * B.nb[1] + (uint32_t)b[1]) * B.nb[2] + (uint32_t)b[2];
 }
 
+// Warp-aggregated: lanes with the same key take one atomic (bin-sorted
+// particle arrays put whole warps on one key).
 __global__ void __launch_bounds__(BIN_TPB) k_bin_count(const __grid_constant__ BinArgs A) {
   const int64_t n = A.dcount ? (int64_t)*A.dcount : A.n;
-  for (int64_t i = blockIdx.x * (int64_t)BIN_TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * BIN_TPB) {
-    const uint32_t k = bin_key_of(A.B, A.x, A.xs, i, A.inv_dx);
-    A.B.key[i] = k;
-    A.B.rank[i] = atomicAdd(&A.B.hist[k], 1u);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)BIN_TPB; i0 < n; i0 += (int64_t)gridDim.x * BIN_TPB) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool live = i < n;
+    const uint32_t k = live ? bin_key_of(A.B, A.x, A.xs, i, A.inv_dx) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (live && lane == leader) base = atomicAdd(&A.B.hist[k], (uint32_t)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (live) {
+      A.B.key[i] = k;
+      A.B.rank[i] = base + __popc(peers & ((1u << lane) - 1u));
+    }
   }
 }
 
@@ -230,8 +242,8 @@ struct MpmBinArgs {
 __device__ __noinline__ void p2g_one(const DevCtx& C, const DTree& T, const DOp& op, int64_t i, int task) {
   mpm_p2g<2>(C, T, op, i, task);
 }
-__device__ __noinline__ void g2p_one(const DevCtx& C, const DTree& T, const DOp& op, int64_t i) {
-  mpm_g2p<2>(C, T, op, i);
+__device__ __noinline__ void g2p_one(const DevCtx& C, const DTree& T, const DOp& op, int64_t i, int64_t io) {
+  mpm_g2p<2>(C, T, op, i, io);
 }
 __device__ __noinline__ void g2p_adj_one(const DevCtx& C, const DTree& T, const DTree& TG, const DOp& op, int64_t i,
                                          int task) {
@@ -464,10 +476,18 @@ __global__ void __launch_bounds__(MB_TPB, 6) k_g2p_bin(const __grid_constant__ M
   float* jo = (float*)Jo.ptr;
   const float dt = op.p[0], inv_dx = op.p[1];
   const float dx = 1.0f / inv_dx, s4 = 4.0f * inv_dx * inv_dx;
+  // out of place with p2 != 0: the output state is written in BIN ORDER (the
+  // particle at bin position j goes to index j), so the next step's binned
+  // kernels read it nearly sequentially; SG_OP_PERMUTE moves the other
+  // particle arrays (ids) the same way
+  const bool bin_order = oo == 4 && op.p[2] != 0.0f;
   MB_FOR_CHUNKS {
     const int m = (int)min((uint32_t)MB_TPB, cnt - c0);
     if (key == A.B.nkeys - 1) {
-      if ((int)threadIdx.x < m) g2p_one(C, T, op, A.B.perm[start + c0 + threadIdx.x]);
+      if ((int)threadIdx.x < m) {
+        const uint32_t j = start + c0 + threadIdx.x;
+        g2p_one(C, T, op, A.B.perm[j], bin_order ? (int64_t)j : (int64_t)A.B.perm[j]);
+      }
       continue;
     }
     int o[3];
@@ -478,6 +498,7 @@ __global__ void __launch_bounds__(MB_TPB, 6) k_g2p_bin(const __grid_constant__ M
     __syncthreads();
     if ((int)threadIdx.x < m) {
       const int64_t i = A.B.perm[start + c0 + threadIdx.x];
+      const int64_t io = bin_order ? (int64_t)(start + c0 + threadIdx.x) : i;
       const float xp[3] = {x[i], x[X.n + i], x[2 * X.n + i]};
       const float J = jin[i];
       const MpmKernel k = mpm_bspline(xp, inv_dx);
@@ -502,14 +523,39 @@ __global__ void __launch_bounds__(MB_TPB, 6) k_g2p_bin(const __grid_constant__ M
           }
 #pragma unroll
       for (int rr = 0; rr < 3; rr++) {
-        vo[rr * Vo.n + i] = nv[rr];
-        xo[rr * Xo.n + i] = xp[rr] + dt * nv[rr];
+        vo[rr * Vo.n + io] = nv[rr];
+        xo[rr * Xo.n + io] = xp[rr] + dt * nv[rr];
 #pragma unroll
-        for (int d = 0; d < 3; d++) co[(3 * rr + d) * Co.n + i] = nC[rr][d];
+        for (int d = 0; d < 3; d++) co[(3 * rr + d) * Co.n + io] = nC[rr][d];
       }
-      jo[i] = J * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
+      jo[io] = J * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
     }
     __syncthreads();
+  }
+}
+
+// PERMUTE: dst[c][j] = src[c][perm[j]] for every component -- the bin order of
+// the positions a0 (the same binning G2P used), 16-byte stores where the
+// arrays allow.  Unbinned grids (SG_NO_BIN, other leaf shapes) copy in place
+// order, matching the unbinned G2P.
+struct PermArgs {
+  DevCtx C;
+  DOp op;
+  DBins B;
+  int64_t n;
+  const int32_t* dcount;
+  int binned;
+};
+
+__global__ void __launch_bounds__(256) k_permute(const __grid_constant__ PermArgs A) {
+  const DArray S = A.C.arrays[A.op.a[1]], D = A.C.arrays[A.op.a[2]];
+  const uint32_t* src = (const uint32_t*)S.ptr;
+  uint32_t* dst = (uint32_t*)D.ptr;
+  const int64_t n = A.dcount ? (int64_t)*A.dcount : A.n;
+  const int nc = S.ncomp < D.ncomp ? S.ncomp : D.ncomp;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = A.binned ? (int64_t)A.B.perm[j] : j;
+    for (int c = 0; c < nc; c++) dst[c * D.n + j] = src[c * S.n + i];
   }
 }
 

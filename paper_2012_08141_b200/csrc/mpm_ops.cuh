@@ -189,7 +189,9 @@ __device__ __forceinline__ void mpm_gather(const DevCtx& C, const DTree& T, cons
 // G2P: in place on a0..a3, or (a4 set) reading state a0..a3 and writing the
 // new state to a4..a7 (C4 keeps every substep's state as a checkpoint).
 template <int LB>
-__device__ __forceinline__ void mpm_g2p(const DevCtx& C, const DTree& T, const DOp& op, int64_t i) {
+__device__ __forceinline__ void mpm_g2p(const DevCtx& C, const DTree& T, const DOp& op, int64_t i,
+                                        int64_t io = -1) {
+  if (io < 0) io = i;   // output index (binned G2P in bin order writes particle i at its bin position)
   const int o = op.a[4] >= 0 ? 4 : 0;
   const DArray X = C.arrays[op.a[0]], Jj = C.arrays[op.a[3]];
   const DArray Xo = C.arrays[op.a[o]], Vo = C.arrays[op.a[o + 1]], Co = C.arrays[op.a[o + 2]],
@@ -208,12 +210,12 @@ __device__ __forceinline__ void mpm_g2p(const DevCtx& C, const DTree& T, const D
   mpm_gather<LB>(C, T, op, k, dx, inv_dx, nv, nC);
 #pragma unroll
   for (int r = 0; r < 3; r++) {
-    vo[r * Vo.n + i] = nv[r];
-    xo[r * Xo.n + i] = xp[r] + dt * nv[r];
+    vo[r * Vo.n + io] = nv[r];
+    xo[r * Xo.n + io] = xp[r] + dt * nv[r];
 #pragma unroll
-    for (int d = 0; d < 3; d++) co[(3 * r + d) * Co.n + i] = nC[r][d];
+    for (int d = 0; d < 3; d++) co[(3 * r + d) * Co.n + io] = nC[r][d];
   }
-  jo[i] = J * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
+  jo[io] = J * (1.0f + dt * (nC[0][0] + nC[1][1] + nC[2][2]));
 }
 
 // Grid update for one cell (struct-for).  cell0 points at the cell in field slot 0.

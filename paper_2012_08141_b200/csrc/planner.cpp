@@ -144,6 +144,7 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
       for (int i = 0; i < 5; i++) A(i, R_RW, AC_DATA);
       A(5, R_READ, AC_DATA); A(6, R_READ, AC_DATA);
       break;
+    case SG_OP_PERMUTE: A(0, R_READ, AC_DATA); A(1, R_READ, AC_DATA); A(2, R_WRITE, AC_DATA, true); break;
     case SG_OP_DIST_SIGNAL:   // send buffers complete -> the neighbours' receive buffers
       A(0, R_READ, AC_DATA); A(1, R_READ, AC_DATA); A(2, R_WRITE, AC_DATA); A(3, R_WRITE, AC_DATA);
       break;
@@ -170,6 +171,7 @@ static int op_min_fields(int op) {
     case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: case SG_OP_G2P_MIGRATE: return 4;
     case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: return 0;
     case SG_OP_DIST_SIGNAL: case SG_OP_DIST_WAIT: return 0;
+    case SG_OP_PERMUTE: return 1;
     case SG_OP_LOSS_MEAN: return 1;
     case SG_OP_SMOOTH_RB: case SG_OP_PROLONG: return 2;
     case SG_OP_RESTRICT: case SG_OP_RESID_NORM2: case SG_OP_DOT: return 3;
@@ -312,6 +314,14 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
     case SG_OP_ARRAY_COUNT:
       if (t.kind != SG_TASK_SERIAL || t.arrays[0] < 0) { err = "ARRAY_COUNT is a serial op on arrays[0]"; return SG_ERR_ARG; }
       return SG_OK;
+    case SG_OP_PERMUTE: {
+      if (t.kind != SG_TASK_RANGE_FOR) { err = "PERMUTE is a range-for op"; return SG_ERR_ARG; }
+      for (int i = 0; i < 3; i++) if (t.arrays[i] < 0) { err = "PERMUTE needs arrays a0 (positions), a1 (src), a2 (dst)"; return SG_ERR_ARG; }
+      if (t.arrays[1] == t.arrays[2]) { err = "PERMUTE is out of place"; return SG_ERR_ARG; }
+      int tree = L.field_tree[t.fields[0]];
+      if (tree < 0 || L.trees[tree].nd != 3 || L.trees[tree].driving < 0) { err = "PERMUTE field must live in a 3-D sparse tree"; return SG_ERR_ARG; }
+      return SG_OK;
+    }
     case SG_OP_DIST_SIGNAL:
     case SG_OP_DIST_WAIT:
       if (t.kind != SG_TASK_SERIAL) { err = "exchange tasks are serial ops"; return SG_ERR_ARG; }
@@ -741,7 +751,7 @@ static bool pass_fusion(const HLayout& L, std::vector<PTask>& seq, PlanStats& st
           auto solo = [](int op) {
             return op == SG_OP_G2P_MIGRATE || op == SG_OP_MIGRATE_APPEND || op == SG_OP_HALO_UNPACK ||
                    op == SG_OP_LOSS_MEAN || op == SG_OP_G2P_ADJ || op == SG_OP_P2G_ADJ || op == SG_OP_P2G ||
-                   op == SG_OP_G2P;
+                   op == SG_OP_G2P || op == SG_OP_PERMUTE;
           };
           if (solo(A.t.op) || solo(B.t.op)) continue;
         } else if (A.type == TT_SERIAL) {

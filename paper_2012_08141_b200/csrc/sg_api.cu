@@ -664,7 +664,8 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       const DTree* gt2 = nullptr;   // G2P_ADJ: the adjoint tree
       if (tk.op == SG_OP_G2P_ADJ) gt2 = &g->dtrees[g->L.field_tree[tk.fields[4]]];
       const DBins* bp = nullptr;
-      const bool mpm_op = tk.op == SG_OP_P2G || tk.op == SG_OP_G2P || tk.op == SG_OP_G2P_ADJ || tk.op == SG_OP_P2G_ADJ;
+      const bool mpm_op = tk.op == SG_OP_P2G || tk.op == SG_OP_G2P || tk.op == SG_OP_G2P_ADJ || tk.op == SG_OP_P2G_ADJ ||
+                          tk.op == SG_OP_PERMUTE;
       if (n > 0 && nops == 1 && mpm_op && gt && !g->no_bin && tree_lb2(*gt) && (!gt2 || tree_lb2(*gt2))) {
         if ((rc = ensure_bins(g, g->L.field_tree[tk.fields[0]], tk.arrays[0], ops[0].p[1], n, dcount, st.aux_kernels)))
           return rc;

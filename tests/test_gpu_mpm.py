@@ -148,3 +148,62 @@ def test_c3_full_size_properties_and_handoff():
     o = oracle.run_program(p1)
     g1, arrs1, _ = gpu_run(p1)
     compare_mpm(g1, arrs1, o, p1)
+
+
+def _by_id(arrs, names):
+    """Particle arrays of one state set, reordered by the id row."""
+    ids = arrs[names[4]].cpu().numpy()[0].astype(np.int64)
+    order = np.argsort(ids)
+    assert np.array_equal(ids[order], np.arange(ids.size)), "ids are not a permutation"
+    return {k: arrs[nm].cpu().numpy()[:, order] for k, nm in zip(("x", "v", "C", "J"), names[:4])}
+
+
+@pytest.mark.parametrize("steps", [1, 2])
+def test_c3_bin_order_handoff(steps):
+    """G2P out of place in bin order + PERMUTE of the ids (reading R38): one step
+    from the oracle's state after `steps - 1` steps, within 1e-5 of the oracle
+    matched by id; masks and grid fields as in the in-place variant."""
+    ng, n = 32, 4000
+    state = None
+    if steps > 1:
+        p0 = W.c3_program(n_grid=ng, n_particles=n, steps=steps - 1, seed=5, v_scale=1.0, J_jitter=0.02,
+                          lo=0.2, hi=0.7)
+        o0 = oracle.run_program(p0)
+        state = {k: o0.array(i).astype(np.float32) for i, k in enumerate(("x", "v", "C", "J"))}
+    prog = W.c3_program(n_grid=ng, n_particles=n, steps=1, seed=5, v_scale=1.0, J_jitter=0.02, lo=0.2, hi=0.7,
+                        bin_order=True)
+    if state:
+        prog["arrays"].update(state)
+    o = oracle.run_program(prog)
+    g, arrs, st = gpu_run(prog)
+    L = prog["layout"]
+    for name, fid in L.fields.items():
+        want, mag = o.field(fid, with_mag=True)
+        assert_field_close(g.field(fid), want, mag, "f32", f"grid {name}")
+    for s in range(1, len(L.rows)):
+        if L.rows[s][0] in (W.BITMASKED, W.POINTER):
+            assert as_set(g.mask(s)) == as_set(o.mask(s)), f"mask {s}"
+    names = list(prog["arrays"])
+    res = [names[i] for i in prog["result_set"]]
+    got = _by_id(arrs, res)
+    for i, k in enumerate(("x", "v", "C", "J")):
+        want, mag = o.array(prog["result_set"][i], with_mag=True)   # the oracle's permutation is the identity
+        assert_field_close(got[k], want, mag, "f32", f"particles {k}")
+    assert st[0]["launches"] == 6 + 1   # + PERMUTE
+
+
+def test_c3_bin_order_full_size_bit_exact_with_in_place():
+    """Full C3 (1M particles, 128^3): one step in bin order equals the in-place
+    step particle by particle (the same binned P2G on the same inputs, each
+    particle's G2P independent), bit for bit."""
+    n = 1_000_000
+    p_in = W.c3_program(n_grid=128, n_particles=n, steps=1, seed=0, v_scale=0.5, J_jitter=0.02)
+    p_bo = W.c3_program(n_grid=128, n_particles=n, steps=1, seed=0, v_scale=0.5, J_jitter=0.02, bin_order=True)
+    g1, a1, _ = gpu_run(p_in)
+    g2, a2, _ = gpu_run(p_bo)
+    names = list(p_bo["arrays"])
+    got = _by_id(a2, [names[i] for i in p_bo["result_set"]])
+    for k in ("x", "v", "C", "J"):
+        np.testing.assert_array_equal(got[k], a1[k].cpu().numpy(), err_msg=k)
+    m1 = g1.field(p_in["layout"].fields["m"])
+    np.testing.assert_array_equal(g2.field(p_bo["layout"].fields["m"]), m1)

@@ -233,3 +233,15 @@ def test_grid_op_gravity_and_walls():
     for c, u in want.items():
         got = [o.field(f[n])[c] for n in ("vx", "vy", "vz")]
         np.testing.assert_allclose(got, u, rtol=1e-14, atol=1e-15, err_msg=str(c))
+
+
+def test_bin_order_program_equals_in_place_on_the_oracle():
+    """The oracle's PERMUTE / bin-order G2P take the identity permutation: the
+    two-state-set program equals the in-place one value for value."""
+    a = W.c3_program(n_grid=32, n_particles=1500, steps=3, seed=2, v_scale=1.0, J_jitter=0.02, lo=0.2, hi=0.7)
+    b = W.c3_program(n_grid=32, n_particles=1500, steps=3, seed=2, v_scale=1.0, J_jitter=0.02, lo=0.2, hi=0.7,
+                     bin_order=True)
+    oa, ob = oracle.run_program(a), oracle.run_program(b)
+    for i in range(4):
+        np.testing.assert_array_equal(ob.array(b["result_set"][i]), oa.array(i))
+    np.testing.assert_array_equal(ob.array(b["result_set"][4])[0], np.arange(1500))

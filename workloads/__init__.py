@@ -250,27 +250,52 @@ def mpm_particles(n, lo=0.15, hi=0.55, seed=0, v_scale=0.0, J_jitter=0.0):
     return {"x": x, "v": v, "C": C, "J": J}
 
 
-def c3_step_calls(L, lv, n, prm):
+def c3_step_calls(L, lv, n, prm, src=(0, 1, 2, 3), dst=None, ids=None):
+    """One MPM substep.  dst=None: G2P in place on the state arrays `src`.
+    dst given: G2P out of place from `src` into `dst` in bin order (a
+    permutation of the particles, include/sg.h), and PERMUTE moves the id array
+    ids[0] -> ids[1] the same way."""
     f = L.fields
     grid_f = [f["vx"], f["vy"], f["vz"], f["m"]]
-    return [deactivate(lv[0]),
-            range_for("P2G", n, grid_f, [0, 1, 2, 3],
-                      [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]], [True] * 4),
-            struct_for("GRID_OP", lv[-1], grid_f, [prm["dt"], prm["gravity"], prm["bound"], prm["n_grid"]]),
-            range_for("G2P", n, grid_f, [0, 1, 2, 3], [prm["dt"], prm["inv_dx"]])]
+    src = list(src)
+    calls = [deactivate(lv[0]),
+             range_for("P2G", n, grid_f, src,
+                       [prm["dt"], prm["inv_dx"], prm["p_mass"], prm["p_vol"], prm["E"]], [True] * 4),
+             struct_for("GRID_OP", lv[-1], grid_f, [prm["dt"], prm["gravity"], prm["bound"], prm["n_grid"]])]
+    if dst is None:
+        calls.append(range_for("G2P", n, grid_f, src, [prm["dt"], prm["inv_dx"]]))
+    else:
+        calls.append(range_for("G2P", n, grid_f, src + list(dst), [prm["dt"], prm["inv_dx"], 1.0]))
+        calls.append(range_for("PERMUTE", n, [f["m"]], [src[0], ids[0], ids[1]], [0.0, prm["inv_dx"]]))
+    return calls
 
 
 def c3_program(n_grid=128, n_particles=1_000_000, steps=1, flush_every=1, seed=0, v_scale=0.0, J_jitter=0.0,
-               lo=0.15, hi=0.55, passes="all", **prm_kw):
+               lo=0.15, hi=0.55, passes="all", bin_order=False, **prm_kw):
+    """bin_order: two particle state sets A (arrays 0-3, ids 4) and B (5-8,
+    ids 9); step s runs G2P out of place A -> B (s even) or B -> A (s odd) in
+    bin order, ids permuted along (reading R38)."""
     L, lv = c3_layout(n_grid)
     prm = mpm_params(n_grid, **prm_kw)
     arrays = mpm_particles(n_particles, lo, hi, seed, v_scale, J_jitter)
+    if bin_order:
+        arrays["id"] = np.arange(n_particles, dtype=np.float32)[None]
+        for k in ("x", "v", "C", "J", "id"):
+            arrays[k + "B"] = np.zeros_like(arrays[k])
     calls = []
     for s in range(steps):
-        calls += c3_step_calls(L, lv, n_particles, prm)
+        if bin_order:
+            a, b = ((0, 1, 2, 3), (5, 6, 7, 8)) if s % 2 == 0 else ((5, 6, 7, 8), (0, 1, 2, 3))
+            ids = (4, 9) if s % 2 == 0 else (9, 4)
+            calls += c3_step_calls(L, lv, n_particles, prm, a, b, ids)
+        else:
+            calls += c3_step_calls(L, lv, n_particles, prm)
         if (s + 1) % flush_every == 0 or s == steps - 1:
             calls.append(flush(passes))
-    return program(L, calls, arrays=arrays, name="C3")
+    prog = program(L, calls, arrays=arrays, name="C3")
+    prog["bin_order"] = bin_order
+    prog["result_set"] = None if not bin_order else ((0, 1, 2, 3, 4) if steps % 2 == 0 else (5, 6, 7, 8, 9))
+    return prog
 
 
 # ----------------------------------------------------------------------------
