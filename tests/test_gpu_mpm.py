@@ -192,10 +192,12 @@ def test_c3_bin_order_handoff(steps):
     assert st[0]["launches"] == 6 + 1   # + PERMUTE
 
 
-def test_c3_bin_order_full_size_bit_exact_with_in_place():
+def test_c3_bin_order_full_size_matches_in_place():
     """Full C3 (1M particles, 128^3): one step in bin order equals the in-place
     step particle by particle (the same binned P2G on the same inputs, each
-    particle's G2P independent), bit for bit."""
+    particle's G2P independent) up to the order of P2G's cross-CTA global
+    atomic adds (run-to-run nondeterministic in both layouts): 1e-5 relative,
+    with a floor of 1e-6 of the array's largest magnitude."""
     n = 1_000_000
     p_in = W.c3_program(n_grid=128, n_particles=n, steps=1, seed=0, v_scale=0.5, J_jitter=0.02)
     p_bo = W.c3_program(n_grid=128, n_particles=n, steps=1, seed=0, v_scale=0.5, J_jitter=0.02, bin_order=True)
@@ -204,6 +206,7 @@ def test_c3_bin_order_full_size_bit_exact_with_in_place():
     names = list(p_bo["arrays"])
     got = _by_id(a2, [names[i] for i in p_bo["result_set"]])
     for k in ("x", "v", "C", "J"):
-        np.testing.assert_array_equal(got[k], a1[k].cpu().numpy(), err_msg=k)
+        ref = a1[k].cpu().numpy()
+        np.testing.assert_allclose(got[k], ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max(), err_msg=k)
     m1 = g1.field(p_in["layout"].fields["m"])
-    np.testing.assert_array_equal(g2.field(p_bo["layout"].fields["m"]), m1)
+    np.testing.assert_allclose(g2.field(p_bo["layout"].fields["m"]), m1, rtol=1e-5, atol=1e-6 * m1.max())
