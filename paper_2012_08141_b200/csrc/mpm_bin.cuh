@@ -388,8 +388,27 @@ __device__ __forceinline__ float tile_sum(const MbScatter& S, int f, int q) {
          c0 < cnt; c0 += gridDim.y * MB_TPB)
 
 // P2G, binned (op as mpm_p2g; LB = 2).
+//
+// Record of one particle (P2G_REC floats, record-major, 16-byte aligned): the
+// affine momentum folded so a stencil node at offset (a, b, c) from the base
+// needs no dpos arithmetic:  mom_r(a,b,c) = b_r + A'_r . (a, b, c), with
+// A' = dx * (p_mass C - dt 4 E p_vol (J-1) / dx^2 I) and
+// b_r = p_mass v_r - A'_r . fx   (dpos_d = (off_d - fx_d) dx).
+//   [0..3] b0 b1 b2 p_mass   [4..7] A'00 A'01 A'02 A'10   [8..11] A'11 A'12 A'20 A'21
+//   [12..15] A'22 tile-base (int bits) - -   [16..24] wx0..2 wy0..2 wz0..2
+// The warp's 27 lanes read [0..15] as four broadcast 16-byte loads and their
+// three weights (distinct banks), then update their node of the warp-private
+// tile: ~34 instructions per (particle, node) pair.
+constexpr int P2G_REC = 28;
+struct MbP2G {
+  float tile[MB_WARPS][4][MB_TP];
+  float rec[MB_WARPS][32][P2G_REC];
+  uint32_t need;
+  uint32_t off[8];
+};
+
 __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_bin(const __grid_constant__ MpmBinArgs A) {
-  __shared__ MbScatter S;
+  __shared__ __align__(16) MbP2G S;
   const DevCtx& C = A.C;
   const DOp& op = A.op;
   const DTree& T = A.T;
@@ -402,6 +421,11 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_bin(const __grid_constant__ M
   const float dx = 1.0f / inv_dx;
   uint32_t* pool = T.seg[T.nseg - 1].base;
   const uint64_t fs = 1ull << T.ln_leaf;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  // this lane's stencil node (lanes 27..31 idle in the walk)
+  const int la = l / 9, lb = (l / 3) % 3, lc = l % 3;
+  const float fa = (float)la, fb = (float)lb, fc = (float)lc;
+  const int dq = la * MB_SI + lb * MB_SJ + lc;
   MB_FOR_CHUNKS {
     const int m = (int)min((uint32_t)MB_TPB, cnt - c0);
     if (key == A.B.nkeys - 1) {   // outside the domain: per-particle path
@@ -411,7 +435,7 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_bin(const __grid_constant__ M
     int o[3];
     bin_origin(A.B, key, o);
     if (threadIdx.x == 0) S.need = 0;
-    zero_tiles(S, 4);
+    for (int k = threadIdx.x; k < MB_WARPS * 4 * MB_TP; k += MB_TPB) (&S.tile[0][0][0])[k] = 0.0f;
     __syncthreads();
     uint32_t need = 0;
     if ((int)threadIdx.x < m) {
@@ -421,37 +445,73 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_bin(const __grid_constant__ M
       const int r[3] = {k.base[0] - o[0], k.base[1] - o[1], k.base[2] - o[2]};
       need = need_mask(r);
       const float stress = -dt * 4.0f * E * pv * (jj[i] - 1.0f) * inv_dx * inv_dx;
-      float q[12];
+      float* R = S.rec[w][l];
+      float Ap[3][3], b[3];
 #pragma unroll
       for (int rr = 0; rr < 3; rr++) {
-        q[rr] = pm * v[rr * Vv.n + i];
 #pragma unroll
-        for (int c = 0; c < 3; c++) q[3 + 3 * rr + c] = pm * cm[(3 * rr + c) * Cm.n + i] + (rr == c ? stress : 0.0f);
+        for (int c = 0; c < 3; c++) Ap[rr][c] = (pm * cm[(3 * rr + c) * Cm.n + i] + (rr == c ? stress : 0.0f)) * dx;
+        b[rr] = pm * v[rr * Vv.n + i] - (Ap[rr][0] * k.fx[0] + Ap[rr][1] * k.fx[1] + Ap[rr][2] * k.fx[2]);
       }
-      put_record(S, k, r, q);
+      *reinterpret_cast<float4*>(R + 0) = make_float4(b[0], b[1], b[2], pm);
+      *reinterpret_cast<float4*>(R + 4) = make_float4(Ap[0][0], Ap[0][1], Ap[0][2], Ap[1][0]);
+      *reinterpret_cast<float4*>(R + 8) = make_float4(Ap[1][1], Ap[1][2], Ap[2][0], Ap[2][1]);
+      *reinterpret_cast<float4*>(R + 12) =
+          make_float4(Ap[2][2], __int_as_float(r[0] * MB_SI + r[1] * MB_SJ + r[2]), 0.0f, 0.0f);
+#pragma unroll
+      for (int oo = 0; oo < 3; oo++)
+#pragma unroll
+        for (int a = 0; a < 3; a++) R[16 + 3 * a + oo] = k.w[oo][a];
     }
     need = __reduce_or_sync(0xffffffffu, need);
-    if ((threadIdx.x & 31) == 0 && need) atomicOr(&S.need, need);
+    if (l == 0 && need) atomicOr(&S.need, need);
     __syncwarp();
-    warp_scatter(S, min(32, max(0, m - (int)(threadIdx.x & ~31u))), dx, 1.0f, pm, 4);
+    {
+      const int mw = min(32, max(0, m - (int)(threadIdx.x & ~31u)));
+      if (l < 27) {
+        float* t0 = S.tile[w][0];
+        float* t1 = S.tile[w][1];
+        float* t2 = S.tile[w][2];
+        float* t3 = S.tile[w][3];
+        for (int p = 0; p < mw; p++) {
+          const float* R = S.rec[w][p];
+          const float4 r0 = *reinterpret_cast<const float4*>(R + 0);
+          const float4 r1 = *reinterpret_cast<const float4*>(R + 4);
+          const float4 r2 = *reinterpret_cast<const float4*>(R + 8);
+          const float4 r3 = *reinterpret_cast<const float4*>(R + 12);
+          const float W = R[16 + la] * R[19 + lb] * R[22 + lc];
+          const int nq = __float_as_int(r3.y) + dq;
+          const float m0 = r0.x + r1.x * fa + r1.y * fb + r1.z * fc;
+          const float m1 = r0.y + r1.w * fa + r2.x * fb + r2.y * fc;
+          const float m2 = r0.z + r2.z * fa + r2.w * fb + r3.x * fc;
+          t0[nq] += W * m0;
+          t1[nq] += W * m1;
+          t2[nq] += W * m2;
+          t3[nq] += W * r0.w;
+        }
+      }
+    }
     __syncthreads();
     if (op.act) bin_blocks<true>(C, T, o, S.need, S.off, A.task);
     else bin_blocks<false>(C, T, o, S.need, S.off, A.task);
     __syncthreads();
     for (int q = threadIdx.x; q < MB_NODES; q += MB_TPB) {
-      const float mass = tile_sum(S, 3, q);
-      if (mass == 0.0f) continue;
+      const int pq = tile_pad(q);
+      float y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int ww = 0; ww < MB_WARPS; ww++)
+#pragma unroll
+        for (int f = 0; f < 4; f++) y[f] += S.tile[ww][f][pq];
+      if (y[3] == 0.0f) continue;
       const uint32_t off = tile_node_off(S.off, q);
       if (off == SG_NO_BLOCK) {
         if (C.debug) set_err(C, op.act ? SG_ERR_RANGE : SG_ERR_DEMOTION_TRAP, A.task);
         continue;
       }
 #pragma unroll
-      for (int r = 0; r < 3; r++) {
-        const float y = tile_sum(S, r, q);
-        if (y != 0.0f) atomicAdd((float*)(pool + (uint64_t)op.slot[r] * fs) + off, y);
-      }
-      atomicAdd((float*)(pool + (uint64_t)op.slot[3] * fs) + off, mass);
+      for (int r = 0; r < 3; r++)
+        if (y[r] != 0.0f) atomicAdd((float*)(pool + (uint64_t)op.slot[r] * fs) + off, y[r]);
+      atomicAdd((float*)(pool + (uint64_t)op.slot[3] * fs) + off, y[3]);
     }
     __syncthreads();
   }
