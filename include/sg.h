@@ -150,6 +150,10 @@ enum { SG_TASK_STRUCT_FOR = 0, SG_TASK_RANGE_FOR = 1, SG_TASK_SERIAL = 2 };
  *   G2P_MIGRATE  range-for  G2P over a0..a3 (x,v,C,J) + a4 (id) with device count, then
  *                           stable in-place compaction of the particles whose cell x stays
  *                           in [p2, p3); leavers appended to a5 (x < p2) / a6 (x >= p3)
+ *   MIGRATE_COMPACT range-for on a0..a3 (x,v,C,J) + a4 (id) with device count: the
+ *                           particles whose cell x (p1 inv_dx) left [p2, p3) are packed
+ *                           into a5 (x < p2) / a6 (x >= p3) and their slots refilled from
+ *                           the tail (hole filling: the order changes, O(leavers) moves)
  *   MIGRATE_APPEND range-for particles of buffers a5, a6 appended to a0..a4
  *   G2P out of place with p2 != 0: the new state is written in the BIN ORDER of
  *                           the input positions (the particle the binned kernel visits
@@ -200,7 +204,7 @@ enum {
   SG_OP_SMOOTH_RB = 31, SG_OP_RESTRICT = 32, SG_OP_PROLONG = 33, SG_OP_RESID_NORM2 = 34,
   SG_OP_DOT = 35, SG_OP_AXPY_RATIO = 36, SG_OP_XPAY_RATIO = 37, SG_OP_COPY_SCALAR = 38,
   SG_OP_DIST_SIGNAL = 40, SG_OP_DIST_WAIT = 41,  /* exchange tasks (sg_dist_init) */
-  SG_OP_PERMUTE = 42
+  SG_OP_PERMUTE = 42, SG_OP_MIGRATE_COMPACT = 43
 };
 
 typedef struct {

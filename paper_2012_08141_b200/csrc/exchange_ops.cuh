@@ -237,3 +237,135 @@ __global__ void __launch_bounds__(256) k_migrate_append(const __grid_constant__ 
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// MIGRATE_COMPACT: migration for particle arrays kept in the binned kernels'
+// order (G2P out of place in bin order, then this op on the new state).  The
+// method fixes no particle order, so leavers are removed by HOLE FILLING
+// instead of a stable compaction: only O(leavers) particles move.
+//   k_migrate_mark: every particle whose cell x left [lo, hi) is appended to
+//     the left / right send buffer (17-word record) and its index to the hole
+//     list.
+//   k_migrate_fill (one CTA): n' = n - holes; the keepers among the tail
+//     positions [n', n) move into the holes below n' (k-th tail keeper into the
+//     k-th low hole); the count becomes n'.
+// ---------------------------------------------------------------------------
+struct CompactArgs {
+  DevCtx C;
+  DOp op;
+  uint32_t* holes;    // [0] count, [1..] indices
+  uint32_t* tail;     // hole marks of the tail positions
+  uint64_t cap;
+  int task;
+};
+
+__global__ void __launch_bounds__(256) k_migrate_mark(const __grid_constant__ CompactArgs A) {
+  const DevCtx& C = A.C;
+  const DOp& op = A.op;
+  const DArray X = C.arrays[op.a[0]], Vv = C.arrays[op.a[1]], Cm = C.arrays[op.a[2]], Jj = C.arrays[op.a[3]],
+               Id = C.arrays[op.a[4]], Lb = C.arrays[op.a[5]], Rb = C.arrays[op.a[6]];
+  const float* x = (const float*)X.ptr;
+  const uint32_t n = (uint32_t)*X.dcount;
+  const float inv_dx = op.p[1], lo = op.p[2], hi = op.p[3];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float xp0 = x[i];
+    const float cx = floorf(__fmul_rn(xp0, inv_dx));
+    if (cx >= lo && cx < hi) continue;
+    const DArray& Bf = cx < lo ? Lb : Rb;
+    const uint32_t s = atomicAdd((uint32_t*)Bf.dcount, 1u);
+    if ((uint64_t)(s + 1) * PREC_WORDS > (uint64_t)Bf.n) { set_err(C, SG_ERR_LIST_OVERFLOW, A.task); continue; }
+    uint32_t* rec = (uint32_t*)Bf.ptr + (uint64_t)s * PREC_WORDS;
+    const uint32_t* xv = (const uint32_t*)X.ptr;
+    const uint32_t* vv = (const uint32_t*)Vv.ptr;
+    const uint32_t* cv = (const uint32_t*)Cm.ptr;
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      rec[r] = xv[r * X.n + i];
+      rec[3 + r] = vv[r * Vv.n + i];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; k++) rec[6 + k] = cv[k * Cm.n + i];
+    rec[15] = ((const uint32_t*)Jj.ptr)[i];
+    rec[16] = ((const uint32_t*)Id.ptr)[i];
+    const uint32_t h = atomicAdd(A.holes, 1u);
+    if (h < A.cap) A.holes[1 + h] = i;
+    else set_err(C, SG_ERR_LIST_OVERFLOW, A.task);
+  }
+}
+
+// Block-wide exclusive scan of one flag per thread (1024 threads).
+__device__ __forceinline__ uint32_t block_scan1024(uint32_t f, uint32_t* s_w, uint32_t& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) s_w[w] = __popc(bal);
+  __syncthreads();
+  if (w == 0) {
+    uint32_t v = s_w[lane], inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    s_w[lane] = inc - v;
+    if (lane == 31) s_w[32] = inc;
+  }
+  __syncthreads();
+  const uint32_t r = s_w[w] + __popc(bal & ((1u << lane) - 1u));
+  total = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) k_migrate_fill(const __grid_constant__ CompactArgs A) {
+  __shared__ uint32_t s_w[33];
+  const DevCtx& C = A.C;
+  const DOp& op = A.op;
+  const DArray X = C.arrays[op.a[0]];
+  const uint32_t n = (uint32_t)*X.dcount;
+  const uint32_t L = (uint32_t)min((uint64_t)A.holes[0], A.cap);
+  const uint32_t np = n - L;
+  // mark the tail positions that are holes
+  for (uint32_t t = threadIdx.x; t < L; t += 1024) A.tail[t] = 0u;
+  __syncthreads();
+  for (uint32_t h = threadIdx.x; h < L; h += 1024) {
+    const uint32_t p = A.holes[1 + h];
+    if (p >= np) A.tail[p - np] = 1u;
+  }
+  __syncthreads();
+  // k-th low hole (in hole-list order) <- k-th tail keeper (in position order):
+  // rank the low holes in place (tail[] is reused below, so first collect the
+  // low holes into holes[1..] compacted)
+  uint32_t base = 0;
+  for (uint32_t h0 = 0; h0 < L; h0 += 1024) {
+    const uint32_t h = h0 + threadIdx.x;
+    const uint32_t p = h < L ? A.holes[1 + h] : 0xFFFFFFFFu;
+    const uint32_t f = h < L && p < np;
+    uint32_t tot;
+    const uint32_t r = block_scan1024(f, s_w, tot);
+    if (f) A.holes[1 + base + r] = p;   // writes only at or below the read position: safe in place
+    base += tot;
+    __syncthreads();
+  }
+  // the tail keepers, in order, move into the low holes
+  uint32_t kbase = 0;
+  for (uint32_t t0 = 0; t0 < L; t0 += 1024) {
+    const uint32_t t = t0 + threadIdx.x;
+    const uint32_t f = t < L && A.tail[t] == 0u;
+    uint32_t tot;
+    const uint32_t r = block_scan1024(f, s_w, tot);
+    if (f) {
+      const uint32_t src = np + t, dst = A.holes[1 + kbase + r];
+      for (int a = 0; a < 5; a++) {
+        const DArray& Ar = C.arrays[op.a[a]];
+        uint32_t* q = (uint32_t*)Ar.ptr;
+        for (int c = 0; c < Ar.ncomp; c++) q[(uint64_t)c * Ar.n + dst] = q[(uint64_t)c * Ar.n + src];
+      }
+    }
+    kbase += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *X.dcount = (int)np;
+    A.holes[0] = 0u;   // ready for the next step
+  }
+}

@@ -78,6 +78,9 @@ struct sg_grid {
   uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
   uint64_t mig_tiles = 0;
   uint32_t* mig_ctl = nullptr;
+  uint32_t* mig_holes = nullptr;    // MIGRATE_COMPACT hole list ([0] count) + tail marks
+  uint32_t* mig_tail = nullptr;
+  uint64_t mig_hole_cap = 0;
   // particle bins (binned MPM kernels) + a one-entry cache keyed by the
   // position array, its write epoch, the tree and the range
   DBins bins{};

@@ -1443,6 +1443,14 @@ int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DO
     k_g2p_migrate<<<std::max(grid, 1), MG_TPB, 0, s>>>(m);
     return check_launch();
   }
+  if (nops == 1 && ops[0].op == SG_OP_MIGRATE_COMPACT) {
+    CompactArgs m;
+    m.C = c; m.op = ops[0]; m.holes = rs->holes; m.tail = rs->tail; m.cap = rs->hole_cap; m.task = task;
+    int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    k_migrate_mark<<<std::max(grid, 1), 256, 0, s>>>(m);
+    k_migrate_fill<<<1, 1024, 0, s>>>(m);
+    return check_launch();
+  }
   if (nops == 1 && ops[0].op == SG_OP_MIGRATE_APPEND) {
     AppArgs m;
     m.C = c; m.op = ops[0]; m.ctl = rs->ctl + 4;

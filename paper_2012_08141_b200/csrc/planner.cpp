@@ -144,6 +144,9 @@ static std::vector<OpUse> op_uses(const sg_task& t) {
       for (int i = 0; i < 5; i++) A(i, R_RW, AC_DATA);
       A(5, R_READ, AC_DATA); A(6, R_READ, AC_DATA);
       break;
+    case SG_OP_MIGRATE_COMPACT:
+      for (int i = 0; i < 7; i++) A(i, R_RW, AC_DATA);
+      break;
     case SG_OP_PERMUTE: A(0, R_READ, AC_DATA); A(1, R_READ, AC_DATA); A(2, R_WRITE, AC_DATA, true); break;
     case SG_OP_DIST_SIGNAL:   // send buffers complete -> the neighbours' receive buffers
       A(0, R_READ, AC_DATA); A(1, R_READ, AC_DATA); A(2, R_WRITE, AC_DATA); A(3, R_WRITE, AC_DATA);
@@ -169,7 +172,7 @@ static int op_min_fields(int op) {
     case SG_OP_ADD_CONST: case SG_OP_STENCIL: case SG_OP_REDUCE_SUM: return 2;
     case SG_OP_AXPY: case SG_OP_JACOBI: return 3;
     case SG_OP_P2G: case SG_OP_GRID_OP: case SG_OP_G2P: case SG_OP_G2P_MIGRATE: return 4;
-    case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: return 0;
+    case SG_OP_ARRAY_COUNT: case SG_OP_MIGRATE_APPEND: case SG_OP_ADJ_INIT: case SG_OP_MIGRATE_COMPACT: return 0;
     case SG_OP_DIST_SIGNAL: case SG_OP_DIST_WAIT: return 0;
     case SG_OP_PERMUTE: return 1;
     case SG_OP_LOSS_MEAN: return 1;
@@ -328,6 +331,7 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
       if (!(t.params[0] == 0.0f || t.params[0] == 1.0f || t.params[0] == 2.0f)) { err = "exchange kind (p0) must be 0, 1 or 2"; return SG_ERR_ARG; }
       return SG_OK;
     case SG_OP_MIGRATE_APPEND:
+    case SG_OP_MIGRATE_COMPACT:
     case SG_OP_HALO_UNPACK:
     case SG_OP_G2P_MIGRATE:
       if (t.kind != SG_TASK_RANGE_FOR) { err = "migration / unpack ops are range-for ops"; return SG_ERR_ARG; }
@@ -340,7 +344,7 @@ static int validate_task(const HLayout& L, const sg_task& t, std::string& err) {
           if (!valid_field(L, t.fields[i]) || L.field_tree[t.fields[i]] != tree) { err = "HALO_UNPACK fields must share a tree"; return SG_ERR_ARG; }
         return SG_OK;
       }
-      if (t.op == SG_OP_MIGRATE_APPEND) return SG_OK;
+      if (t.op == SG_OP_MIGRATE_APPEND || t.op == SG_OP_MIGRATE_COMPACT) return SG_OK;
       break;   // G2P_MIGRATE: grid checks below
     case SG_OP_LOSS_MEAN:
       if (t.kind != SG_TASK_RANGE_FOR || t.arrays[0] < 0) { err = "LOSS_MEAN is a range-for op over arrays[0]"; return SG_ERR_ARG; }
@@ -750,6 +754,7 @@ static bool pass_fusion(const HLayout& L, std::vector<PTask>& seq, PlanStats& st
           // ops with their own kernels (scan / append / unpack, the binned MPM transfers) run alone
           auto solo = [](int op) {
             return op == SG_OP_G2P_MIGRATE || op == SG_OP_MIGRATE_APPEND || op == SG_OP_HALO_UNPACK ||
+                   op == SG_OP_MIGRATE_COMPACT ||
                    op == SG_OP_LOSS_MEAN || op == SG_OP_G2P_ADJ || op == SG_OP_P2G_ADJ || op == SG_OP_P2G ||
                    op == SG_OP_G2P || op == SG_OP_PERMUTE;
           };

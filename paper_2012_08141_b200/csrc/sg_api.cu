@@ -641,6 +641,18 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
         n = a0->n;
         dcount = a0->dcount;
       }
+      if (tk.op == SG_OP_MIGRATE_COMPACT) {
+        for (int s = 0; s < 7; s++)
+          if (!arr(s) || ((s == 0 || s >= 5) && !arr(s)->dcount)) return fail(SG_ERR_ARG, "migration arrays need device counts");
+        const uint64_t cap = (uint64_t)(arr(5)->n + arr(6)->n) / 17 + 1;
+        if (cap > g->mig_hole_cap) {
+          g->mig_holes = (uint32_t*)g->dev_alloc((cap + 1) * 4);
+          g->mig_tail = (uint32_t*)g->dev_alloc(cap * 4);
+          if (!g->mig_holes || !g->mig_tail) return fail(SG_ERR_CUDA, "migration scratch allocation failed");
+          CUDA_TRY(cudaMemsetAsync(g->mig_holes, 0, 4, g->stream));
+          g->mig_hole_cap = cap;
+        }
+      }
       if (tk.op == SG_OP_G2P_MIGRATE || tk.op == SG_OP_MIGRATE_APPEND) {
         for (int s = 0; s < 7; s++)
           if (!arr(s) || ((s == 0 || s >= 5) && !arr(s)->dcount)) return fail(SG_ERR_ARG, "migration arrays need device counts");
@@ -657,7 +669,7 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
           CUDA_TRY(cudaMemsetAsync(g->mig_ctl, 0, 64, g->stream));
         }
       }
-      RangeScratch rs{g->mig_status, g->mig_ctl};
+      RangeScratch rs{g->mig_status, g->mig_ctl, g->mig_holes, g->mig_tail, g->mig_hole_cap};
       const DTree* gt = nullptr;
       if (tk.fields[0] >= 0 && tk.fields[0] < (int)g->L.field_tree.size() && g->L.field_tree[tk.fields[0]] >= 0)
         gt = &g->dtrees[g->L.field_tree[tk.fields[0]]];

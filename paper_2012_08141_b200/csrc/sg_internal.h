@@ -168,6 +168,9 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int tree_id, const DList*
 struct RangeScratch {
   uint64_t* status;   // look-back descriptors for G2P_MIGRATE tiles
   uint32_t* ctl;      // [0..3] migrate tile/done/epoch/count, [5] append ticket
+  uint32_t* holes;    // MIGRATE_COMPACT: [0] hole count, then hole indices
+  uint32_t* tail;     // MIGRATE_COMPACT: per-tail-position hole marks
+  uint64_t hole_cap;  // capacity of holes / tail (entries)
 };
 int launch_range_for(const DevCtx& c, int64_t n, const int32_t* dcount, const DOp* ops, int nops, int task_id,
                      void* stream, const RangeScratch* rs, const DTree* grid_tree, const DTree* tree2,

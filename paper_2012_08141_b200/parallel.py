@@ -11,9 +11,10 @@ the particles whose cell x lies in it.  Every step, in libsg tasks only:
      neighbours packed; GRID_OP; HALO_PACK of the two boundary layers;
      DIST_SIGNAL(halo fill).
   3. DIST_WAIT(halo fill); HALO_UNPACK store into the ghost layers;
-     G2P_MIGRATE: G2P fused with the stable in-place compaction of the
-     particles that stay, leavers appended to the migration send buffers;
-     DIST_SIGNAL(migration).
+     G2P into the rank's second particle state set in the binned kernels'
+     order (bin-order storage: the next step's particle reads are sequential),
+     PERMUTE of the ids, MIGRATE_COMPACT: leavers packed into the migration
+     send buffers and their slots refilled from the tail; DIST_SIGNAL(migration).
   4. DIST_WAIT(migration); MIGRATE_APPEND of the received particles.
 
 The library moves the bytes (sg_dist_init, include/sg.h): on the peer
@@ -94,7 +95,8 @@ class RankState:
         self.plan_only = plan_only
         g = self.grid
         if plan_only:
-            self.a = [g.register_array_plan(capacity, nc) for nc in (3, 3, 9, 1, 1)]
+            self.aset = [[g.register_array_plan(capacity, nc) for nc in (3, 3, 9, 1, 1)] for _ in range(2)]
+            self.cur = 0
             return
         import torch
         n = particles["x"].shape[1]
@@ -105,15 +107,37 @@ class RankState:
         def arr(ncomp, dtype=torch.float32):
             return torch.zeros((ncomp, capacity), dtype=dtype, device=dev)
 
-        self.x, self.v, self.C, self.J = arr(3), arr(3), arr(9), arr(1)
-        self.id = arr(1, torch.int32)
+        # two particle state sets: G2P writes the new state of set `cur` into the
+        # other one in the binned kernels' order (bin-order storage, reading
+        # R38); both share one device count
         self.count = torch.zeros(4, dtype=torch.int32, device=dev)
-        for name in ("x", "v", "C", "J", "id"):
-            getattr(self, name)[:, :n] = torch.as_tensor(np.ascontiguousarray(particles[name]), device=dev)
+        self.sets, self.aset = [], []
+        for k in range(2):
+            st = {"x": arr(3), "v": arr(3), "C": arr(9), "J": arr(1), "id": arr(1, torch.int32)}
+            if k == 0:
+                for name in ("x", "v", "C", "J", "id"):
+                    st[name][:, :n] = torch.as_tensor(np.ascontiguousarray(particles[name]), device=dev)
+            ids = [g.register_array(t, t.shape[0]) for t in (st["x"], st["v"], st["C"], st["J"], st["id"])]
+            for a in ids:
+                sg.set_array_count(g, a, self.count)
+            self.sets.append(st)
+            self.aset.append(ids)
         self.count[0] = n
-        self.a = [g.register_array(t, t.shape[0]) for t in (self.x, self.v, self.C, self.J, self.id)]
-        for a in self.a:
-            sg.set_array_count(g, a, self.count)
+        self.cur = 0
+
+    # the current particle state (set `cur`)
+    @property
+    def a(self):
+        return self.aset[self.cur]
+
+    @property
+    def a_next(self):
+        return self.aset[1 - self.cur]
+
+    def __getattr__(self, name):
+        if name in ("x", "v", "C", "J", "id"):
+            return self.__dict__["sets"][self.__dict__["cur"]][name]
+        raise AttributeError(name)
 
     def connect(self, world, nccl_uid=None):
         sg.dist_init(self.grid, self.rank, world, nccl_uid)
@@ -255,15 +279,20 @@ class SlabMPM:
             for side in (0, 1):
                 g.task(sg.TASK_SERIAL, "ARRAY_COUNT", arrays=[st.send[(PART, side)]], params=[0.0])
             lo_f, hi_f = self.part.migration_bounds(st.rank)
-            g.task(sg.TASK_RANGE_FOR, "G2P_MIGRATE", -1, self.gf,
-                   st.a + [st.send[(PART, 0)], st.send[(PART, 1)]], [prm["dt"], prm["inv_dx"], lo_f, hi_f], n=-1)
+            a, b = st.a, st.a_next
+            # G2P into the other state set in bin order, ids along, then the
+            # particles that left the slab are packed and their slots refilled
+            g.task(sg.TASK_RANGE_FOR, "G2P", -1, self.gf, a[:4] + b[:4], [prm["dt"], prm["inv_dx"], 1.0], n=-1)
+            g.task(sg.TASK_RANGE_FOR, "PERMUTE", -1, [self.gf[3]], [a[0], a[4], b[4]], [0.0, prm["inv_dx"]], n=-1)
+            g.task(sg.TASK_RANGE_FOR, "MIGRATE_COMPACT", -1, [],
+                   b + [st.send[(PART, 0)], st.send[(PART, 1)]], [0.0, prm["inv_dx"], lo_f, hi_f], n=-1)
             self._signal(st, PART)
 
         def p4():
             if self.world > 1:
                 self._wait(st, PART)
                 st.grid.task(sg.TASK_RANGE_FOR, "MIGRATE_APPEND", -1, [],
-                             st.a + [st.recv[(PART, 0)], st.recv[(PART, 1)]], n=0)
+                             st.a_next + [st.recv[(PART, 0)], st.recv[(PART, 1)]], n=0)
 
         return [p1, p2, p3, p4]
 
@@ -281,14 +310,16 @@ class SlabMPM:
                 for ph in self.phases(st):
                     ph()
                 stats.append(st.grid.flush("all"))
-            return stats
-        per_rank = {r: self.phases(st) for r, st in self.ranks.items()}
-        for k in range(4):
-            if k == 3 and self.world == 1:
-                break
-            for r, st in self.ranks.items():
-                per_rank[r][k]()
-                stats.append(st.grid.flush("all"))
+        else:
+            per_rank = {r: self.phases(st) for r, st in self.ranks.items()}
+            for k in range(4):
+                if k == 3 and self.world == 1:
+                    break
+                for r, st in self.ranks.items():
+                    per_rank[r][k]()
+                    stats.append(st.grid.flush("all"))
+        for st in self.ranks.values():
+            st.cur = 1 - st.cur   # the new state lives in the other set
         return stats
 
     # --- inspection (tests) --------------------------------------------------

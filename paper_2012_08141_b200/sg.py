@@ -30,7 +30,7 @@ OPS = {"FILL": 1, "ADD_CONST": 2, "INC": 3, "AXPY": 4, "STENCIL": 5, "JACOBI": 6
        "LOSS_MEAN": 27, "ADJ_INIT": 28, "G2P_ADJ": 29, "P2G_ADJ": 30,
        "SMOOTH_RB": 31, "RESTRICT": 32, "PROLONG": 33, "RESID_NORM2": 34,
        "DOT": 35, "AXPY_RATIO": 36, "XPAY_RATIO": 37, "COPY_SCALAR": 38,
-       "DIST_SIGNAL": 40, "DIST_WAIT": 41, "PERMUTE": 42}
+       "DIST_SIGNAL": 40, "DIST_WAIT": 41, "PERMUTE": 42, "MIGRATE_COMPACT": 43}
 CLEAR_VALUES, DEACTIVATE = 0, 1
 PASS_LISTGEN_REMOVAL, PASS_ACT_DEMOTION, PASS_FUSION, PASS_DSE = 1, 2, 4, 8
 PASS_ALL = 15

@@ -159,7 +159,7 @@ def test_send_buffer_writes_stay_between_their_exchanges():
         checked = 0
         for pos, r in enumerate(plan):
             op, call = int(r[5]), int(r[2])
-            if op not in (11, 23, 25):      # ARRAY_COUNT, HALO_PACK, G2P_MIGRATE
+            if op not in (11, 23, 25, 43):  # ARRAY_COUNT, HALO_PACK, G2P_MIGRATE, MIGRATE_COMPACT
                 continue
             for x in (40, 41):
                 in_plan = sum(1 for q in plan[:pos] if int(q[5]) == x)
