@@ -331,13 +331,13 @@ def cpu_baseline_c5(args, thick=2):
             "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "oracle_threads": 1}
 
 
-def _timed_flushes(grid, enqueue, steps, warmup, l2=None, after_warmup=None):
+def _timed_flushes(grid, enqueue, steps, warmup, l2=None, after_warmup=None, passes="all"):
     """Device time (ms) of `steps` flushes; each flush = one step of a config."""
     import torch
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         enqueue()
-        st = grid.flush("all")
+        st = grid.flush(passes)
     torch.cuda.synchronize()
     if after_warmup:
         after_warmup()   # e.g. drop the launch profile of the warm-up (lazy module loading, allocations)
@@ -348,7 +348,7 @@ def _timed_flushes(grid, enqueue, steps, warmup, l2=None, after_warmup=None):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         enqueue()
-        st = grid.flush("all")
+        st = grid.flush(passes)
         b.record(stream)
         b.synchronize()
         ms += a.elapsed_time(b)
@@ -677,11 +677,27 @@ def measure_mg(steps=10, warmup=3, cycles=10):
 
     ms, st = _timed_flushes(g, enqueue, steps, warmup)
     res = float(np.asarray(g.field(L.fields["res"])).reshape(-1)[0])
-    return {"solves_per_s": 1000.0 / ms, "ms_per_solve": ms, "vcycles_per_s": cycles * 1000.0 / ms,
-            "launches_per_solve": st["launches"], "tasks_lowered": st["tasks_lowered"],
-            "listgens_launched": st["listgen_launched"], "listgens_removed": st["listgens_removed"],
-            "demotions": st["demotions"], "tasks_fused": st["tasks_fused"], "residual_norm2": res,
-            "active_cells_finest": int(len(calls[0]["coords"]) * 256)}
+    out = {"solves_per_s": 1000.0 / ms, "ms_per_solve": ms, "vcycles_per_s": cycles * 1000.0 / ms,
+           "launches_per_solve": st["launches"], "tasks_lowered": st["tasks_lowered"],
+           "listgens_launched": st["listgen_launched"], "listgens_removed": st["listgens_removed"],
+           "demotions": st["demotions"], "tasks_fused": st["tasks_fused"], "residual_norm2": res,
+           "residual_norm2_initial": float(len(calls[0]["coords"]) * 256),
+           "active_cells_finest": int(len(calls[0]["coords"]) * 256)}
+    out["modes"] = _modes(g, enqueue, steps, warmup)
+    return out
+
+
+def _modes(g, enqueue, steps, warmup):
+    """Passes on / off and the beyond-paper chain pass (the
+    bottom level's 64 dependent half sweeps in one one-CTA launch)."""
+    res = {}
+    for name, passes in (("optimized", "all"), ("optimized_chain", "all+chain"), ("eager", 0)):
+        ms, st = _timed_flushes(g, enqueue, steps, warmup, passes=passes)
+        res[name] = {"solves_per_s": 1000.0 / ms, "ms_per_solve": ms, "launches": st["launches"],
+                     "launches_chained": st["launches_chained"]}
+    res["speedup_passes"] = res["optimized"]["solves_per_s"] / res["eager"]["solves_per_s"]
+    res["speedup_chain_over_optimized"] = res["optimized_chain"]["solves_per_s"] / res["optimized"]["solves_per_s"]
+    return res
 
 
 def measure_mgpcg(steps=5, warmup=3, iters=10):
@@ -701,11 +717,13 @@ def measure_mgpcg(steps=5, warmup=3, iters=10):
 
     ms, st = _timed_flushes(g, enqueue, steps, warmup)
     rtr = float(np.asarray(g.field(L.fields["rTr"])).reshape(-1)[0])
-    return {"solves_per_s": 1000.0 / ms, "ms_per_solve": ms, "cg_iterations": iters,
-            "launches_per_solve": st["launches"], "tasks_lowered": st["tasks_lowered"],
-            "listgens_launched": st["listgen_launched"], "listgens_removed": st["listgens_removed"],
-            "demotions": st["demotions"], "tasks_fused": st["tasks_fused"], "dead_removed": st["dead_removed"],
-            "final_rTr": rtr}
+    out = {"solves_per_s": 1000.0 / ms, "ms_per_solve": ms, "cg_iterations": iters,
+           "launches_per_solve": st["launches"], "tasks_lowered": st["tasks_lowered"],
+           "listgens_launched": st["listgen_launched"], "listgens_removed": st["listgens_removed"],
+           "demotions": st["demotions"], "tasks_fused": st["tasks_fused"], "dead_removed": st["dead_removed"],
+           "final_rTr": rtr, "initial_rTr": float(len(calls[0]["coords"]) * 256)}
+    out["modes"] = _modes(g, enqueue, steps, warmup)
+    return out
 
 
 def c5_sim(args, rank, world, local, uid=None):

@@ -72,9 +72,6 @@ struct sg_grid {
   std::unordered_map<uint64_t, uint64_t> gsig;   // launch-argument signature of each exec's last capture
   std::unordered_map<uint64_t, int> plan_runs;
   int num_sms = 148;
-  char* chain_buf = nullptr;        // SG_PASS_CHAIN op tables
-  size_t chain_bytes = 0;
-  std::vector<char> chain_host;
   uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
   uint64_t mig_tiles = 0;
   uint32_t* mig_ctl = nullptr;

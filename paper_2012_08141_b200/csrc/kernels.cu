@@ -1242,25 +1242,16 @@ int launch_clear_list(const DList& l, void* stream) {
 static int ilog2(uint64_t v) { int r = 0; while ((1ull << r) < v) r++; return r; }
 
 template <typename V, int ND, bool PAIR, int GL>
-static void sf_dispatch(SFArgs* a, int grid, cudaStream_t s, const DOp* optab, const int* phase_end, int nphases) {
-  if (nphases <= 1) {
+static void sf_dispatch(SFArgs* a, int grid, cudaStream_t s, const ChainTab* chain) {
+  if (!chain) {
     k_struct_for<V, ND, PAIR, GL><<<grid, SF_TPB, 0, s>>>(*a);
     return;
   }
-  // cooperative launch: every CTA resident (grid-wide barriers between phases)
-  auto kern = k_struct_chain<V, ND, PAIR, GL>;
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SF_TPB, 0) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
-  }
-  int g = std::max(1, std::min(grid, per_sm * num_sms()));
-  void* args[] = {(void*)a, (void*)&optab, (void*)&phase_end, (void*)&nphases};
-  cudaLaunchCooperativeKernel((const void*)kern, dim3(g), dim3(SF_TPB), args, 0, s);
+  k_struct_chain<V, ND, PAIR, GL><<<1, SF_TPB, 0, s>>>(*a, *chain);
 }
 
 int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, const DOp* ops, int nops,
-                      int task, void* stream, int grid_hint, const DOp* dev_optab, const int* dev_phase_end,
+                      int task, void* stream, int grid_hint, const DOp* chain_ops, const int* chain_phase_end,
                       int nphases, int chain_needs_nbr) {
   SFArgs* a = new SFArgs();
   a->T = t; a->C = c; a->task = task; a->nops = nops;
@@ -1301,8 +1292,16 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   }
   // one resident wave: 5 CTAs per SM (__launch_bounds__(SF_TPB, 5)); tiles are
   // sized on the device so every CTA gets an equal share
-  (void)grid_hint;
   int grid = num_sms() * 5;
+  (void)grid_hint;
+  ChainTab* ct = nullptr;
+  if (nphases > 1) {   // one-CTA chain (the caller checked the list is small and the table fits)
+    ct = new ChainTab();
+    const int tot = chain_phase_end[nphases - 1];
+    for (int i = 0; i < tot && i < SG_CHAIN_OPS; i++) ct->ops[i] = chain_ops[i];
+    for (int i = 0; i < nphases && i < SG_CHAIN_OPS; i++) ct->phase_end[i] = chain_phase_end[i];
+    ct->nphases = nphases;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const int nd = quad ? t.nd : 0;
   static int pair = -1;
@@ -1332,18 +1331,19 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   }
 #define SG_SF_LAUNCH(V)                                                                           \
   switch (nd * 10 + gl) {                                                                         \
-    case 10: sf_dispatch<V, 1, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
-    case 20: sf_dispatch<V, 2, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
-    case 23: sf_dispatch<V, 2, false, 3>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
-    case 30: if (pair && stencil) sf_dispatch<V, 3, true, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); \
-             else sf_dispatch<V, 3, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;          \
-    case 31: sf_dispatch<V, 3, false, 1>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
-    case 32: sf_dispatch<V, 3, false, 2>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
-    default: sf_dispatch<V, 0, false, 0>(a, grid, s, dev_optab, dev_phase_end, nphases); break;   \
+    case 10: sf_dispatch<V, 1, false, 0>(a, grid, s, ct); break;   \
+    case 20: sf_dispatch<V, 2, false, 0>(a, grid, s, ct); break;   \
+    case 23: sf_dispatch<V, 2, false, 3>(a, grid, s, ct); break;   \
+    case 30: if (pair && stencil) sf_dispatch<V, 3, true, 0>(a, grid, s, ct); \
+             else sf_dispatch<V, 3, false, 0>(a, grid, s, ct); break;          \
+    case 31: sf_dispatch<V, 3, false, 1>(a, grid, s, ct); break;   \
+    case 32: sf_dispatch<V, 3, false, 2>(a, grid, s, ct); break;   \
+    default: sf_dispatch<V, 0, false, 0>(a, grid, s, ct); break;   \
   }
   if (i32) { SG_SF_LAUNCH(int) } else { SG_SF_LAUNCH(float) }
 #undef SG_SF_LAUNCH
   delete a;
+  delete ct;
   return check_launch();
 }
 

@@ -485,6 +485,18 @@ static void make_op(const sg_grid* g, const PTask& t, uint32_t act, int loop_tre
   }
 }
 
+constexpr uint64_t CHAIN_SOLO_CELLS = 8192;
+
+// A chained group over a list of more than CHAIN_SOLO_CELLS cells launches its
+// phases one by one (see launch_group).
+static bool chain_is_split(const sg_grid* g, const PTask& t0, size_t nops = 0, size_t nphases = 0) {
+  if (nops > 96 || nphases > 96) return true;   // SG_CHAIN_OPS: the table must fit the kernel parameters
+  const DTree& T = g->dtrees[t0.tree];
+  const DList* drive = T.driving >= 0 ? &g->lists[t0.tree][T.driving] : nullptr;
+  const uint64_t cap = drive && drive->entries ? (uint64_t)drive->capacity : (T.driving >= 0 ? 0xFFFFFFFFull : 1ull);
+  return (cap << T.lblk) > CHAIN_SOLO_CELLS;
+}
+
 static int grid_hint_struct(const sg_grid* g, const DTree& T) {
   (void)T;
   return g->num_sms * 8;
@@ -595,21 +607,25 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
           nbr |= op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER || op == SG_OP_SMOOTH_RB ||
                  op == SG_OP_RESTRICT || op == SG_OP_RESID_NORM2;
         }
-        const size_t bytes = nops * sizeof(DOp) + phase_end.size() * sizeof(int) + 64;
-        if (bytes > g->chain_bytes) {
-          g->chain_buf = (char*)g->dev_alloc(std::max<size_t>(bytes, 64 * 1024));
-          if (!g->chain_buf) return fail(SG_ERR_CUDA, "chain op table allocation failed");
-          g->chain_bytes = std::max<size_t>(bytes, 64 * 1024);
+        // a chain pays off only when its barriers are CTA barriers: lists of at
+        // most CHAIN_SOLO_CELLS cells (the MG bottom level) run as ONE CTA with
+        // every phase in it; larger lists launch the phases one by one (a
+        // grid-wide barrier costs more than a graph-replayed launch, measured)
+        if (chain_is_split(g, t0, (size_t)nops, phase_end.size())) {
+          int begin = 0;
+          for (size_t ph = 0; ph < phase_end.size() && !rc; ph++) {
+            const int end = phase_end[ph];
+            rc = launch_struct_for(g->ctx, T, t0.tree, drive, all.data() + begin, end - begin, task, g->stream,
+                                   grid_hint_struct(g, T), nullptr, nullptr, 1, 0);
+            begin = end;
+            if (ph + 1 < phase_end.size()) st.launches++;
+          }
+          break;
         }
-        // the host staging copy must stay valid until the async copy ran: one buffer per grid
-        g->chain_host.resize(bytes);
-        std::memcpy(g->chain_host.data(), all.data(), nops * sizeof(DOp));
-        std::memcpy(g->chain_host.data() + nops * sizeof(DOp), phase_end.data(), phase_end.size() * sizeof(int));
-        CUDA_TRY(cudaMemcpyAsync(g->chain_buf, g->chain_host.data(), bytes - 64, cudaMemcpyHostToDevice, g->stream));
+        // one-CTA chain: the whole op table travels in the kernel parameters
         const int last0 = phase_end[phase_end.size() - 2], nlast = nops - last0;
-        rc = launch_struct_for(g->ctx, T, t0.tree, drive, all.data() + last0, nlast, task, g->stream,
-                               grid_hint_struct(g, T), (const DOp*)g->chain_buf,
-                               (const int*)(g->chain_buf + nops * sizeof(DOp)), (int)phase_end.size(), nbr);
+        rc = launch_struct_for(g->ctx, T, t0.tree, drive, all.data() + last0, nlast, task, g->stream, 1, all.data(),
+                               phase_end.data(), (int)phase_end.size(), nbr);
         st.launches_chained++;
       }
     } break;
@@ -773,14 +789,13 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
   st.plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
   sg_status rc = SG_OK;
   g->task_counter = 0;
-  // CUDA graph replay of a plan that already ran once (its allocations done);
-  // chains upload a host op table per flush and stay on direct launches
+  // CUDA graph replay of a plan that already ran once (its allocations done)
   bool capturing = false;
   const cudaStream_t user = g->stream;
   uint64_t sig = 0;
   if (!g->plan_only && g->use_graphs && !g->profiling && g->plan_runs[key]++ > 0) {
-    bool chain = false;
-    for (const auto& pe : plan->phase_ends) chain |= pe.size() > 1;
+    // (chains carry their op tables in the kernel parameters: capturable like any launch)
+    const bool chain = false;
     // signature of everything a capture bakes into launch arguments beyond the
     // plan: activation buffers, the array table, list / bin capacities
     sig = 1469598103934665603ull;
@@ -803,7 +818,6 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
     for (const DArray& a : g->arrays) { mix((uint64_t)(uintptr_t)a.ptr); mix((uint64_t)a.n); mix((uint64_t)(uintptr_t)a.dcount); }
     mix((uint64_t)g->bin_cap);
     mix((uint64_t)g->bin_keys_cap);
-    mix((uint64_t)g->chain_bytes);
     auto ex = g->gexec.find(key);
     if (!chain && ex != g->gexec.end() && ex->second && g->gsig[key] == sig) {
       // identical window: relaunch the graph as captured
@@ -818,7 +832,11 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         st.launches++;
         if (t.type == TT_LISTGEN) st.listgen_launched++;
         if (t.type == TT_CLEAR_LIST) st.clear_list_launched++;
-        if (plan->phase_ends[gi].size() > 1) st.launches_chained++;
+        if (plan->phase_ends[gi].size() > 1) {
+          if (chain_is_split(g, t, mem.size(), plan->phase_ends[gi].size()))
+            st.launches += (int64_t)plan->phase_ends[gi].size() - 1;
+          else st.launches_chained++;
+        }
       }
       st.aux_kernels = g->gaux[key];
       sg_status rc2 = SG_OK;

@@ -163,7 +163,7 @@ int launch_clear_list(const DList& l, void* stream);
 // nphases > 1: a chain (SG_PASS_CHAIN) -- `ops` are the LAST phase's ops (reductions),
 // the whole op table and the phase ends are in device memory.
 int launch_struct_for(const DevCtx& c, const DTree& t, int tree_id, const DList* drive, const DOp* ops, int nops,
-                      int task_id, void* stream, int grid_hint, const DOp* dev_optab, const int* dev_phase_end,
+                      int task_id, void* stream, int grid_hint, const DOp* chain_ops, const int* chain_phase_end,
                       int nphases, int chain_needs_nbr);
 struct RangeScratch {
   uint64_t* status;   // look-back descriptors for G2P_MIGRATE tiles

@@ -896,36 +896,39 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
 }
 
 // Beyond the paper (SG_PASS_CHAIN): a chain of struct-for phases
-// over one list in ONE cooperative launch; phase p+1 starts after a grid-wide
-// barrier, so dependent stencils (Jacobi sweeps) chain without a kernel
-// boundary.  Op table and phase ends come from device memory; reductions are
-// allowed in the last phase only (their aux / s_red slots are that phase's).
+// over one SMALL list in ONE launch of ONE CTA; phase p+1 starts after a CTA
+// barrier, so dependent stencils (the multigrid bottom smoother's 64 half
+// sweeps) chain without a kernel boundary.  The op table travels in the
+// kernel parameters (graph-capturable, no upload); reductions are allowed in
+// the last phase only (their aux / s_red slots are that phase's).  Larger
+// lists launch their phases one by one (sg_api.cu: a grid-wide barrier costs
+// more than a graph-replayed launch).
+constexpr int SG_CHAIN_OPS = 96;
+struct ChainTab {
+  DOp ops[SG_CHAIN_OPS];
+  int phase_end[SG_CHAIN_OPS];
+  int nphases;
+};
+
 template <typename V, int ND, bool PAIR, int GL>
-__global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5)
-    k_struct_chain(const __grid_constant__ SFArgs A, const DOp* __restrict__ optab, const int* __restrict__ phase_end,
-                   int nphases) {
+__global__ void __launch_bounds__(SF_TPB, 1)
+    k_struct_chain(const __grid_constant__ SFArgs A, const __grid_constant__ ChainTab CT) {
   __shared__ SFTile tile;
-  __shared__ DOp s_ops[SG_MAXOPS];
-  cg::grid_group grid = cg::this_grid();
   if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
   const bool rows_ok0 = A.table && A.table_ctl[4] != 0u;
   int begin = 0;
   int last_n = 0;
-  for (int p = 0; p < nphases; p++) {
-    const int end = phase_end[p], n = end - begin;
-    for (int i = threadIdx.x; i < n * (int)(sizeof(DOp) / 4); i += SF_TPB)
-      reinterpret_cast<uint32_t*>(s_ops)[i] = reinterpret_cast<const uint32_t*>(optab + begin)[i];
-    __syncthreads();
+  for (int p = 0; p < CT.nphases; p++) {
+    const int end = CT.phase_end[p], n = end - begin;
     // rows built by phase 0 are visible to the later phases after the barrier
-    sf_tiles<V, ND, PAIR, GL>(A, s_ops, n, tile, rows_ok0 || p > 0, p > 0);
+    sf_tiles<V, ND, PAIR, GL>(A, CT.ops + begin, n, tile, rows_ok0 || p > 0, p > 0);
     last_n = n;
-    begin = end;
-    if (p + 1 < nphases) {
-      __threadfence();
-      grid.sync();
+    if (p + 1 < CT.nphases) {
+      __syncthreads();
+      begin = end;
     }
   }
-  if (A.has_reduce) finish_reductions<V>(A, s_ops, last_n);
+  if (A.has_reduce) finish_reductions<V>(A, CT.ops + begin, last_n);
   sf_mark_table(A, rows_ok0);
 }
 

@@ -105,3 +105,20 @@ def test_mgpcg_full_size(iters):
     rTr = float(np.asarray(g.field(prog["layout"].fields["rTr"])).reshape(-1)[0])
     if iters == 10:
         assert np.isfinite(rTr) and rTr < 1e-3 * 88064.0, rTr
+
+
+@pytest.mark.parametrize("which", ["mg", "mgpcg"])
+def test_chain_pass_full_size(which):
+    """SG_PASS_CHAIN (beyond the paper) at the bench size: the
+    bottom level's dependent half sweeps run as ONE one-CTA launch; results
+    within 1e-5 of the oracle like the unchained plan."""
+    prog = W.mg_program(n=512, cycles=2) if which == "mg" else W.mgpcg_program(n=512, iters=2)
+    o = oracle.run_program(prog)
+    g = sg.Grid(prog["desc"])
+    st = sg.replay(g, prog, passes="all+chain", device="cuda")
+    g.sync()
+    compare(g, o, prog)
+    assert st[0]["launches_chained"] >= 2
+    g2 = sg.Grid(prog["desc"])
+    st2 = sg.replay(g2, prog, passes="all", device="cuda")
+    assert st[0]["launches"] < st2[0]["launches"] - 100
