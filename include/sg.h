@@ -341,6 +341,27 @@ sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int32_t n_kind
  * (pool base, stride words, capacity, payload offset words). */
 sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
 
+/* JIT-specialized fusion (PAPER.md:265-266 parallel
+ * compilation, PAPER.md:394-396 the IR bank): every fused struct-for group is
+ * hashed by its content (ops, operand slots, activation bits, parameters,
+ * block geometry, value type); worker threads compile a kernel whose op table
+ * is a compile-time constant with NVRTC for sm_100a and cache it by the hash;
+ * launches of that content use it once ready (the op-table interpreter runs
+ * meanwhile; CUDA graphs are recaptured).  Env SG_JIT: 0 off, 1 asynchronous
+ * (default), 2 synchronous (first launch waits: tests and benchmarks).
+ * out (n <= 7 int64): [mode, kernels ready, compiling, failed, hits, misses,
+ * total compile time in microseconds]. */
+sg_status sg_jit_info(int64_t* out, int32_t n);
+/* Process-wide JIT mode (0, 1, 2 as SG_JIT; -1 = back to the environment). */
+sg_status sg_jit_set_mode(int32_t mode);
+/* Host-side check (no GPU needed): NVRTC-compiles, without loading, the
+ * specialized kernel of a group of `nops` op codes with placeholder operands
+ * (nd / gl: quad-path dimensionality and constant block geometry, i32: value
+ * type); the compile log is copied into log (cap bytes).  SG_ERR_STATE when
+ * NVRTC is missing or the compile fails. */
+sg_status sg_jit_selftest(int32_t nd, int32_t gl, int32_t i32, const int32_t* ops, int32_t nops, char* log,
+                          int64_t cap);
+
 /* Thread-local message of the last failing call on this thread (SPEC.md:50,
  * :59, :78 error conventions). */
 const char* sg_last_error(void);

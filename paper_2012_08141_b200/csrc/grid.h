@@ -71,6 +71,7 @@ struct sg_grid {
   std::unordered_map<uint64_t, int64_t> gaux;   // aux kernels captured in each plan's graph
   std::unordered_map<uint64_t, uint64_t> gsig;   // launch-argument signature of each exec's last capture
   std::unordered_map<uint64_t, int> plan_runs;
+  std::unordered_map<uint64_t, char> jit_prefetched;   // plans whose groups were submitted to the JIT
   int num_sms = 148;
   uint64_t* mig_status = nullptr;   // G2P_MIGRATE look-back scratch
   uint64_t mig_tiles = 0;

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "grid.h"
+#include "jit.h"
 #include "planner.h"
 #include "sg_internal.h"
 
@@ -816,6 +817,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
     mix((uint64_t)(uintptr_t)g->d_arrays);
     mix((uint64_t)g->arrays.size());
     for (const DArray& a : g->arrays) { mix((uint64_t)(uintptr_t)a.ptr); mix((uint64_t)a.n); mix((uint64_t)(uintptr_t)a.dcount); }
+    mix((uint64_t)jit_generation());   // a specialized kernel became ready: recapture
     mix((uint64_t)g->bin_cap);
     mix((uint64_t)g->bin_keys_cap);
     auto ex = g->gexec.find(key);
@@ -856,6 +858,23 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         cudaGetLastError();
       }
     }
+  }
+  // parallel compilation: submit every struct-for group's
+  // specialized kernel before the first launch, so they compile concurrently
+  if (!g->plan_only && !g->jit_prefetched[key]) {
+    g->jit_prefetched[key] = 1;
+    int64_t jm[1] = {0};
+    jit_stats(jm, 1);
+    if (jm[0])
+      for (size_t gi = 0; gi < plan->groups.size(); gi++) {
+        const PTask& t0 = g->eager[plan->groups[gi][0]];
+        if (t0.type != TT_STRUCT_FOR || plan->phase_ends[gi].size() > 1) continue;
+        DOp ops[SG_MAXOPS];
+        const int nops = (int)plan->groups[gi].size();
+        for (int i = 0; i < nops; i++) make_op(g, g->eager[plan->groups[gi][i]], plan->acts[gi][i], t0.tree, ops[i]);
+        JitGroup G;
+        if (jit_group_of(g->dtrees[t0.tree], ops, nops, G)) jit_lookup(G, true);
+      }
   }
   for (size_t gi = 0; gi < plan->groups.size(); gi++) {
     const auto& mem = plan->groups[gi];
@@ -1123,3 +1142,22 @@ extern "C" sg_status sg_profile_read(sg_grid* g, double* ms, int64_t* count, int
 }
 
 extern "C" const char* sg_last_error(void) { return g_err.c_str(); }
+
+extern "C" sg_status sg_jit_info(int64_t* out, int32_t n) {
+  if (!out || n < 1) return fail(SG_ERR_ARG, "null output");
+  jit_stats(out, n);
+  return SG_OK;
+}
+
+extern "C" sg_status sg_jit_set_mode(int32_t mode) {
+  if (mode < -1 || mode > 2) return fail(SG_ERR_ARG, "JIT mode is -1 (env), 0, 1 or 2");
+  jit_set_mode(mode);
+  return SG_OK;
+}
+
+extern "C" sg_status sg_jit_selftest(int32_t nd, int32_t gl, int32_t i32, const int32_t* ops, int32_t nops,
+                                     char* log, int64_t cap) {
+  if (!ops || nops < 1 || nops > SG_MAXOPS) return fail(SG_ERR_ARG, "bad op list");
+  const int rc = jit_selftest(nd, gl, i32, ops, nops, log, cap);
+  return rc == 0 ? SG_OK : fail(SG_ERR_STATE, "NVRTC compile failed (" + std::to_string(rc) + ")");
+}

@@ -45,6 +45,19 @@ struct SFArgs {
 
 constexpr int SF_TPB = 256, SF_MAXE = 256;
 
+// Op sources of a fused group.  OpsRT: the op table of the launch (kernel
+// parameters).  A JIT-specialized kernel (jit.cpp) passes a type
+// whose operator[] returns compile-time constant DOps and whose size is a
+// constant: the op loops unroll, every switch on the op code and every slot /
+// parameter folds into the instruction stream.
+struct OpsRT {
+  static constexpr int kUnroll = 1;
+  const DOp* p;
+  int n;
+  __device__ __forceinline__ const DOp& operator[](int i) const { return p[i]; }
+  __device__ __forceinline__ int size() const { return n; }
+};
+
 struct SFTile {
   uint32_t blk[SF_MAXE];
   uint32_t maskw[SF_MAXE];
@@ -100,8 +113,9 @@ __device__ __forceinline__ void warp_add(int o, V v) {
   if ((threadIdx.x & 31) == 0 && d != 0.0) atomicAdd(&s_red[o], d);
 }
 
-template <typename V>
-__device__ void finish_reductions(const SFArgs& A, const DOp* ops, int nops) {
+template <typename V, class OPS>
+__device__ void finish_reductions(const SFArgs& A, const OPS& ops) {
+  const int nops = ops.size();
   __shared__ bool s_last;
   __shared__ double s_sum[SF_TPB];
   __syncthreads();
@@ -113,6 +127,7 @@ __device__ void finish_reductions(const SFArgs& A, const DOp* ops, int nops) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+#pragma unroll(OPS::kUnroll)
   for (int o = 0; o < nops; o++) {
     if (ops[o].op != SG_OP_REDUCE_SUM && ops[o].op != SG_OP_RESID_NORM2 && ops[o].op != SG_OP_DOT) continue;
     double t = 0.0;   // fixed-order tree sum over CTAs
@@ -453,12 +468,14 @@ __device__ __forceinline__ void run_lanes(const SFArgs& A, const DOp& op, int o,
   if (op.op == SG_OP_RESID_NORM2 || op.op == SG_OP_DOT) warp_add<V>(o, acc);
 }
 
-template <typename V, int ND, bool PAIR, int GL>
-__device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int nops, const SFTile& tile, uint32_t* P,
+template <typename V, int ND, bool PAIR, int GL, class OPS>
+__device__ __forceinline__ void run_quads(const SFArgs& A, const OPS& ops, const SFTile& tile, uint32_t* P,
                                           uint32_t nq, uint32_t lq, bool chunked, uint32_t jbase, uint64_t fs) {
   const QG g = make_qg<GL>(A);
+  const int nops = ops.size();
+#pragma unroll(OPS::kUnroll)
   for (int o = 0; o < nops; o++) {
-    const DOp& op = ops[o];
+    decltype(auto) op = ops[o];
     const uint64_t s0 = (uint64_t)op.slot[0] * fs, s1 = (uint64_t)(op.slot[1] < 0 ? 0 : op.slot[1]) * fs,
                    s2 = (uint64_t)(op.slot[2] < 0 ? 0 : op.slot[2]) * fs;
     switch (op.op) {
@@ -704,13 +721,15 @@ __device__ __forceinline__ void run_quads(const SFArgs& A, const DOp* ops, int n
   }
 }
 
-template <typename V>
-__device__ __forceinline__ void run_cells(const SFArgs& A, const DOp* ops, int nops, const SFTile& tile, uint32_t* P,
+template <typename V, class OPS>
+__device__ __forceinline__ void run_cells(const SFArgs& A, const OPS& ops, const SFTile& tile, uint32_t* P,
                                           uint32_t tcells, bool chunked, uint32_t jbase, uint64_t fs) {
   const DTree& T = A.T;
   const int lblk = T.lblk;
+  const int nops = ops.size();
+#pragma unroll(OPS::kUnroll)
   for (int o = 0; o < nops; o++) {
-    const DOp& op = ops[o];
+    decltype(auto) op = ops[o];
     V acc = V(0);
     if (op.op == SG_OP_HALO_PACK) {
       int nf = 0;
@@ -758,8 +777,8 @@ __device__ __forceinline__ void run_cells(const SFArgs& A, const DOp* ops, int n
 // the kernels
 // ---------------------------------------------------------------------------
 // One pass over every tile of the list with the given op list.
-template <typename V, int ND, bool PAIR, int GL>
-__device__ __forceinline__ void sf_tiles(const SFArgs& A, const DOp* ops, int nops, SFTile& tile, bool rows_ok,
+template <typename V, int ND, bool PAIR, int GL, class OPS>
+__device__ __forceinline__ void sf_tiles(const SFArgs& A, const OPS& ops, SFTile& tile, bool rows_ok,
                                          bool tile_cached = false) {
   const DTree& T = A.T;
   uint32_t* P = T.seg[T.nseg - 1].base;
@@ -863,9 +882,9 @@ __device__ __forceinline__ void sf_tiles(const SFArgs& A, const DOp* ops, int no
     }
     __syncthreads();
     if (ND > 0)
-      run_quads<V, (ND > 0 ? ND : 1), PAIR, GL>(A, ops, nops, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked,
-                                                jbase, fs);
-    else run_cells<V>(A, ops, nops, tile, P, tcells, chunked, jbase, fs);
+      run_quads<V, (ND > 0 ? ND : 1), PAIR, GL>(A, ops, tile, P, tcells >> 2, (uint32_t)lblk - 2, chunked, jbase,
+                                                fs);
+    else run_cells<V>(A, ops, tile, P, tcells, chunked, jbase, fs);
     __syncthreads();
   }
 }
@@ -890,8 +909,9 @@ __global__ void __launch_bounds__(SF_TPB, PAIR ? 3 : 5) k_struct_for(const __gri
   __shared__ SFTile tile;
   if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
   const bool rows_ok = A.table && A.table_ctl[4] != 0u;   // set by an earlier launch
-  sf_tiles<V, ND, PAIR, GL>(A, A.ops, A.nops, tile, rows_ok);
-  if (A.has_reduce) finish_reductions<V>(A, A.ops, A.nops);
+  const OpsRT ops{A.ops, A.nops};
+  sf_tiles<V, ND, PAIR, GL>(A, ops, tile, rows_ok);
+  if (A.has_reduce) finish_reductions<V>(A, ops);
   sf_mark_table(A, rows_ok);
 }
 
@@ -921,14 +941,14 @@ __global__ void __launch_bounds__(SF_TPB, 1)
   for (int p = 0; p < CT.nphases; p++) {
     const int end = CT.phase_end[p], n = end - begin;
     // rows built by phase 0 are visible to the later phases after the barrier
-    sf_tiles<V, ND, PAIR, GL>(A, CT.ops + begin, n, tile, rows_ok0 || p > 0, p > 0);
+    sf_tiles<V, ND, PAIR, GL>(A, OpsRT{CT.ops + begin, n}, tile, rows_ok0 || p > 0, p > 0);
     last_n = n;
     if (p + 1 < CT.nphases) {
       __syncthreads();
       begin = end;
     }
   }
-  if (A.has_reduce) finish_reductions<V>(A, CT.ops + begin, last_n);
+  if (A.has_reduce) finish_reductions<V>(A, OpsRT{CT.ops + begin, last_n});
   sf_mark_table(A, rows_ok0);
 }
 

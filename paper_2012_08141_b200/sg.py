@@ -512,3 +512,37 @@ def dist_info(grid):
     return {"transport": TRANSPORTS.get(v[0], v[0]), "rank": v[1], "world": v[2], "axis": v[3],
             "send": {(k, s): v[4 + 2 * k + s] for k in range(3) for s in range(2)},
             "recv": {(k, s): v[10 + 2 * k + s] for k in range(3) for s in range(2)}}
+
+
+_lib.sg_jit_info.argtypes = [_P(ctypes.c_int64), ctypes.c_int32]
+_lib.sg_jit_info.restype = ctypes.c_int32
+EXPORTS += ["sg_jit_info"]
+
+
+def jit_info():
+    """{mode, ready, compiling, failed, hits, misses, compile_ms} of the NVRTC-specialized kernels."""
+    out = (ctypes.c_int64 * 7)()
+    _check(_lib.sg_jit_info(out, 7))
+    v = list(out)
+    return {"mode": v[0], "ready": v[1], "compiling": v[2], "failed": v[3], "hits": v[4], "misses": v[5],
+            "compile_ms": v[6] / 1000.0}
+
+_lib.sg_jit_selftest.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P(ctypes.c_int32), ctypes.c_int32,
+                                 ctypes.c_char_p, ctypes.c_int64]
+_lib.sg_jit_selftest.restype = ctypes.c_int32
+_lib.sg_jit_set_mode.argtypes = [ctypes.c_int32]
+_lib.sg_jit_set_mode.restype = ctypes.c_int32
+EXPORTS += ["sg_jit_selftest", "sg_jit_set_mode"]
+
+
+def jit_set_mode(mode):
+    """0 off, 1 asynchronous, 2 synchronous, -1 back to SG_JIT."""
+    _check(_lib.sg_jit_set_mode(int(mode)))
+
+
+def jit_selftest(ops, nd=3, gl=1, i32=False):
+    """NVRTC-compile (no GPU) a specialized kernel for the op names; returns (ok, log)."""
+    arr = (ctypes.c_int32 * len(ops))(*[OPS[o] for o in ops])
+    log = ctypes.create_string_buffer(1 << 16)
+    rc = _lib.sg_jit_selftest(nd, gl, int(i32), arr, len(ops), log, len(log))
+    return rc == 0, log.value.decode(errors="replace")
