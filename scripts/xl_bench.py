@@ -62,12 +62,14 @@ def jac_xl(iters=10, radius=288.0):
             "frac": ach / peak, "launches": n}
 
 
-def sf_xl(iters=10, radius=288.0):
+def sf_xl(iters=10, radius=288.0, jit=False):
     """SF-XL: the generic fused megakernel (k_struct_for op table) at JAC-XL
     size: JACOBI fused with the residual-style reduction s += x1 (PAPER.md:440
     "fuse the Jacobi smoothing and reduction kernels"), one launch per
     iteration.  Algorithmic bytes: 12 B per active cell (read x0, b; write x1;
     the reduction reads x1 from the thread's registers)."""
+    if not jit:
+        sg.jit_set_mode(0)
     L, lv = W.c2_layout(ptr=32)
     f = L.fields
     coords = W.block_ball_coords(128, 8, radius)
@@ -92,9 +94,14 @@ def sf_xl(iters=10, radius=288.0):
         return sg.profile_read(g).get(100 + sg.OPS["JACOBI"], (0.0, 0)), st
 
     solve(2)
+    solve(1)
+    solve(iters + 1)   # every group content of the timed flushes compiled (JIT) and warm
+    solve(1)
     sg.set_profiling(g, True)
     (t1, _), _ = solve(1)
     (tk, nk), st = solve(iters + 1)
+    if not jit:
+        sg.jit_set_mode(-1)
     ms, n = tk - t1, iters
     nbytes = len(coords) * 512 * 12
     peak, kind = bench.hbm_peak()
@@ -103,6 +110,20 @@ def sf_xl(iters=10, radius=288.0):
             "cells": len(coords) * 512, "bytes_per_launch": nbytes, "avg_launch_us": ms / n * 1e3,
             "achieved_GBps": ach, "peak_GBps": peak, "peak_source": kind, "frac": ach / peak, "launches": n,
             "tasks_fused": st["tasks_fused"]}
+
+
+def sf_xl_jit(**kw):
+    """SF-XL with the group's NVRTC-specialized kernel (JIT
+    synchronous, so every timed launch runs it) beside the interpreter's."""
+    sg.jit_set_mode(2)
+    try:
+        r = sf_xl(jit=True, **kw)
+    finally:
+        sg.jit_set_mode(-1)
+    r["variant"] = "SF-XL (JIT-specialized)"
+    r["kernel"] = "NVRTC-specialized JACOBI+REDUCE_SUM (jit.cpp)"
+    r["jit"] = sg.jit_info()
+    return r
 
 
 def lg_xl(reps=15, p_ptr=0.25, p_bit=0.10, seed=0):
@@ -217,3 +238,5 @@ if __name__ == "__main__":
         print(json.dumps(act_xl()), flush=True)
     if "sf" in which:
         print(json.dumps(sf_xl()), flush=True)
+    if "sfjit" in which:
+        print(json.dumps(sf_xl_jit()), flush=True)
