@@ -917,7 +917,10 @@ def main():
                              ("c2_chain", measure_c2_chain), ("c1", measure_c1), ("c3", measure_c3),
                              ("c4", measure_c4), ("mg", measure_mg), ("mgpcg", measure_mgpcg),
                              ("c5_1gpu", lambda: measure_c5_1gpu(args)),
-                             ("jac_xl", xl_bench.jac_xl), ("sf_xl", xl_bench.sf_xl), ("lg_xl", xl_bench.lg_xl),
+                             ("jac_xl", xl_bench.jac_xl), ("sf_xl", xl_bench.sf_xl),
+                             ("sf_xl_interpreter", lambda: xl_bench.sf_xl(interpreter=True)),
+                             ("cg_xl", lambda: xl_bench.sf_xl(group="axpy_dot")),
+                             ("cg_xl_jit", lambda: xl_bench.sf_xl_jit(group="axpy_dot")), ("lg_xl", xl_bench.lg_xl),
                              ("act_xl", xl_bench.act_xl)):
                 try:
                     extra[name] = fn()
@@ -927,7 +930,7 @@ def main():
             out["roofline_xl"] = {k: {"achieved": extra[k].get("achieved_GBps"), "frac": extra[k].get("frac"),
                                       "peak": extra[k].get("peak_GBps"), "unit": "GB/s",
                                       "bytes_per_launch": extra[k].get("bytes_per_launch")}
-                                  for k in ("jac_xl", "sf_xl", "lg_xl")}
+                                  for k in ("jac_xl", "sf_xl", "sf_xl_interpreter", "cg_xl", "cg_xl_jit", "lg_xl")}
             jx = extra.get("jac_xl", {})
             if "frac" in jx:
                 out["roofline_hbm"] = {"bound": "hbm", "kernel": "k_jacobi8 at JAC-XL (1024^3, 206K 8^3 blocks)",

@@ -1022,7 +1022,10 @@ bool jit_group_of(const DTree& t, const DOp* ops, int nops, JitGroup& G) {
   else if (nd == 3 && lb[0] == 2 && lb[1] == 2 && lb[2] == 2) gl = 2;
   else if (nd == 2 && lb[0] == 2 && lb[1] == 2) gl = 3;
   const bool i32 = ops[0].dt == SG_I32;
-  if (nops == 1 && ops[0].op == SG_OP_JACOBI && gl == 1 && !i32 && !t.leaf_bitmasked) return false;   // k_jacobi8
+  const bool jac_red = nops == 2 && ops[0].op == SG_OP_JACOBI && ops[1].op == SG_OP_REDUCE_SUM &&
+                       ops[1].f[1] == ops[0].f[0] && ops[1].scalar >= 0;
+  if ((nops == 1 || jac_red) && ops[0].op == SG_OP_JACOBI && gl == 1 && !i32 && !t.leaf_bitmasked)
+    return false;   // k_jacobi8
   G.nops = nops; G.nd = nd; G.gl = gl; G.i32 = i32 ? 1 : 0;
   for (int o = 0; o < nops; o++) G.ops[o] = ops[o];
   return true;
@@ -1093,17 +1096,25 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   else if (nd == 3 && a->lb[0] == 2 && a->lb[1] == 2 && a->lb[2] == 2) gl = 2;
   else if (nd == 2 && a->lb[0] == 2 && a->lb[1] == 2) gl = 3;
   // dedicated kernel: a lone f32 JACOBI over 8^3 dense blocks with a block table
-  if (nops == 1 && ops[0].op == SG_OP_JACOBI && gl == 1 && !i32 && !t.leaf_bitmasked && nphases <= 1 && drive &&
-      drive->table && getenv("SG_NO_JAC8") == nullptr) {
+  // dedicated kernel: a lone f32 JACOBI over 8^3 dense blocks with a block
+  // table, or JACOBI fused with the reduction of its output
+  const bool jac_red = nops == 2 && ops[0].op == SG_OP_JACOBI && ops[1].op == SG_OP_REDUCE_SUM &&
+                       ops[1].f[1] == ops[0].f[0] && ops[1].scalar >= 0;
+  if ((nops == 1 || jac_red) && ops[0].op == SG_OP_JACOBI && gl == 1 && !i32 && !t.leaf_bitmasked && nphases <= 1 &&
+      drive && drive->table && getenv("SG_NO_JAC8") == nullptr) {
     JacArgs j;
     j.T = t; j.entries = drive->entries; j.count = drive->count; j.table = drive->table; j.table_ctl = drive->ctl;
     const uint64_t fs = 1ull << t.ln_leaf;
     j.s_dst = (uint64_t)ops[0].slot[0] * fs; j.s_src = (uint64_t)ops[0].slot[1] * fs;
     j.s_rhs = (uint64_t)ops[0].slot[2] * fs;
     j.inv = 1.0f / 6.0f;
+    j.red_target = jac_red ? c.scalars + ops[1].scalar : nullptr;
+    j.partials = c.partials;
+    j.red_done = c.red_done;
     // (programmatic dependent launch was measured here: 4.36 vs 4.12 us per
     // launch inside the graph -- slower, so plain launches)
-    k_jacobi8<<<num_sms() * 4, 256, 0, s>>>(j);
+    if (jac_red) k_jacobi8<true><<<num_sms() * 4, 256, 0, s>>>(j);
+    else k_jacobi8<false><<<num_sms() * 4, 256, 0, s>>>(j);
     delete a;
     return check_launch();
   }
@@ -1111,8 +1122,8 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
   // the interpreter runs while it compiles
   if (!ct && !(pair && stencil)) {
     JitGroup G;
-    jit_group_of(t, ops, nops, G);
-    if (const void* k = jit_lookup(G)) {
+    const void* k = jit_group_of(t, ops, nops, G) ? jit_lookup(G) : nullptr;
+    if (k) {
       void* args[] = {(void*)a};
       cudaLaunchKernel(k, dim3(grid), dim3(SF_TPB), args, 0, s);
       delete a;

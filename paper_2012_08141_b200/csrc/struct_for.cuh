@@ -972,6 +972,12 @@ struct JacArgs {
   uint32_t* table_ctl;
   uint64_t s_dst, s_src, s_rhs;   // field offsets (words) from the pool base
   float inv;
+  // RED: the group JACOBI + REDUCE_SUM(s += dst) fused ("fuse the
+  // Jacobi smoothing and reduction kernels"): per-CTA f64 partials, summed in
+  // CTA order by the last CTA (deterministic, as finish_reductions)
+  uint32_t* red_target;
+  double* partials;
+  uint32_t* red_done;
 };
 
 // out of line: the slow path must not shape the hot loop's register allocation
@@ -983,7 +989,9 @@ __device__ __forceinline__ float4 u2f(uint4 u) {
   return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
 }
 
+template <bool RED>
 __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacArgs A) {
+  double acc = 0.0;
   const uint32_t* P = A.T.seg[A.T.nseg - 1].base;
   const uint32_t* __restrict__ src = P + A.s_src;
   const uint32_t* __restrict__ rhs = P + A.s_rhs;
@@ -1046,8 +1054,10 @@ __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacA
       s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
       s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
       s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
-      *reinterpret_cast<uint4*>(dst + o0) = make_uint4(__float_as_uint((r.x + s0) * inv), __float_as_uint((r.y + s1) * inv),
-                                                       __float_as_uint((r.z + s2) * inv), __float_as_uint((r.w + s3) * inv));
+      const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
+      *reinterpret_cast<uint4*>(dst + o0) = make_uint4(__float_as_uint(out.x), __float_as_uint(out.y),
+                                                       __float_as_uint(out.z), __float_as_uint(out.w));
+      if (RED) acc += (double)(((out.x + out.y) + out.z) + out.w);
     }
     {
       const float lo = zh ? p1 : z1, hi = zh ? z1 : p1;
@@ -1057,8 +1067,43 @@ __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacA
       s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
       s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
       s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
-      *reinterpret_cast<uint4*>(dst + o1) = make_uint4(__float_as_uint((r.x + s0) * inv), __float_as_uint((r.y + s1) * inv),
-                                                       __float_as_uint((r.z + s2) * inv), __float_as_uint((r.w + s3) * inv));
+      const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
+      *reinterpret_cast<uint4*>(dst + o1) = make_uint4(__float_as_uint(out.x), __float_as_uint(out.y),
+                                                       __float_as_uint(out.z), __float_as_uint(out.w));
+      if (RED) acc += (double)(((out.x + out.y) + out.z) + out.w);
+    }
+  }
+  if (RED) {
+    __shared__ double s_acc;
+    __shared__ bool s_last;
+    __shared__ double s_sum[256];
+    if (threadIdx.x == 0) s_acc = 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc != 0.0) atomicAdd(&s_acc, acc);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      A.partials[blockIdx.x] = s_acc;
+      __threadfence();
+      s_last = atomicAdd(A.red_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      double t = 0.0;   // fixed-order tree sum over CTAs
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) t += __ldcg(&A.partials[b]);
+      s_sum[threadIdx.x] = t;
+      __syncthreads();
+      for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        const float old = __uint_as_float(*A.red_target);
+        *A.red_target = __float_as_uint((float)((double)old + s_sum[0]));
+        *A.red_done = 0u;
+      }
     }
   }
   // the rows built here (no table yet) become the list's block table

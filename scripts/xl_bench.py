@@ -62,7 +62,7 @@ def jac_xl(iters=10, radius=288.0):
             "frac": ach / peak, "launches": n}
 
 
-def sf_xl(iters=10, radius=288.0, jit=False):
+def sf_xl(iters=10, radius=288.0, jit=False, interpreter=False, group="jacobi_reduce"):
     """SF-XL: the generic fused megakernel (k_struct_for op table) at JAC-XL
     size: JACOBI fused with the residual-style reduction s += x1 (PAPER.md:440
     "fuse the Jacobi smoothing and reduction kernels"), one launch per
@@ -70,6 +70,8 @@ def sf_xl(iters=10, radius=288.0, jit=False):
     the reduction reads x1 from the thread's registers)."""
     if not jit:
         sg.jit_set_mode(0)
+    if (interpreter or jit) and group == "jacobi_reduce":   # not the dedicated k_jacobi8<RED>
+        os.environ["SG_NO_JAC8"] = "1"
     L, lv = W.c2_layout(ptr=32)
     f = L.fields
     coords = W.block_ball_coords(128, 8, radius)
@@ -83,15 +85,22 @@ def sf_xl(iters=10, radius=288.0, jit=False):
     src, dst = f["x0"], f["x1"]
 
     def solve(k):
+        # s accumulates every sweep's sum (no clear in between: each reduction
+        # is read by the next one, so DSE keeps all of them and every sweep is
+        # one fused JACOBI+REDUCE_SUM launch)
         nonlocal src, dst
         flush_buf.zero_()
+        g.serial("CLEAR_SCALAR", [f["s"]])
         for _ in range(k):
-            g.serial("CLEAR_SCALAR", [f["s"]])
-            g.struct_for("JACOBI", lv[-1], [dst, src, f["b"]])
-            g.struct_for("REDUCE_SUM", lv[-1], [f["s"], dst])
+            if group == "jacobi_reduce":
+                g.struct_for("JACOBI", lv[-1], [dst, src, f["b"]])
+                g.struct_for("REDUCE_SUM", lv[-1], [f["s"], dst])
+            else:   # MGPCG's A p and p.Ap (no dedicated kernel: interpreter or JIT)
+                g.struct_for("STENCIL", lv[-1], [dst, src])
+                g.struct_for("DOT", lv[-1], [f["s"], src, dst], [-1.0])
             src, dst = dst, src
         st = g.flush("all")
-        return sg.profile_read(g).get(100 + sg.OPS["JACOBI"], (0.0, 0)), st
+        return sg.profile_read(g).get(100 + sg.OPS["JACOBI" if group == "jacobi_reduce" else "STENCIL"], (0.0, 0)), st
 
     solve(2)
     solve(1)
@@ -102,11 +111,18 @@ def sf_xl(iters=10, radius=288.0, jit=False):
     (tk, nk), st = solve(iters + 1)
     if not jit:
         sg.jit_set_mode(-1)
+    os.environ.pop("SG_NO_JAC8", None)
     ms, n = tk - t1, iters
-    nbytes = len(coords) * 512 * 12
+    # 12 B per cell (x0, b read, x1 written) for JACOBI+REDUCE; 8 B (p read,
+    # Ap written; the dot reads both from registers) for STENCIL+DOT
+    nbytes = len(coords) * 512 * (12 if group == "jacobi_reduce" else 8)
     peak, kind = bench.hbm_peak()
     ach = nbytes / (ms / n / 1e3) / 1e9
-    return {"variant": "SF-XL", "kernel": "k_struct_for (JACOBI+REDUCE_SUM fused)", "blocks": len(coords),
+    assert st["tasks_fused"] == iters + 1, st
+    gname = "JACOBI+REDUCE_SUM" if group == "jacobi_reduce" else "STENCIL+DOT"
+    kern = ("NVRTC-specialized k_struct_for" if jit else "k_struct_for interpreter" if interpreter or
+            group != "jacobi_reduce" else "k_jacobi8<RED> (dedicated)") + f" running the fused {gname} group"
+    return {"variant": "SF-XL", "kernel": kern, "blocks": len(coords),
             "cells": len(coords) * 512, "bytes_per_launch": nbytes, "avg_launch_us": ms / n * 1e3,
             "achieved_GBps": ach, "peak_GBps": peak, "peak_source": kind, "frac": ach / peak, "launches": n,
             "tasks_fused": st["tasks_fused"]}
@@ -121,7 +137,6 @@ def sf_xl_jit(**kw):
     finally:
         sg.jit_set_mode(-1)
     r["variant"] = "SF-XL (JIT-specialized)"
-    r["kernel"] = "NVRTC-specialized JACOBI+REDUCE_SUM (jit.cpp)"
     r["jit"] = sg.jit_info()
     return r
 
@@ -240,3 +255,8 @@ if __name__ == "__main__":
         print(json.dumps(sf_xl()), flush=True)
     if "sfjit" in which:
         print(json.dumps(sf_xl_jit()), flush=True)
+    if "sfint" in which:
+        print(json.dumps(sf_xl(interpreter=True)), flush=True)
+    if "cg" in which:
+        print(json.dumps(sf_xl(group="axpy_dot")), flush=True)
+        print(json.dumps(sf_xl_jit(group="axpy_dot")), flush=True)
