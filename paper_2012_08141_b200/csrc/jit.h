@@ -12,6 +12,7 @@ struct JitGroup {
   int nd = 0;     // quad-path dimensionality (0: generic cell path)
   int gl = 0;     // constant block geometry (0: runtime)
   int i32 = 0;    // value type int (else float)
+  int stream = 0; // 8^3 streaming structure (stream8_body) instead of the tile loop
   DOp ops[SG_MAXOPS];
 };
 

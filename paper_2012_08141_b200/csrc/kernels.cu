@@ -1006,6 +1006,19 @@ static void sf_dispatch(SFArgs* a, int grid, cudaStream_t s, const ChainTab* cha
   k_struct_chain<V, ND, PAIR, GL><<<1, SF_TPB, 0, s>>>(*a, *chain);
 }
 
+// A group of f32 quad ops on 8^3 dense blocks (k_stream8 / stream8_body).
+static bool stream8_group(const DTree& t, const DOp* ops, int nops, int gl, bool i32) {
+  if (gl != 1 || i32 || t.leaf_bitmasked) return false;
+  for (int o = 0; o < nops; o++) {
+    const int op = ops[o].op;
+    if (!(op == SG_OP_FILL || op == SG_OP_ADD_CONST || op == SG_OP_INC || op == SG_OP_AXPY || op == SG_OP_STENCIL ||
+          op == SG_OP_JACOBI || op == SG_OP_REDUCE_SUM || op == SG_OP_DOT || op == SG_OP_AXPY_RATIO ||
+          op == SG_OP_XPAY_RATIO))
+      return false;
+  }
+  return true;
+}
+
 // The JIT content of a struct-for group (same geometry decisions as
 // launch_struct_for); false when the group runs a dedicated kernel instead.
 bool jit_group_of(const DTree& t, const DOp* ops, int nops, JitGroup& G) {
@@ -1027,6 +1040,7 @@ bool jit_group_of(const DTree& t, const DOp* ops, int nops, JitGroup& G) {
   if ((nops == 1 || jac_red) && ops[0].op == SG_OP_JACOBI && gl == 1 && !i32 && !t.leaf_bitmasked)
     return false;   // k_jacobi8
   G.nops = nops; G.nd = nd; G.gl = gl; G.i32 = i32 ? 1 : 0;
+  G.stream = stream8_group(t, ops, nops, gl, i32) && getenv("SG_NO_STREAM8") == nullptr ? 1 : 0;
   for (int o = 0; o < nops; o++) G.ops[o] = ops[o];
   return true;
 }
@@ -1118,6 +1132,10 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
     delete a;
     return check_launch();
   }
+  // groups of quad ops on 8^3 dense blocks: the streaming kernel (k_jacobi8's
+  // structure, no shared-memory tiles) instead of the tile interpreter
+  const bool stream8 = stream8_group(t, ops, nops, gl, i32) && drive && drive->table && !ct &&
+                       getenv("SG_NO_STREAM8") == nullptr;
   // JIT-specialized kernel of this group's content (jit.cpp);
   // the interpreter runs while it compiles
   if (!ct && !(pair && stencil)) {
@@ -1125,10 +1143,15 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
     const void* k = jit_group_of(t, ops, nops, G) ? jit_lookup(G) : nullptr;
     if (k) {
       void* args[] = {(void*)a};
-      cudaLaunchKernel(k, dim3(grid), dim3(SF_TPB), args, 0, s);
+      cudaLaunchKernel(k, dim3(G.stream ? num_sms() * 4 : grid), dim3(SF_TPB), args, 0, s);
       delete a;
       return check_launch();
     }
+  }
+  if (stream8) {
+    k_stream8<<<num_sms() * 4, 256, 0, s>>>(*a);
+    delete a;
+    return check_launch();
   }
 #define SG_SF_LAUNCH(V)                                                                           \
   switch (nd * 10 + gl) {                                                                         \

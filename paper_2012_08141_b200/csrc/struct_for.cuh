@@ -1119,3 +1119,197 @@ __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacA
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// Streaming kernel for fused groups of quad ops on 8^3 dense blocks (the
+// k_jacobi8 structure for any group of FILL / ADD_CONST / INC / AXPY /
+// STENCIL / JACOBI / REDUCE_SUM / DOT / AXPY_RATIO / XPAY_RATIO): one warp per
+// half block, a lane owns two quads, block rows by shuffles from the table,
+// no shared-memory tiles and no CTA barriers in the loop.  Ops run in group
+// order on the lane's quads; an identity operand written by an earlier op of
+// the group is re-read by the same thread (L1).  Reductions go through the
+// interpreter's warp_add / finish_reductions (deterministic per-CTA f64
+// partials).  Same arithmetic order as the quad path.  Used by the launcher
+// (OpsRT) and by the JIT-specialized kernels (OpsJit).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool stream8_op(int op) {
+  return op == SG_OP_FILL || op == SG_OP_ADD_CONST || op == SG_OP_INC || op == SG_OP_AXPY || op == SG_OP_STENCIL ||
+         op == SG_OP_JACOBI || op == SG_OP_REDUCE_SUM || op == SG_OP_DOT || op == SG_OP_AXPY_RATIO ||
+         op == SG_OP_XPAY_RATIO;
+}
+
+__device__ __forceinline__ void st4f(uint32_t* p, float a, float b, float c, float d) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d));
+}
+
+// Neighbour sums of the lane's two quads of field `src` (k_jacobi8's loads and
+// order): s[q][k] = sum of the 6 face neighbours of cell k of quad q.
+__device__ __forceinline__ void stream8_nbr(const uint32_t* __restrict__ src, uint32_t o0, uint32_t o1, uint32_t j0,
+                                            uint32_t j1, int x0, int y, int zh, const uint32_t nb[6], float4& c0,
+                                            float4& c1, float s[2][4]) {
+  const uint4 c0u = *reinterpret_cast<const uint4*>(src + o0);
+  const uint4 c1u = *reinterpret_cast<const uint4*>(src + o1);
+  const uint32_t nz = zh ? nb[5] : nb[4];
+  const uint32_t zo = zh ? 0u : 7u;
+  const float z0 = __uint_as_float(ld1_if(src + nz + (j0 & ~7u) + zo, nz != SG_NO_BLOCK));
+  const float z1 = __uint_as_float(ld1_if(src + nz + (j1 & ~7u) + zo, nz != SG_NO_BLOCK));
+  const uint4 xmu = ld4_if(src + (x0 > 0 ? o0 - 64u : nb[0] + j0 + 448u), x0 > 0 || nb[0] != SG_NO_BLOCK);
+  const uint4 xpu = ld4_if(src + (x0 + 1 < 7 ? o1 + 64u : nb[1] + j1 - 448u), x0 + 1 < 7 || nb[1] != SG_NO_BLOCK);
+  const bool ym_in = y > 0, yp_in = y < 7;
+  const uint32_t ym0 = ym_in ? o0 - 8u : nb[2] + j0 + 56u, yp0 = yp_in ? o0 + 8u : nb[3] + j0 - 56u;
+  const uint4 ym0u = ld4_if(src + ym0, ym_in || nb[2] != SG_NO_BLOCK);
+  const uint4 yp0u = ld4_if(src + yp0, yp_in || nb[3] != SG_NO_BLOCK);
+  const uint4 ym1u = ld4_if(src + ym0 + 64u, ym_in || nb[2] != SG_NO_BLOCK);
+  const uint4 yp1u = ld4_if(src + yp0 + 64u, yp_in || nb[3] != SG_NO_BLOCK);
+  c0 = u2f(c0u);
+  c1 = u2f(c1u);
+  const float p0 = __shfl_xor_sync(0xffffffffu, zh ? c0.x : c0.w, 1);
+  const float p1 = __shfl_xor_sync(0xffffffffu, zh ? c1.x : c1.w, 1);
+  {
+    const float lo = zh ? p0 : z0, hi = zh ? z0 : p0;
+    const float4 xm = u2f(xmu), xp = c1, ym = u2f(ym0u), yp = u2f(yp0u);
+    s[0][0] = lo + c0.y; s[0][1] = c0.x + c0.z; s[0][2] = c0.y + c0.w; s[0][3] = c0.z + hi;
+    s[0][0] += xm.x; s[0][1] += xm.y; s[0][2] += xm.z; s[0][3] += xm.w;
+    s[0][0] += xp.x; s[0][1] += xp.y; s[0][2] += xp.z; s[0][3] += xp.w;
+    s[0][0] += ym.x; s[0][1] += ym.y; s[0][2] += ym.z; s[0][3] += ym.w;
+    s[0][0] += yp.x; s[0][1] += yp.y; s[0][2] += yp.z; s[0][3] += yp.w;
+  }
+  {
+    const float lo = zh ? p1 : z1, hi = zh ? z1 : p1;
+    const float4 xm = c0, xp = u2f(xpu), ym = u2f(ym1u), yp = u2f(yp1u);
+    s[1][0] = lo + c1.y; s[1][1] = c1.x + c1.z; s[1][2] = c1.y + c1.w; s[1][3] = c1.z + hi;
+    s[1][0] += xm.x; s[1][1] += xm.y; s[1][2] += xm.z; s[1][3] += xm.w;
+    s[1][0] += xp.x; s[1][1] += xp.y; s[1][2] += xp.z; s[1][3] += xp.w;
+    s[1][0] += ym.x; s[1][1] += ym.y; s[1][2] += ym.z; s[1][3] += ym.w;
+    s[1][0] += yp.x; s[1][1] += yp.y; s[1][2] += yp.z; s[1][3] += yp.w;
+  }
+}
+
+template <class OPS>
+__device__ __forceinline__ void stream8_body(const SFArgs& A, const OPS& ops) {
+  uint32_t* P = A.T.seg[A.T.nseg - 1].base;
+  const uint64_t fs = 1ull << A.T.ln_leaf;
+  const uint32_t nent = *A.count;
+  const bool rows_ok = A.table_ctl[4] != 0u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), GW = gridDim.x * (blockDim.x >> 5);
+  const int xp2 = (lane >> 4) * 2, y = (lane >> 1) & 7, zh = lane & 1;
+  const int nops = ops.size();
+  for (uint32_t wq = gw; wq < nent * 2u; wq += GW) {
+    const uint32_t e = wq >> 1, part = wq & 1u;
+    uint32_t blk, nb[6];
+    if (rows_ok) {
+      const uint32_t rv = lane < 12 ? reinterpret_cast<const uint32_t*>(A.table + e)[lane] : 0u;
+      blk = __shfl_sync(0xffffffffu, rv, 0);
+#pragma unroll
+      for (int d = 0; d < 6; d++) nb[d] = __shfl_sync(0xffffffffu, rv, 6 + d);
+    } else {
+      BlockRow r;
+      make_block_row(A.T, A.entries[e], &r);
+      if (part == 0 && lane == 0) A.table[e] = r;
+      blk = r.blk;
+#pragma unroll
+      for (int d = 0; d < 6; d++) nb[d] = r.nbr[d];
+    }
+    if (blk == SG_NO_BLOCK) continue;
+    const int x0 = (int)part * 4 + xp2;
+    const uint32_t j0 = ((uint32_t)x0 << 6) | ((uint32_t)y << 3) | ((uint32_t)zh << 2), j1 = j0 + 64u;
+    const uint32_t o0 = blk + j0, o1 = o0 + 64u;
+#pragma unroll(OPS::kUnroll)
+    for (int o = 0; o < nops; o++) {
+      decltype(auto) op = ops[o];
+      uint32_t* f0 = P + (uint64_t)(op.slot[0] < 0 ? 0 : op.slot[0]) * fs;
+      const uint32_t* f1 = P + (uint64_t)(op.slot[1] < 0 ? 0 : op.slot[1]) * fs;
+      const uint32_t* f2 = P + (uint64_t)(op.slot[2] < 0 ? 0 : op.slot[2]) * fs;
+      const float p0 = op.p[0];
+      switch (op.op) {
+        case SG_OP_FILL:
+          st4f(f0 + o0, p0, p0, p0, p0);
+          st4f(f0 + o1, p0, p0, p0, p0);
+          break;
+        case SG_OP_ADD_CONST:
+        case SG_OP_INC: {
+          const uint32_t* src = op.op == SG_OP_INC ? f0 : f1;
+          const float4 a = u2f(*reinterpret_cast<const uint4*>(src + o0)), b = u2f(*reinterpret_cast<const uint4*>(src + o1));
+          st4f(f0 + o0, a.x + p0, a.y + p0, a.z + p0, a.w + p0);
+          st4f(f0 + o1, b.x + p0, b.y + p0, b.z + p0, b.w + p0);
+        } break;
+        case SG_OP_AXPY: {
+          const float4 a0 = u2f(*reinterpret_cast<const uint4*>(f1 + o0)), a1 = u2f(*reinterpret_cast<const uint4*>(f1 + o1));
+          const float4 b0 = u2f(*reinterpret_cast<const uint4*>(f2 + o0)), b1 = u2f(*reinterpret_cast<const uint4*>(f2 + o1));
+          st4f(f0 + o0, p0 * a0.x + b0.x, p0 * a0.y + b0.y, p0 * a0.z + b0.z, p0 * a0.w + b0.w);
+          st4f(f0 + o1, p0 * a1.x + b1.x, p0 * a1.y + b1.y, p0 * a1.z + b1.z, p0 * a1.w + b1.w);
+        } break;
+        case SG_OP_STENCIL:
+        case SG_OP_JACOBI: {
+          float4 c0, c1;
+          float s[2][4];
+          const bool jac = op.op == SG_OP_JACOBI;
+          float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+          if (jac) {
+            r0 = u2f(*reinterpret_cast<const uint4*>(f2 + o0));
+            r1 = u2f(*reinterpret_cast<const uint4*>(f2 + o1));
+          }
+          stream8_nbr(f1, o0, o1, j0, j1, x0, y, zh, nb, c0, c1, s);
+          const float inv = 1.0f / 6.0f;
+          if (jac) {
+            st4f(f0 + o0, (r0.x + s[0][0]) * inv, (r0.y + s[0][1]) * inv, (r0.z + s[0][2]) * inv, (r0.w + s[0][3]) * inv);
+            st4f(f0 + o1, (r1.x + s[1][0]) * inv, (r1.y + s[1][1]) * inv, (r1.z + s[1][2]) * inv, (r1.w + s[1][3]) * inv);
+          } else {
+            st4f(f0 + o0, s[0][0] - 6.0f * c0.x, s[0][1] - 6.0f * c0.y, s[0][2] - 6.0f * c0.z, s[0][3] - 6.0f * c0.w);
+            st4f(f0 + o1, s[1][0] - 6.0f * c1.x, s[1][1] - 6.0f * c1.y, s[1][2] - 6.0f * c1.z, s[1][3] - 6.0f * c1.w);
+          }
+        } break;
+        case SG_OP_REDUCE_SUM: {
+          const float4 a = u2f(*reinterpret_cast<const uint4*>(f1 + o0)), b = u2f(*reinterpret_cast<const uint4*>(f1 + o1));
+          float acc = 0.0f;
+          acc += a.x; acc += a.y; acc += a.z; acc += a.w;
+          acc += b.x; acc += b.y; acc += b.z; acc += b.w;
+          warp_add<float>(o, acc);
+        } break;
+        case SG_OP_DOT: {
+          const float4 a0 = u2f(*reinterpret_cast<const uint4*>(f1 + o0)), a1 = u2f(*reinterpret_cast<const uint4*>(f1 + o1));
+          const float4 b0 = u2f(*reinterpret_cast<const uint4*>(f2 + o0)), b1 = u2f(*reinterpret_cast<const uint4*>(f2 + o1));
+          float acc = 0.0f;
+          acc += p0 * a0.x * b0.x; acc += p0 * a0.y * b0.y; acc += p0 * a0.z * b0.z; acc += p0 * a0.w * b0.w;
+          acc += p0 * a1.x * b1.x; acc += p0 * a1.y * b1.y; acc += p0 * a1.z * b1.z; acc += p0 * a1.w * b1.w;
+          warp_add<float>(o, acc);
+        } break;
+        case SG_OP_AXPY_RATIO:
+        case SG_OP_XPAY_RATIO: {
+          const float ratio = scalar_of<float>(A, op.f[2]) / scalar_of<float>(A, op.f[3]);
+          const bool ax = op.op == SG_OP_AXPY_RATIO;
+          const float4 a0 = u2f(*reinterpret_cast<const uint4*>(f1 + o0)), a1 = u2f(*reinterpret_cast<const uint4*>(f1 + o1));
+          const float4 d0 = u2f(*reinterpret_cast<const uint4*>(f0 + o0)), d1 = u2f(*reinterpret_cast<const uint4*>(f0 + o1));
+          if (ax) {
+            st4f(f0 + o0, d0.x + p0 * ratio * a0.x, d0.y + p0 * ratio * a0.y, d0.z + p0 * ratio * a0.z, d0.w + p0 * ratio * a0.w);
+            st4f(f0 + o1, d1.x + p0 * ratio * a1.x, d1.y + p0 * ratio * a1.y, d1.z + p0 * ratio * a1.z, d1.w + p0 * ratio * a1.w);
+          } else {
+            st4f(f0 + o0, a0.x + ratio * d0.x, a0.y + ratio * d0.y, a0.z + ratio * d0.z, a0.w + ratio * d0.w);
+            st4f(f0 + o1, a1.x + ratio * d1.x, a1.y + ratio * d1.y, a1.z + ratio * d1.z, a1.w + ratio * d1.w);
+          }
+        } break;
+        default: break;
+      }
+    }
+  }
+  if (!rows_ok) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&A.table_ctl[3], 1u) == gridDim.x - 1) {
+        A.table_ctl[3] = 0u;
+        __threadfence();
+        A.table_ctl[4] = 1u;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) k_stream8(const __grid_constant__ SFArgs A) {
+  if (A.has_reduce && threadIdx.x < SG_MAXOPS) s_red[threadIdx.x] = 0.0;
+  __syncthreads();
+  const OpsRT ops{A.ops, A.nops};
+  stream8_body(A, ops);
+  if (A.has_reduce) finish_reductions<float>(A, ops);
+}
