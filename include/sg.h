@@ -347,9 +347,9 @@ sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
  * block geometry, value type); worker threads compile a kernel whose op table
  * is a compile-time constant with NVRTC for sm_100a and cache it by the hash;
  * launches of that content use it once ready (the op-table interpreter runs
- * meanwhile; CUDA graphs are recaptured).  Env SG_JIT: 0 off (default: the
- * specialized kernels measured no faster than the interpreter), 1
- * asynchronous, 2 synchronous (first launch waits: tests and benchmarks).
+ * meanwhile; CUDA graphs are recaptured).  Env SG_JIT: 0 off, 1
+ * asynchronous (default), 2 synchronous (first launch waits: tests and
+ * benchmarks).
  * out (n <= 7 int64): [mode, kernels ready, compiling, failed, hits, misses,
  * total compile time in microseconds]. */
 sg_status sg_jit_info(int64_t* out, int32_t n);

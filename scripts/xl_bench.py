@@ -68,6 +68,7 @@ def sf_xl(iters=10, radius=288.0, jit=False, interpreter=False, group="jacobi_re
     "fuse the Jacobi smoothing and reduction kernels"), one launch per
     iteration.  Algorithmic bytes: 12 B per active cell (read x0, b; write x1;
     the reduction reads x1 from the thread's registers)."""
+    prev = sg.jit_info()["mode"]
     if not jit:
         sg.jit_set_mode(0)
     if (interpreter or jit) and group == "jacobi_reduce":   # not the dedicated k_jacobi8<RED>
@@ -110,7 +111,7 @@ def sf_xl(iters=10, radius=288.0, jit=False, interpreter=False, group="jacobi_re
     (t1, _), _ = solve(1)
     (tk, nk), st = solve(iters + 1)
     if not jit:
-        sg.jit_set_mode(-1)
+        sg.jit_set_mode(prev)
     os.environ.pop("SG_NO_JAC8", None)
     ms, n = tk - t1, iters
     # 12 B per cell (x0, b read, x1 written) for JACOBI+REDUCE; 8 B (p read,
@@ -131,11 +132,12 @@ def sf_xl(iters=10, radius=288.0, jit=False, interpreter=False, group="jacobi_re
 def sf_xl_jit(**kw):
     """SF-XL with the group's NVRTC-specialized kernel (JIT
     synchronous, so every timed launch runs it) beside the interpreter's."""
+    prev = sg.jit_info()["mode"]
     sg.jit_set_mode(2)
     try:
         r = sf_xl(jit=True, **kw)
     finally:
-        sg.jit_set_mode(-1)
+        sg.jit_set_mode(prev)
     r["variant"] = "SF-XL (JIT-specialized)"
     r["jit"] = sg.jit_info()
     return r
