@@ -121,8 +121,9 @@ def sf_xl(iters=10, radius=288.0, jit=False, interpreter=False, group="jacobi_re
     ach = nbytes / (ms / n / 1e3) / 1e9
     assert st["tasks_fused"] == iters + 1, st
     gname = "JACOBI+REDUCE_SUM" if group == "jacobi_reduce" else "STENCIL+DOT"
-    kern = ("NVRTC-specialized k_struct_for" if jit else "k_struct_for interpreter" if interpreter or
-            group != "jacobi_reduce" else "k_jacobi8<RED> (dedicated)") + f" running the fused {gname} group"
+    kern = ("NVRTC-specialized streaming kernel (stream8_body, constant op table)" if jit
+            else "k_stream8 (streaming kernel, runtime op table)" if interpreter or group != "jacobi_reduce"
+            else "k_jacobi8<RED> (dedicated)") + f" running the fused {gname} group"
     return {"variant": "SF-XL", "kernel": kern, "blocks": len(coords),
             "cells": len(coords) * 512, "bytes_per_launch": nbytes, "avg_launch_us": ms / n * 1e3,
             "achieved_GBps": ach, "peak_GBps": peak, "peak_source": kind, "frac": ach / peak, "launches": n,
