@@ -793,9 +793,45 @@ def run_c5(args, rank, world, local):
         sim = c5_sim(args, rank, world, local)
     ms, launches, clocks, st = time_c5(sim, args, local, world)
     me = sim.ranks[rank]
-    return {"ms_per_step": ms, "launches": launches, "clocks": clocks, "n_local": me.n(),
+    # roofline of the dominant kernel (P2G, FP32 / shared-memory bound): per-launch
+    # device time from the library's events over two more steps
+    from paper_2012_08141_b200 import sg
+    sg.set_profiling(me.grid, True)
+    sg.profile_read(me.grid)
+    for _ in range(2):
+        sim.step(fused=True)
+    prof = sg.profile_read(me.grid)
+    sg.set_profiling(me.grid, False)
+    t, c = prof.get(300 + sg.OPS["P2G"], (0.0, 0))
+    p2g_us = t / max(c, 1) * 1e3
+    n_loc = me.n()
+    fpk = fp32_peak_tflops()
+    tflops = MPM_FLOPS["P2G"] * n_loc / (p2g_us / 1e6) / 1e12 if p2g_us > 0 else 0.0
+    step_ms_prof = sum(v[0] for k, v in prof.items() if k < 100) / 2
+    roof = {"bound": "alu", "kernel": "k_p2g_bin (P2G, rank 0)", "achieved": tflops, "peak": fpk,
+            "unit": "TFLOP/s", "frac": tflops / fpk, "traffic": None,
+            "peak_source": "FP32 FMA peak: SMs x 128 x 2 x 1965 MHz (DESIGN.md s6)",
+            "avg_launch_us": p2g_us, "flops_per_particle": MPM_FLOPS["P2G"], "particles": n_loc,
+            "hbm_GBps": MPM_BYTES["P2G"] * n_loc / (p2g_us / 1e6) / 1e9 if p2g_us > 0 else 0.0,
+            "share_of_step": (p2g_us / 1e3) / step_ms_prof if step_ms_prof > 0 else None}
+    # e2e through the public API: every step host-synchronous with a 4-byte D2H
+    # of the rank's particle count (the state stays resident: no per-step input)
+    import time as _time
+    import torch
+    torch.cuda.synchronize()
+    t0 = _time.perf_counter()
+    for _ in range(args.steps):
+        sim.step(fused=True)
+        _ = int(me.count[0].item())
+    e2e_s = _time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    return {"ms_per_step": ms, "launches": launches, "clocks": clocks, "n_local": n_loc,
             "launches_per_step_rank0": sum(s["launches"] for s in st), "transport": me.transport,
-            "single_gpu": single}
+            "single_gpu": single, "roofline": roof, "e2e": args.steps / e2e_s}
 
 
 def c5_config(args, world):
@@ -865,6 +901,10 @@ def main():
                    "gpu_launches": r["launches"], "launches_per_step_rank0": r["launches_per_step_rank0"],
                    "transport": r["transport"],
                    "single_gpu_same_run": r["single_gpu"],
+                   "roofline": r["roofline"],
+                   "e2e": {"value": r["e2e"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4,
+                           "method": "SlabMPM.step (public API) + a 4-byte D2H of the particle count every step, "
+                                     "host-synchronous; the particle state is resident by design"},
                    "clocks": r["clocks"]}
             print(json.dumps(out))
         if world > 1:
