@@ -355,6 +355,12 @@ sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
 sg_status sg_jit_info(int64_t* out, int32_t n);
 /* Process-wide JIT mode (0, 1, 2 as SG_JIT; -1 = back to the environment). */
 sg_status sg_jit_set_mode(int32_t mode);
+/* Stops the JIT for the rest of the process: queued compilations are dropped,
+ * in-flight ones are waited for (<= 60 s), later launches use the op-table
+ * interpreter.  Call before process exit while compilations may be running:
+ * NVRTC's exit-time teardown under a running compile crashes the process
+ * (the Python binding calls it from an atexit hook).  Always SG_OK. */
+sg_status sg_jit_shutdown(void);
 /* Host-side check (no GPU needed): NVRTC-compiles, without loading, the
  * specialized kernel of a group of `nops` op codes with placeholder operands
  * (nd / gl: quad-path dimensionality and constant block geometry, i32: value

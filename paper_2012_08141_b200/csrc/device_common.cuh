@@ -87,7 +87,7 @@ __device__ __forceinline__ uint32_t* locate_active(const DTree& T, const int c[3
   return cont;
 }
 
-__device__ int32_t pool_pop(const DSeg& S) {
+static __device__ int32_t pool_pop(const DSeg& S) {
   int32_t top = atomicSub(&S.alloc[1], 1);
   if (top > 0) return (int32_t)S.free_list[top - 1];
   atomicAdd(&S.alloc[1], 1);
@@ -98,7 +98,7 @@ __device__ int32_t pool_pop(const DSeg& S) {
 
 // Pointer child acquisition (PAPER.md:166 allocator; SURVEY.md s7 hard part 1):
 // CAS NULL->BUSY, pop the pool, record the origin, publish slot with release.
-__device__ int32_t acquire_child(const DevCtx& C, const DTree& T, const DLevel& L, uint32_t* cont, uint32_t idx,
+static __device__ int32_t acquire_child(const DevCtx& C, const DTree& T, const DLevel& L, uint32_t* cont, uint32_t idx,
                                  const int c[3], int task) {
   uint32_t* sp = cont + L.slot_off + idx;
   uint32_t v = ld_acquire(sp);
@@ -131,7 +131,7 @@ __device__ int32_t acquire_child(const DevCtx& C, const DTree& T, const DLevel& 
 
 // Activating walk: every sparse ancestor of c becomes
 // active; returns the leaf container + index.  Idempotent; never touches payload.
-__device__ uint32_t* activate_walk(const DevCtx& C, const DTree& T, const int c[3], uint32_t& idx, int task) {
+static __device__ uint32_t* activate_walk(const DevCtx& C, const DTree& T, const int c[3], uint32_t& idx, int task) {
   uint32_t* cont = T.seg[0].base;
   idx = 0;
   for (int l = 0; l < T.nlev; l++) {
@@ -152,7 +152,7 @@ __device__ uint32_t* activate_walk(const DevCtx& C, const DTree& T, const int c[
 }
 
 // Level-global coordinates of the level-l cell (container slot cs, index idx).
-__device__ void cell_coords(const DTree& T, int l, uint32_t cs, uint32_t idx, int g[3]) {
+static __device__ void cell_coords(const DTree& T, int l, uint32_t cs, uint32_t idx, int g[3]) {
   const DLevel& L = T.lev[l];
   const DSeg& S = T.seg[L.seg];
   int acc[3] = {0, 0, 0}, sh[3] = {0, 0, 0};

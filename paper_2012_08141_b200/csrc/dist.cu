@@ -25,6 +25,8 @@
 // safe); flags only grow.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <execinfo.h>
+#include <signal.h>
 #include <unistd.h>
 
 #include <cstdlib>
@@ -471,3 +473,24 @@ void sg_dist_destroy(sg_grid* g) {
   if (D.arena) cudaFree(D.arena);
   D = DistState();
 }
+
+// Diagnostics: SG_SEGV_TRACE=1 installs a SIGSEGV handler at library load that
+// prints the faulting thread's native backtrace to stderr (Python's
+// faulthandler is off by the time C exit handlers run).
+namespace {
+void sg_segv_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "libsg: fatal signal, native backtrace:\n";
+  (void)!write(2, msg, sizeof(msg) - 1);
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct SegvTrace {
+  SegvTrace() {
+    const char* e = std::getenv("SG_SEGV_TRACE");
+    if (e && std::atoi(e)) signal(SIGSEGV, sg_segv_handler);
+  }
+} g_segv_trace;
+}  // namespace

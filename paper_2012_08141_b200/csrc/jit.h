@@ -26,6 +26,7 @@ const void* jit_lookup(const JitGroup& g, bool prefetch = false);
 // Bumped whenever a specialized kernel becomes ready (CUDA-graph signatures).
 int64_t jit_generation();
 void jit_set_mode(int m);   // -1: back to SG_JIT
+void jit_shutdown();        // drop queued compiles, wait for in-flight ones, JIT off for good
 int jit_selftest(int nd, int gl, int i32, const int32_t* ops, int nops, char* log, int64_t cap);
 // [mode, ready, pending, failed, hits, misses, compile_us_total]
 void jit_stats(int64_t* out, int n);

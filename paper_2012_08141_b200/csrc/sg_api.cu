@@ -1155,6 +1155,11 @@ extern "C" sg_status sg_jit_set_mode(int32_t mode) {
   return SG_OK;
 }
 
+extern "C" sg_status sg_jit_shutdown(void) {
+  jit_shutdown();
+  return SG_OK;
+}
+
 extern "C" sg_status sg_jit_selftest(int32_t nd, int32_t gl, int32_t i32, const int32_t* ops, int32_t nops,
                                      char* log, int64_t cap) {
   if (!ops || nops < 1 || nops > SG_MAXOPS) return fail(SG_ERR_ARG, "bad op list");

@@ -7,13 +7,15 @@ at import: there is no CPU fallback.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsg.so")
+# SG_LIB_PATH: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("SG_LIB_PATH") or os.path.join(_HERE, "libsg.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libsg.so not built at {LIB_PATH}: run __graft_entry__.build() (no CPU fallback exists)")
@@ -532,7 +534,19 @@ _lib.sg_jit_selftest.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
 _lib.sg_jit_selftest.restype = ctypes.c_int32
 _lib.sg_jit_set_mode.argtypes = [ctypes.c_int32]
 _lib.sg_jit_set_mode.restype = ctypes.c_int32
-EXPORTS += ["sg_jit_selftest", "sg_jit_set_mode"]
+_lib.sg_jit_shutdown.argtypes = []
+_lib.sg_jit_shutdown.restype = ctypes.c_int32
+EXPORTS += ["sg_jit_selftest", "sg_jit_set_mode", "sg_jit_shutdown"]
+
+
+def jit_shutdown():
+    """Stop the JIT (drop queued compiles, wait for in-flight ones): NVRTC's
+    exit-time teardown under a running compile crashes the process."""
+    _check(_lib.sg_jit_shutdown())
+
+
+# Python atexit hooks run before any C exit handler (include/sg.h)
+atexit.register(jit_shutdown)
 
 
 def jit_set_mode(mode):
