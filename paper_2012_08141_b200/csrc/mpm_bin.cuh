@@ -407,7 +407,10 @@ struct MbP2G {
   uint32_t off[8];
 };
 
-__global__ void __launch_bounds__(MB_TPB, 4) k_p2g_bin(const __grid_constant__ MpmBinArgs A) {
+#ifndef MB_P2G_MINB
+#define MB_P2G_MINB 6   // CTAs per SM the P2G register budget is sized for (4: 122 registers, C3 P2G 158 us; 6: 80, 144 us; 8: 148 us)
+#endif
+__global__ void __launch_bounds__(MB_TPB, MB_P2G_MINB) k_p2g_bin(const __grid_constant__ MpmBinArgs A) {
   __shared__ __align__(16) MbP2G S;
   const DevCtx& C = A.C;
   const DOp& op = A.op;
@@ -518,7 +521,10 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_bin(const __grid_constant__ M
 }
 
 // G2P, binned: the chunk's 6^3 x 3 velocity tile is staged in shared memory.
-__global__ void __launch_bounds__(MB_TPB, 6) k_g2p_bin(const __grid_constant__ MpmBinArgs A) {
+#ifndef MB_G2P_MINB
+#define MB_G2P_MINB 6
+#endif
+__global__ void __launch_bounds__(MB_TPB, MB_G2P_MINB) k_g2p_bin(const __grid_constant__ MpmBinArgs A) {
   __shared__ float s_u[3][MB_NODES];
   __shared__ uint32_t s_off[8];
   const DevCtx& C = A.C;
