@@ -462,7 +462,8 @@ def measure_c2_variants(args, device, steps=10, warmup=3):
 
 def measure_c2_chain(steps=20, warmup=5):
     """Beyond the paper (SG_PASS_CHAIN): the same C2 solve with the
-    dependent Jacobi sweeps chained in one cooperative launch."""
+    dependent Jacobi sweeps chained in one cooperative launch with
+    per-half-block completion flags (kernels_flow.cu; SG_FLOW=1, set by main)."""
     import torch
     from paper_2012_08141_b200 import sg
     L, lv, coords, calls, result = c2_setup(50)
@@ -487,7 +488,8 @@ def measure_c2_chain(steps=20, warmup=5):
     ms /= steps
     return {"solves_per_s": 1000.0 / ms, "ms_per_step": ms, "launches_per_step": st["launches"],
             "tasks_chained": st["tasks_chained"], "result_s": float(g.field(L.fields["s"])),
-            "note": "beyond the paper: dependent stencils chained with grid-wide barriers"}
+            "note": "beyond the paper (negative result): the 50 dependent sweeps as ONE persistent launch, "
+                    "point-to-point completion flags per half block instead of launch boundaries"}
 
 
 def measure_c1(steps=200, warmup=10):
@@ -842,6 +844,9 @@ def c5_config(args, world):
 
 
 def main():
+    # chained C2 sweeps run the flag-chained kernel (opt-in in the library; only
+    # the c2_chain extra uses the chain pass on 8^3 blocks)
+    os.environ.setdefault("SG_FLOW", "1")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -79,6 +79,10 @@ struct sg_grid {
   uint32_t* mig_holes = nullptr;    // MIGRATE_COMPACT hole list ([0] count) + tail marks
   uint32_t* mig_tail = nullptr;
   uint64_t mig_hole_cap = 0;
+  // flag-chained JACOBI sweeps (kernels_flow.cu): per tree one completion flag
+  // per half block of the leaf pool, one epoch / done counter pair per grid
+  std::vector<uint32_t*> flow_flags;
+  uint32_t* flow_ctl = nullptr;
   // particle bins (binned MPM kernels) + a one-entry cache keyed by the
   // position array, its write epoch, the tree and the range
   DBins bins{};

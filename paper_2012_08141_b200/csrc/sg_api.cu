@@ -488,6 +488,50 @@ static void make_op(const sg_grid* g, const PTask& t, uint32_t act, int loop_tre
 
 constexpr uint64_t CHAIN_SOLO_CELLS = 8192;
 
+// The device op table of a plan group.
+static void group_ops(const sg_grid* g, const std::vector<int>& members, const std::vector<uint32_t>& acts, int tree,
+                      std::vector<DOp>& all) {
+  all.resize(members.size());
+  for (size_t i = 0; i < members.size(); i++) make_op(g, g->eager[members[i]], acts[i], tree, all[i]);
+}
+
+// The first phase of a chain's tail of JACOBI sweeps that runs as one
+// flag-chained launch (the phases before it launch one by one), or -1.
+// Opt-in (SG_FLOW=1): measured SLOWER than one graph-replayed launch per
+// sweep on C2 (1,866 vs 3,974 solves/s: every sweep of a half block pays a
+// flag poll, its loads and a release fence in series, ~10 us per sweep
+// against ~4.4 us per graph-replayed launch) -- a negative result kept with
+// its tests.
+static int chain_flow_start(const sg_grid* g, const PTask& t0, const std::vector<DOp>& all,
+                            const std::vector<int>& phase_end) {
+  static const bool on = getenv("SG_FLOW") && atoi(getenv("SG_FLOW")) != 0;
+  if (!on || phase_end.size() < 2) return -1;
+  const DTree& T = g->dtrees[t0.tree];
+  const DList* drive = T.driving >= 0 ? &g->lists[t0.tree][T.driving] : nullptr;
+  return jacobi_flow_start(T, drive, all.data(), phase_end.data(), (int)phase_end.size());
+}
+
+// Flag buffers of a tree (allocated and zeroed on first use: a plan's first
+// run is never captured, so this happens outside any CUDA-graph capture).
+static bool flow_buffers(sg_grid* g, int tree, uint32_t** flags, uint32_t** ctl) {
+  if ((int)g->flow_flags.size() <= tree) g->flow_flags.resize(tree + 1, nullptr);
+  if (!g->flow_flags[tree]) {
+    const DSeg& S = g->dtrees[tree].seg[g->dtrees[tree].nseg - 1];
+    const size_t n = 2 * (((size_t)S.capacity + 1) * S.stride / 512 + 1);
+    uint32_t* f = (uint32_t*)g->dev_alloc(n * 4);
+    if (!f || cudaMemsetAsync(f, 0, n * 4, g->stream) != cudaSuccess) return false;
+    g->flow_flags[tree] = f;
+  }
+  if (!g->flow_ctl) {
+    uint32_t* c = (uint32_t*)g->dev_alloc(16);
+    if (!c || cudaMemsetAsync(c, 0, 16, g->stream) != cudaSuccess) return false;
+    g->flow_ctl = c;
+  }
+  *flags = g->flow_flags[tree];
+  *ctl = g->flow_ctl;
+  return true;
+}
+
 // A chained group over a list of more than CHAIN_SOLO_CELLS cells launches its
 // phases one by one (see launch_group).
 static bool chain_is_split(const sg_grid* g, const PTask& t0, size_t nops = 0, size_t nphases = 0) {
@@ -602,8 +646,26 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
         // chain (SG_PASS_CHAIN): whole op table + phase ends to the device
         std::vector<DOp> all(nops);
         int nbr = 0;
+        for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], t0.tree, all[i]);
+        uint32_t *ffl = nullptr, *fct = nullptr;
+        const int fs = chain_flow_start(g, t0, all, phase_end);
+        if (fs >= 0 && flow_buffers(g, t0.tree, &ffl, &fct)) {
+          // leading phases (e.g. the fused FILLs of a solve) one launch each,
+          // then the sweeps as one flag-chained launch
+          int begin = 0;
+          for (int ph = 0; ph < fs && !rc; ph++) {
+            rc = launch_struct_for(g->ctx, T, t0.tree, drive, all.data() + begin, phase_end[ph] - begin, task,
+                                   g->stream, grid_hint_struct(g, T), nullptr, nullptr, 1, 0);
+            begin = phase_end[ph];
+            st.launches++;
+          }
+          if (!rc)
+            rc = launch_jacobi_flow(g->ctx, T, drive, all.data(), phase_end.data(), fs, (int)phase_end.size(), ffl,
+                                    fct, task, g->stream);
+          st.launches_chained++;
+          break;
+        }
         for (int i = 0; i < nops; i++) {
-          make_op(g, g->eager[members[i]], acts[i], t0.tree, all[i]);
           int op = all[i].op;
           nbr |= op == SG_OP_STENCIL || op == SG_OP_JACOBI || op == SG_OP_JITTER || op == SG_OP_SMOOTH_RB ||
                  op == SG_OP_RESTRICT || op == SG_OP_RESID_NORM2;
@@ -835,7 +897,11 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         if (t.type == TT_LISTGEN) st.listgen_launched++;
         if (t.type == TT_CLEAR_LIST) st.clear_list_launched++;
         if (plan->phase_ends[gi].size() > 1) {
-          if (chain_is_split(g, t, mem.size(), plan->phase_ends[gi].size()))
+          std::vector<DOp> all;
+          group_ops(g, mem, acts, t.tree, all);
+          const int fs = chain_flow_start(g, t, all, plan->phase_ends[gi]);
+          if (fs >= 0) { st.launches += fs; st.launches_chained++; }
+          else if (chain_is_split(g, t, mem.size(), plan->phase_ends[gi].size()))
             st.launches += (int64_t)plan->phase_ends[gi].size() - 1;
           else st.launches_chained++;
         }

@@ -165,6 +165,15 @@ int launch_clear_list(const DList& l, void* stream);
 int launch_struct_for(const DevCtx& c, const DTree& t, int tree_id, const DList* drive, const DOp* ops, int nops,
                       int task_id, void* stream, int grid_hint, const DOp* chain_ops, const int* chain_phase_end,
                       int nphases, int chain_needs_nbr);
+// The tail of a chain (SG_PASS_CHAIN) whose phases are lone f32 JACOBI sweeps
+// on 8^3 dense blocks (the last may be fused with the reduction of its
+// output) runs as ONE persistent launch with per-half-block completion flags
+// (kernels_flow.cu).  jacobi_flow_start: the first phase of that tail (>= 2
+// phases), or -1.  flags: 2 * (leaf pool words / 512 + 1) zeroed u32; ctl: 3
+// zeroed u32.
+int jacobi_flow_start(const DTree& t, const DList* drive, const DOp* ops, const int* phase_end, int nph);
+int launch_jacobi_flow(const DevCtx& c, const DTree& t, const DList* drive, const DOp* ops, const int* phase_end,
+                       int first, int nph, uint32_t* flags, uint32_t* ctl, int task_id, void* stream);
 struct RangeScratch {
   uint64_t* status;   // look-back descriptors for G2P_MIGRATE tiles
   uint32_t* ctl;      // [0..3] migrate tile/done/epoch/count, [5] append ticket

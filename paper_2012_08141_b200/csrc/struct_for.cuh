@@ -989,6 +989,107 @@ __device__ __forceinline__ float4 u2f(uint4 u) {
   return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
 }
 
+// One warp's half block of a JACOBI sweep on an 8^3 dense block (k_jacobi8
+// and the flag-chained k_jacobi8_flow): a lane owns the quads at
+// x0 = 4*part + 2*(lane/16) and x0 + 1 (same y, z-half), their shared x face
+// loaded once; every load of both quads issued before the arithmetic.
+// Returns the lane's sum of the written values (RED).
+template <bool RED>
+__device__ __forceinline__ double jac8_half(const uint32_t* __restrict__ src, const uint32_t* __restrict__ rhs,
+                                            uint32_t* dst, uint32_t blk, const uint32_t (&nb)[6], uint32_t part,
+                                            int lane, float inv) {
+  double acc = 0.0;
+  const int xp2 = (lane >> 4) * 2, y = (lane >> 1) & 7, zh = lane & 1;
+  const int x0 = (int)part * 4 + xp2;
+  const uint32_t j0 = ((uint32_t)x0 << 6) | ((uint32_t)y << 3) | ((uint32_t)zh << 2), j1 = j0 + 64u;
+  const uint32_t o0 = blk + j0, o1 = o0 + 64u;
+  // every load of both quads issued before the arithmetic
+  const uint4 c0u = *reinterpret_cast<const uint4*>(src + o0);
+  const uint4 c1u = *reinterpret_cast<const uint4*>(src + o1);
+  const uint4 r0u = *reinterpret_cast<const uint4*>(rhs + o0);
+  const uint4 r1u = *reinterpret_cast<const uint4*>(rhs + o1);
+  const uint32_t nz = zh ? nb[5] : nb[4];
+  const uint32_t zo = zh ? 0u : 7u;
+  const float z0 = __uint_as_float(ld1_if(src + nz + (j0 & ~7u) + zo, nz != SG_NO_BLOCK));
+  const float z1 = __uint_as_float(ld1_if(src + nz + (j1 & ~7u) + zo, nz != SG_NO_BLOCK));
+  const uint4 xmu = ld4_if(src + (x0 > 0 ? o0 - 64u : nb[0] + j0 + 448u), x0 > 0 || nb[0] != SG_NO_BLOCK);
+  const uint4 xpu = ld4_if(src + (x0 + 1 < 7 ? o1 + 64u : nb[1] + j1 - 448u), x0 + 1 < 7 || nb[1] != SG_NO_BLOCK);
+  const bool ym_in = y > 0, yp_in = y < 7;
+  const uint32_t ym0 = ym_in ? o0 - 8u : nb[2] + j0 + 56u, yp0 = yp_in ? o0 + 8u : nb[3] + j0 - 56u;
+  const uint4 ym0u = ld4_if(src + ym0, ym_in || nb[2] != SG_NO_BLOCK);
+  const uint4 yp0u = ld4_if(src + yp0, yp_in || nb[3] != SG_NO_BLOCK);
+  const uint4 ym1u = ld4_if(src + ym0 + 64u, ym_in || nb[2] != SG_NO_BLOCK);
+  const uint4 yp1u = ld4_if(src + yp0 + 64u, yp_in || nb[3] != SG_NO_BLOCK);
+  const float4 c0 = u2f(c0u), c1 = u2f(c1u);
+  const float p0 = __shfl_xor_sync(0xffffffffu, zh ? c0.x : c0.w, 1);
+  const float p1 = __shfl_xor_sync(0xffffffffu, zh ? c1.x : c1.w, 1);
+  {
+    const float lo = zh ? p0 : z0, hi = zh ? z0 : p0;
+    const float4 xm = u2f(xmu), xp = c1, ym = u2f(ym0u), yp = u2f(yp0u), r = u2f(r0u);
+    float s0 = lo + c0.y, s1 = c0.x + c0.z, s2 = c0.y + c0.w, s3 = c0.z + hi;
+    s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
+    s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
+    s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
+    s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
+    const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
+    *reinterpret_cast<uint4*>(dst + o0) = make_uint4(__float_as_uint(out.x), __float_as_uint(out.y),
+                                                     __float_as_uint(out.z), __float_as_uint(out.w));
+    if (RED) acc += (double)(((out.x + out.y) + out.z) + out.w);
+  }
+  {
+    const float lo = zh ? p1 : z1, hi = zh ? z1 : p1;
+    const float4 xm = c0, xp = u2f(xpu), ym = u2f(ym1u), yp = u2f(yp1u), r = u2f(r1u);
+    float s0 = lo + c1.y, s1 = c1.x + c1.z, s2 = c1.y + c1.w, s3 = c1.z + hi;
+    s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
+    s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
+    s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
+    s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
+    const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
+    *reinterpret_cast<uint4*>(dst + o1) = make_uint4(__float_as_uint(out.x), __float_as_uint(out.y),
+                                                     __float_as_uint(out.z), __float_as_uint(out.w));
+    if (RED) acc += (double)(((out.x + out.y) + out.z) + out.w);
+  }
+  return acc;
+}
+
+// Deterministic end of a fused JACOBI + REDUCE_SUM (k_jacobi8<true>,
+// k_jacobi8_flow<true>): per-CTA f64 partials summed in CTA order by the last
+// CTA into the 0-D target.
+__device__ __forceinline__ void jac_reduce_tail(const JacArgs& A, double acc) {
+  const int lane = threadIdx.x & 31;
+  __shared__ double s_acc;
+  __shared__ bool s_last;
+  __shared__ double s_sum[256];
+  if (threadIdx.x == 0) s_acc = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0 && acc != 0.0) atomicAdd(&s_acc, acc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    A.partials[blockIdx.x] = s_acc;
+    __threadfence();
+    s_last = atomicAdd(A.red_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    double t = 0.0;   // fixed-order tree sum over CTAs
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) t += __ldcg(&A.partials[b]);
+    s_sum[threadIdx.x] = t;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const float old = __uint_as_float(*A.red_target);
+      *A.red_target = __float_as_uint((float)((double)old + s_sum[0]));
+      *A.red_done = 0u;
+    }
+  }
+}
+
 template <bool RED>
 __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacArgs A) {
   double acc = 0.0;
@@ -1000,9 +1101,7 @@ __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacA
   const bool rows_ok = A.table_ctl[4] != 0u;   // set by an earlier launch
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), GW = gridDim.x * (blockDim.x >> 5);
-  // one warp per half block; a lane owns the quads at x0 = 4*part + 2*(lane/16)
-  // and x0 + 1 (same y, z-half): their shared x face is loaded once
-  const int xp2 = (lane >> 4) * 2, y = (lane >> 1) & 7, zh = lane & 1;
+  // one warp per half block (jac8_half)
   for (uint32_t wq = gw; wq < nent * 2u; wq += GW) {
     const uint32_t e = wq >> 1, part = wq & 1u;
     uint32_t blk, nb[6];
@@ -1022,90 +1121,9 @@ __global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacA
       for (int d = 0; d < 6; d++) nb[d] = r.nbr[d];
     }
     if (blk == SG_NO_BLOCK) continue;
-    const int x0 = (int)part * 4 + xp2;
-    const uint32_t j0 = ((uint32_t)x0 << 6) | ((uint32_t)y << 3) | ((uint32_t)zh << 2), j1 = j0 + 64u;
-    const uint32_t o0 = blk + j0, o1 = o0 + 64u;
-    // every load of both quads issued before the arithmetic
-    const uint4 c0u = *reinterpret_cast<const uint4*>(src + o0);
-    const uint4 c1u = *reinterpret_cast<const uint4*>(src + o1);
-    const uint4 r0u = *reinterpret_cast<const uint4*>(rhs + o0);
-    const uint4 r1u = *reinterpret_cast<const uint4*>(rhs + o1);
-    const uint32_t nz = zh ? nb[5] : nb[4];
-    const uint32_t zo = zh ? 0u : 7u;
-    const float z0 = __uint_as_float(ld1_if(src + nz + (j0 & ~7u) + zo, nz != SG_NO_BLOCK));
-    const float z1 = __uint_as_float(ld1_if(src + nz + (j1 & ~7u) + zo, nz != SG_NO_BLOCK));
-    const uint4 xmu = ld4_if(src + (x0 > 0 ? o0 - 64u : nb[0] + j0 + 448u), x0 > 0 || nb[0] != SG_NO_BLOCK);
-    const uint4 xpu = ld4_if(src + (x0 + 1 < 7 ? o1 + 64u : nb[1] + j1 - 448u), x0 + 1 < 7 || nb[1] != SG_NO_BLOCK);
-    const bool ym_in = y > 0, yp_in = y < 7;
-    const uint32_t ym0 = ym_in ? o0 - 8u : nb[2] + j0 + 56u, yp0 = yp_in ? o0 + 8u : nb[3] + j0 - 56u;
-    const uint4 ym0u = ld4_if(src + ym0, ym_in || nb[2] != SG_NO_BLOCK);
-    const uint4 yp0u = ld4_if(src + yp0, yp_in || nb[3] != SG_NO_BLOCK);
-    const uint4 ym1u = ld4_if(src + ym0 + 64u, ym_in || nb[2] != SG_NO_BLOCK);
-    const uint4 yp1u = ld4_if(src + yp0 + 64u, yp_in || nb[3] != SG_NO_BLOCK);
-    const float4 c0 = u2f(c0u), c1 = u2f(c1u);
-    const float p0 = __shfl_xor_sync(0xffffffffu, zh ? c0.x : c0.w, 1);
-    const float p1 = __shfl_xor_sync(0xffffffffu, zh ? c1.x : c1.w, 1);
-    const float inv = A.inv;
-    {
-      const float lo = zh ? p0 : z0, hi = zh ? z0 : p0;
-      const float4 xm = u2f(xmu), xp = c1, ym = u2f(ym0u), yp = u2f(yp0u), r = u2f(r0u);
-      float s0 = lo + c0.y, s1 = c0.x + c0.z, s2 = c0.y + c0.w, s3 = c0.z + hi;
-      s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
-      s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
-      s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
-      s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
-      const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
-      *reinterpret_cast<uint4*>(dst + o0) = make_uint4(__float_as_uint(out.x), __float_as_uint(out.y),
-                                                       __float_as_uint(out.z), __float_as_uint(out.w));
-      if (RED) acc += (double)(((out.x + out.y) + out.z) + out.w);
-    }
-    {
-      const float lo = zh ? p1 : z1, hi = zh ? z1 : p1;
-      const float4 xm = c0, xp = u2f(xpu), ym = u2f(ym1u), yp = u2f(yp1u), r = u2f(r1u);
-      float s0 = lo + c1.y, s1 = c1.x + c1.z, s2 = c1.y + c1.w, s3 = c1.z + hi;
-      s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
-      s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
-      s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
-      s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
-      const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
-      *reinterpret_cast<uint4*>(dst + o1) = make_uint4(__float_as_uint(out.x), __float_as_uint(out.y),
-                                                       __float_as_uint(out.z), __float_as_uint(out.w));
-      if (RED) acc += (double)(((out.x + out.y) + out.z) + out.w);
-    }
+    acc += jac8_half<RED>(src, rhs, dst, blk, nb, part, lane, A.inv);
   }
-  if (RED) {
-    __shared__ double s_acc;
-    __shared__ bool s_last;
-    __shared__ double s_sum[256];
-    if (threadIdx.x == 0) s_acc = 0.0;
-    __syncthreads();
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0 && acc != 0.0) atomicAdd(&s_acc, acc);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      A.partials[blockIdx.x] = s_acc;
-      __threadfence();
-      s_last = atomicAdd(A.red_done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      double t = 0.0;   // fixed-order tree sum over CTAs
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += 256) t += __ldcg(&A.partials[b]);
-      s_sum[threadIdx.x] = t;
-      __syncthreads();
-      for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) {
-        const float old = __uint_as_float(*A.red_target);
-        *A.red_target = __float_as_uint((float)((double)old + s_sum[0]));
-        *A.red_done = 0u;
-      }
-    }
-  }
+  if (RED) jac_reduce_tail(A, acc);
   // the rows built here (no table yet) become the list's block table
   if (!rows_ok) {
     __syncthreads();

@@ -195,3 +195,56 @@ def test_c2_full_size_unfused_jacobi(iters):
         want, mag = o.field(L.fields[name], with_mag=True)
         assert_field_close(g.field(L.fields[name]), want, mag, "f32", f"C2 full size, {iters} sweeps, {name}")
     assert st[0]["launches"] == 4 + iters   # activate, 2 listgens, FILL b + FILL x0, the sweeps
+
+
+_FLOW_CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import workloads as W
+from paper_2012_08141_b200 import sg
+iters, reduce = {iters}, {reduce}
+coords = W.block_ball_coords(32, 8, 68.0)
+L, lv = W.c2_layout()
+calls, _ = W.c2_solve_calls(L, lv, coords, iters=iters, reduce_result=reduce)
+prog = W.program(L, calls + [W.flush()])
+g, st = sg.run_program(prog, passes="all+chain")
+np.savez({out!r}, **{{n: np.asarray(g.field(L.fields[n])) for n in ("x0", "x1", "s")}})
+print(json.dumps({{"launches": st[0]["launches"], "chained": st[0]["launches_chained"]}}))
+"""
+
+
+@pytest.mark.parametrize("iters,reduce", [(3, False), (50, True)])
+def test_c2_full_size_flag_chain(iters, reduce, tmp_path):
+    """N2 (SG_PASS_CHAIN, opt-in SG_FLOW=1): the C2 solve's JACOBI sweeps as ONE
+    persistent launch with per-half-block completion flags (kernels_flow.cu),
+    run in a child process with SG_FLOW=1.  Same arithmetic per cell as one
+    launch per sweep, so the fields equal the unchained plan's bit for bit
+    (and the oracle's within 1e-5 for the 3-sweep case); the 50-sweep solve
+    ends with the fused reduction, as bench.py times it."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "flow.npz")
+    code = _FLOW_CHILD.format(root=root, iters=iters, reduce=reduce, out=out)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SG_FLOW="1"), capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    st1 = json.loads(r.stdout.strip().splitlines()[-1])
+    flow = np.load(out)
+    coords = W.block_ball_coords(32, 8, 68.0)
+    L, lv = W.c2_layout()
+    calls, _ = W.c2_solve_calls(L, lv, coords, iters=iters, reduce_result=reduce)
+    prog = W.program(L, calls + [W.flush()])
+    g0, st0 = sg.run_program(prog, passes="all")
+    assert st1["chained"] == 1 and st1["launches"] < st0[0]["launches"], (st0[0], st1)
+    names = ("x0", "x1", "s") if reduce else ("x0", "x1")
+    for name in names:
+        np.testing.assert_array_equal(flow[name], np.asarray(g0.field(L.fields[name])), err_msg=name)
+    if not reduce:
+        o = oracle.run_program(prog)
+        for name in names:
+            want, mag = o.field(L.fields[name], with_mag=True)
+            assert_field_close(flow[name], want, mag, "f32", f"C2 flag chain, {iters} sweeps, {name}")
