@@ -437,9 +437,9 @@ __global__ void __launch_bounds__(MB_TPB, MB_P2G_MINB) k_p2g_bin(const __grid_co
     }
     int o[3];
     bin_origin(A.B, key, o);
-    if (threadIdx.x == 0) S.need = 0;
-    for (int k = threadIdx.x; k < MB_WARPS * 4 * MB_TP; k += MB_TPB) (&S.tile[0][0][0])[k] = 0.0f;
-    __syncthreads();
+    // the particle records first (their global loads overlap the tile
+    // zeroing and the barrier; a warp's record slice is its own, consumed by
+    // its own walk of the previous chunk before that chunk's last barrier)
     uint32_t need = 0;
     if ((int)threadIdx.x < m) {
       const int64_t i = A.B.perm[start + c0 + threadIdx.x];
@@ -466,6 +466,9 @@ __global__ void __launch_bounds__(MB_TPB, MB_P2G_MINB) k_p2g_bin(const __grid_co
 #pragma unroll
         for (int a = 0; a < 3; a++) R[16 + 3 * a + oo] = k.w[oo][a];
     }
+    if (threadIdx.x == 0) S.need = 0;
+    for (int k = threadIdx.x; k < MB_WARPS * 4 * MB_TP; k += MB_TPB) (&S.tile[0][0][0])[k] = 0.0f;
+    __syncthreads();
     need = __reduce_or_sync(0xffffffffu, need);
     if (l == 0 && need) atomicOr(&S.need, need);
     __syncwarp();
@@ -558,35 +561,58 @@ __global__ void __launch_bounds__(MB_TPB, MB_G2P_MINB) k_g2p_bin(const __grid_co
     }
     int o[3];
     bin_origin(A.B, key, o);
+    // the particle's loads and weights first: they overlap the block lookups,
+    // the tile staging and its barriers
+    const bool act = (int)threadIdx.x < m;
+    int64_t i = 0;
+    float xp[3] = {0.0f, 0.0f, 0.0f}, J = 0.0f;
+    if (act) {
+      i = A.B.perm[start + c0 + threadIdx.x];
+      xp[0] = x[i]; xp[1] = x[X.n + i]; xp[2] = x[2 * X.n + i];
+      J = jin[i];
+    }
+    const MpmKernel k = mpm_bspline(xp, inv_dx);
     bin_blocks<false>(C, T, o, 0xffu, s_off, A.task);
     __syncthreads();
     stage_tile(T, op, 0, 3, s_off, s_u);
     __syncthreads();
-    if ((int)threadIdx.x < m) {
-      const int64_t i = A.B.perm[start + c0 + threadIdx.x];
+    if (act) {
       const int64_t io = bin_order ? (int64_t)(start + c0 + threadIdx.x) : i;
-      const float xp[3] = {x[i], x[X.n + i], x[2 * X.n + i]};
-      const float J = jin[i];
-      const MpmKernel k = mpm_bspline(xp, inv_dx);
       const int r[3] = {k.base[0] - o[0], k.base[1] - o[1], k.base[2] - o[2]};
+      // APIC: C = 4/dx^2 sum w g dpos^T with dpos = (node - fx) dx; the
+      // per-axis offsets (a - fx_d) are hoisted and the constant s4 dx applied
+      // once at the end (reassociation only: within R29's 1e-5 bound)
       float nv[3] = {0.0f, 0.0f, 0.0f}, nC[3][3] = {{0.0f}};
+      float q[3][3];
+#pragma unroll
+      for (int d = 0; d < 3; d++)
+#pragma unroll
+        for (int a = 0; a < 3; a++) q[d][a] = (float)a - k.fx[d];
+      const int nq0 = (r[0] * 6 + r[1]) * 6 + r[2];
 #pragma unroll
       for (int a = 0; a < 3; a++)
 #pragma unroll
-        for (int b = 0; b < 3; b++)
+        for (int b = 0; b < 3; b++) {
+          const float wab = k.w[a][0] * k.w[b][1];
 #pragma unroll
           for (int c = 0; c < 3; c++) {
-            const int nq = ((r[0] + a) * 6 + (r[1] + b)) * 6 + (r[2] + c);
-            const float wgt = k.w[a][0] * k.w[b][1] * k.w[c][2];
-            const float dpos[3] = {((float)a - k.fx[0]) * dx, ((float)b - k.fx[1]) * dx, ((float)c - k.fx[2]) * dx};
+            const int nq = nq0 + (a * 6 + b) * 6 + c;
+            const float wgt = wab * k.w[c][2];
 #pragma unroll
             for (int rr = 0; rr < 3; rr++) {
-              const float g = s_u[rr][nq];
-              nv[rr] += wgt * g;
-#pragma unroll
-              for (int d = 0; d < 3; d++) nC[rr][d] += s4 * wgt * g * dpos[d];
+              const float wg = wgt * s_u[rr][nq];
+              nv[rr] += wg;
+              nC[rr][0] += wg * q[0][a];
+              nC[rr][1] += wg * q[1][b];
+              nC[rr][2] += wg * q[2][c];
             }
           }
+        }
+      const float sc = s4 * dx;
+#pragma unroll
+      for (int rr = 0; rr < 3; rr++)
+#pragma unroll
+        for (int d = 0; d < 3; d++) nC[rr][d] *= sc;
 #pragma unroll
       for (int rr = 0; rr < 3; rr++) {
         vo[rr * Vo.n + io] = nv[rr];
