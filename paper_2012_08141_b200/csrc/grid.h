@@ -83,6 +83,7 @@ struct sg_grid {
   // per half block of the leaf pool, one epoch / done counter pair per grid
   std::vector<uint32_t*> flow_flags;
   uint32_t* flow_ctl = nullptr;
+  std::vector<sg::T2Buffers> t2_bufs;   // 2-sweep chain scratch per tree
   // particle bins (binned MPM kernels) + a one-entry cache keyed by the
   // position array, its write epoch, the tree and the range
   DBins bins{};

@@ -495,20 +495,58 @@ static void group_ops(const sg_grid* g, const std::vector<int>& members, const s
   for (size_t i = 0; i < members.size(); i++) make_op(g, g->eager[members[i]], acts[i], tree, all[i]);
 }
 
-// The first phase of a chain's tail of JACOBI sweeps that runs as one
-// flag-chained launch (the phases before it launch one by one), or -1.
-// Opt-in (SG_FLOW=1): measured SLOWER than one graph-replayed launch per
-// sweep on C2 (1,866 vs 3,974 solves/s: every sweep of a half block pays a
-// flag poll, its loads and a release fence in series, ~10 us per sweep
-// against ~4.4 us per graph-replayed launch) -- a negative result kept with
-// its tests.
-static int chain_flow_start(const sg_grid* g, const PTask& t0, const std::vector<DOp>& all,
-                            const std::vector<int>& phase_end) {
+// A chain's tail of JACOBI sweeps on 8^3 blocks, two opt-in variants, both
+// bit-identical to one launch per sweep and both measured SLOWER than one
+// graph-replayed launch per sweep on C2 (~4.4 us each) -- negative results
+// kept with their tests (kernels_flow.cu):
+//   SG_T2=1   two sweeps per launch (temporal blocking through shared
+//             memory): 1,840 vs 3,954 solves/s -- a CTA stages one block with
+//             its 2-deep halo per iteration, so only ~4 blocks per SM are in
+//             flight (registers, 23.6 KB of shared memory each) and every
+//             block pays its L2 round trips in series: ~20 us per 2 sweeps;
+//   SG_FLOW=1 one flag-chained launch: 1,866 vs 3,974 solves/s (every sweep
+//             of a half block pays a flag poll, its loads and a release fence
+//             in series, ~10 us per sweep).
+// The phases before the tail launch one by one.
+static bool t2_on() {
+  static const bool on = getenv("SG_T2") && atoi(getenv("SG_T2")) != 0;
+  return on;
+}
+
+static bool flow_on() {
   static const bool on = getenv("SG_FLOW") && atoi(getenv("SG_FLOW")) != 0;
-  if (!on || phase_end.size() < 2) return -1;
+  return on;
+}
+
+// The first phase of a chain's tail of JACOBI sweeps on 8^3 blocks, or -1.
+static int chain_jacobi_start(const sg_grid* g, const PTask& t0, const std::vector<DOp>& all,
+                              const std::vector<int>& phase_end) {
+  if (phase_end.size() < 2) return -1;
   const DTree& T = g->dtrees[t0.tree];
   const DList* drive = T.driving >= 0 ? &g->lists[t0.tree][T.driving] : nullptr;
   return jacobi_flow_start(T, drive, all.data(), phase_end.data(), (int)phase_end.size());
+}
+
+// Scratch of the 2-sweep chain kernels for a tree's driving list (first use
+// is never inside a CUDA-graph capture, as for the flag buffers).
+static bool t2_buffers(sg_grid* g, int tree, const DList* drive, T2Buffers* bf) {
+  if ((int)g->t2_bufs.size() <= tree) g->t2_bufs.resize(tree + 1, T2Buffers{nullptr, nullptr, nullptr, nullptr});
+  T2Buffers& b = g->t2_bufs[tree];
+  if (!b.ctl) {
+    const DSeg& S = g->dtrees[tree].seg[g->dtrees[tree].nseg - 1];
+    const size_t ninv = ((size_t)S.capacity + 1) * S.stride / 512 + 1, cap = drive->capacity;
+    b.inv = (uint64_t*)g->dev_alloc(ninv * 8);
+    b.rows = (uint32_t*)g->dev_alloc(cap * 54 * 4);
+    b.tmp = (float*)g->dev_alloc(cap * 512 * 4);
+    b.ctl = (uint32_t*)g->dev_alloc(16);
+    if (!b.inv || !b.rows || !b.tmp || !b.ctl || cudaMemsetAsync(b.inv, 0, ninv * 8, g->stream) != cudaSuccess ||
+        cudaMemsetAsync(b.ctl, 0, 16, g->stream) != cudaSuccess) {
+      b.ctl = nullptr;
+      return false;
+    }
+  }
+  *bf = b;
+  return true;
 }
 
 // Flag buffers of a tree (allocated and zeroed on first use: a plan's first
@@ -648,8 +686,28 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
         int nbr = 0;
         for (int i = 0; i < nops; i++) make_op(g, g->eager[members[i]], acts[i], t0.tree, all[i]);
         uint32_t *ffl = nullptr, *fct = nullptr;
-        const int fs = chain_flow_start(g, t0, all, phase_end);
-        if (fs >= 0 && flow_buffers(g, t0.tree, &ffl, &fct)) {
+        const int fs = chain_jacobi_start(g, t0, all, phase_end);
+        T2Buffers bf;
+        if (fs >= 0 && !flow_on() && t2_on() &&
+            jacobi_t2_applies(all.data(), phase_end.data(), fs, (int)phase_end.size()) &&
+            t2_buffers(g, t0.tree, drive, &bf)) {
+          int begin = 0;
+          for (int ph = 0; ph < fs && !rc; ph++) {
+            rc = launch_struct_for(g->ctx, T, t0.tree, drive, all.data() + begin, phase_end[ph] - begin, task,
+                                   g->stream, grid_hint_struct(g, T), nullptr, nullptr, 1, 0);
+            begin = phase_end[ph];
+            st.launches++;
+          }
+          if (!rc) {
+            const int nl = launch_jacobi_t2(g->ctx, T, drive, all.data(), phase_end.data(), fs,
+                                            (int)phase_end.size(), bf, task, g->stream);
+            if (nl < 0) rc = nl;
+            else st.launches += nl - 1;
+          }
+          st.launches_chained++;
+          break;
+        }
+        if (fs >= 0 && flow_on() && flow_buffers(g, t0.tree, &ffl, &fct)) {
           // leading phases (e.g. the fused FILLs of a solve) one launch each,
           // then the sweeps as one flag-chained launch
           int begin = 0;
@@ -899,8 +957,12 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
         if (plan->phase_ends[gi].size() > 1) {
           std::vector<DOp> all;
           group_ops(g, mem, acts, t.tree, all);
-          const int fs = chain_flow_start(g, t, all, plan->phase_ends[gi]);
-          if (fs >= 0) { st.launches += fs; st.launches_chained++; }
+          const int fs = chain_jacobi_start(g, t, all, plan->phase_ends[gi]);
+          const int nph = (int)plan->phase_ends[gi].size();
+          if (fs >= 0 && !flow_on() && t2_on() && jacobi_t2_applies(all.data(), plan->phase_ends[gi].data(), fs, nph)) {
+            st.launches += fs + jacobi_t2_launches(fs, nph) - 1;
+            st.launches_chained++;
+          } else if (fs >= 0 && flow_on()) { st.launches += fs; st.launches_chained++; }
           else if (chain_is_split(g, t, mem.size(), plan->phase_ends[gi].size()))
             st.launches += (int64_t)plan->phase_ends[gi].size() - 1;
           else st.launches_chained++;

@@ -172,6 +172,24 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int tree_id, const DList*
 // phases), or -1.  flags: 2 * (leaf pool words / 512 + 1) zeroed u32; ctl: 3
 // zeroed u32.
 int jacobi_flow_start(const DTree& t, const DList* drive, const DOp* ops, const int* phase_end, int nph);
+// Scratch of the 2-sweep (temporal) chain kernels (kernels_flow.cu): inv
+// [leaf pool words / 512 + 1] u64, rows [list capacity * 54] u32, tmp [list
+// capacity * 512] f32, ctl 2 zeroed u32.
+struct T2Buffers {
+  uint64_t* inv;
+  uint32_t* rows;
+  float* tmp;
+  uint32_t* ctl;
+};
+// The chain tail [first, nph) ping-pongs between two fields with one rhs and
+// has >= 4 sweeps; the launches it takes two sweeps per launch.
+bool jacobi_t2_applies(const DOp* ops, const int* phase_end, int first, int nph);
+int jacobi_t2_launches(int first, int nph);
+// Launches the chain tail [first, nph) two sweeps per launch; returns the
+// launch count, 0 when the chain does not have the ping-pong shape, or a
+// negative sg_status.
+int launch_jacobi_t2(const DevCtx& c, const DTree& t, const DList* drive, const DOp* ops, const int* phase_end,
+                     int first, int nph, const T2Buffers& bf, int task_id, void* stream);
 int launch_jacobi_flow(const DevCtx& c, const DTree& t, const DList* drive, const DOp* ops, const int* phase_end,
                        int first, int nph, uint32_t* flags, uint32_t* ctl, int task_id, void* stream);
 struct RangeScratch {

@@ -1,12 +1,15 @@
 """C2 solve timed as bench.py times its headline (device events around each
 flush, steps pipelined, L2 flushed before each) with passes "all" (one launch
 per sweep, graph-replayed) and "all+chain" (the sweeps as one flag-chained
-launch, kernels_flow.cu); one JSON line."""
+launch, or two sweeps per launch with SG_T2=1; kernels_flow.cu); one JSON line."""
 import json
 import os
 import sys
 
-os.environ.setdefault("SG_FLOW", "1")   # the chain pass runs the flag-chained kernel
+# the chain pass runs the flag-chained kernel (SG_FLOW=1) unless SG_T2=1 picks
+# the two-sweep kernel
+if os.environ.get("SG_T2") != "1":
+    os.environ.setdefault("SG_FLOW", "1")
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402

@@ -248,3 +248,61 @@ def test_c2_full_size_flag_chain(iters, reduce, tmp_path):
         for name in names:
             want, mag = o.field(L.fields[name], with_mag=True)
             assert_field_close(flow[name], want, mag, "f32", f"C2 flag chain, {iters} sweeps, {name}")
+
+
+_T2_CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import workloads as W
+from paper_2012_08141_b200 import sg
+iters, reduce = {iters}, {reduce}
+coords = W.block_ball_coords(32, 8, 68.0)
+L, lv = W.c2_layout()
+calls, _ = W.c2_solve_calls(L, lv, coords, iters=iters, reduce_result=reduce)
+prog = W.program(L, calls + [W.flush()])
+g, st = sg.Grid(prog["desc"]), []
+res = []
+for _ in range(3):   # the second flush is captured as a CUDA graph, the third replays it
+    st = sg.replay(g, prog, passes="all+chain", device="cuda")
+    g.sync()
+    res.append({{n: np.asarray(g.field(L.fields[n])) for n in ("x0", "x1", "s")}})
+np.savez({out!r}, **{{f"{{n}}_{{i}}": r[n] for i, r in enumerate(res) for n in r}})
+print(json.dumps({{"launches": st[0]["launches"], "chained": st[0]["launches_chained"]}}))
+"""
+
+
+@pytest.mark.parametrize("iters,reduce", [(4, False), (7, False), (50, True)])
+def test_c2_full_size_two_sweep_chain(iters, reduce, tmp_path):
+    """N2 (SG_PASS_CHAIN, opt-in SG_T2=1, run in a child process): the C2
+    solve's JACOBI sweeps two per launch (temporal blocking with a scratch
+    field, kernels_flow.cu): each cell sees the same float operations in the
+    same order as one launch per sweep, so both ping-pong fields equal the
+    unchained plan's bit for bit, on the first flush, the captured second and
+    the replayed third; the fused reduction sums in another order (1e-6).
+    7 sweeps: 3 single launches + one A/B cycle; 50: 2 singles + 12 cycles."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "t2.npz")
+    code = _T2_CHILD.format(root=root, iters=iters, reduce=reduce, out=out)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SG_T2="1"), capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    st1 = json.loads(r.stdout.strip().splitlines()[-1])
+    t2 = np.load(out)
+    coords = W.block_ball_coords(32, 8, 68.0)
+    L, lv = W.c2_layout()
+    calls, _ = W.c2_solve_calls(L, lv, coords, iters=iters, reduce_result=reduce)
+    prog = W.program(L, calls + [W.flush()])
+    g0, st0 = sg.run_program(prog, passes="all")
+    assert st1["chained"] == 1 and st1["launches"] <= st0[0]["launches"], (st0[0], st1)
+    for i in range(3):
+        for name in ("x0", "x1"):
+            np.testing.assert_array_equal(t2[f"{name}_{i}"], np.asarray(g0.field(L.fields[name])),
+                                          err_msg=f"flush {i}: {name}")
+        if reduce:
+            a, b = float(t2[f"s_{i}"]), float(g0.field(L.fields["s"]))
+            assert abs(a - b) <= 1e-6 * abs(b), (i, a, b)
