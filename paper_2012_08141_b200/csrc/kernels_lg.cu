@@ -397,7 +397,17 @@ __global__ void __launch_bounds__(LG_TPB) k_listgen(const __grid_constant__ LGAr
 // the list (correct, uncoalesced).
 // ---------------------------------------------------------------------------
 constexpr int LGW_MIN_HINT = 64;   // CTA tiles (2048 chunks) below which the CTA-tile kernel runs
-constexpr int LGW_TPB = 128, LGW_WARPS = LGW_TPB / 32, LGW_WPL = 8, LGW_SUBTILE = 32 * LGW_WPL, LGW_SUB = 4,
+#ifndef LGW_UNROLL
+#define LGW_UNROLL 4   // extraction loop unroll (8 measured slower: 297 vs 287 us)
+#endif
+constexpr int kLgwUnroll = LGW_UNROLL;
+#ifndef LGW_SUBN
+#define LGW_SUBN 4   // sub-tiles per warp tile (one look-back per tile)
+#endif
+#ifndef LGW_TPBN
+#define LGW_TPBN 128
+#endif
+constexpr int LGW_TPB = LGW_TPBN, LGW_WARPS = LGW_TPB / 32, LGW_WPL = 8, LGW_SUBTILE = 32 * LGW_WPL, LGW_SUB = LGW_SUBN,
               LGW_TILE = LGW_SUB * LGW_SUBTILE, LGW_CAP = 1024, LGW_LB = 1;
 #ifndef LGW_SLEEP
 #define LGW_SLEEP 128   // look-back back-off (ns); 0 / 32 / 512 measured the same on LG-XL
@@ -419,7 +429,7 @@ __device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {   // index of the hi
 // streams per lane to overlap that load measured slower: 1.5x the
 // instructions, 350 vs 287 us on LG-XL.)
 __device__ __forceinline__ void lgw_extract(uint32_t* dst, uint32_t cnt, uint32_t b, uint32_t hi, const uint2* rec) {
-#pragma unroll 4   // (8 measured slower: 297 vs 287 us)
+#pragma unroll kLgwUnroll
   for (uint32_t i = 0; i < cnt; i++) {
     if (b == 0u) {
       const uint2 r = *rec;
