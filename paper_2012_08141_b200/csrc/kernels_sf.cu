@@ -157,8 +157,8 @@ int launch_struct_for(const DevCtx& c, const DTree& t, int, const DList* drive, 
     j.red_done = c.red_done;
     // (programmatic dependent launch was measured here: 4.36 vs 4.12 us per
     // launch inside the graph -- slower, so plain launches)
-    if (jac_red) k_jacobi8<true><<<num_sms() * 4, 256, 0, s>>>(j);
-    else k_jacobi8<false><<<num_sms() * 4, 256, 0, s>>>(j);
+    if (jac_red) k_jacobi8<true><<<num_sms() * SG_JAC8_MINB, 256, 0, s>>>(j);
+    else k_jacobi8<false><<<num_sms() * SG_JAC8_MINB, 256, 0, s>>>(j);
     delete a;
     return check_launch();
   }

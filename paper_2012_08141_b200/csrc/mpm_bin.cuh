@@ -832,25 +832,32 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_adj_bin(const __grid_constant
     }
     int o[3];
     bin_origin(A.B, key, o);
+    // the particle's state loads first: they overlap the block lookups, the
+    // tile staging and its barriers (as k_g2p_bin)
+    const bool act = (int)threadIdx.x < m;
+    int64_t i = 0;
+    float xp[3] = {0.0f, 0.0f, 0.0f}, J = 1.0f, vv[3] = {0.0f, 0.0f, 0.0f}, Am[3][3];
+    if (act) {
+      i = A.B.perm[start + c0 + threadIdx.x];
+      xp[0] = x[i]; xp[1] = x[nx + i]; xp[2] = x[2 * nx + i];
+      J = jj[i];
+#pragma unroll
+      for (int rr = 0; rr < 3; rr++) vv[rr] = v[rr * nv + i];
+    }
+#pragma unroll
+    for (int rr = 0; rr < 3; rr++)
+#pragma unroll
+      for (int c = 0; c < 3; c++)
+        Am[rr][c] = (act ? pm * cm[(3 * rr + c) * nc + i] : 0.0f) + (rr == c ? kJ * (J - 1.0f) : 0.0f);
     bin_blocks<false>(C, T, o, 0xffu, s_off, A.task);
     __syncthreads();
     stage_tile(T, op, 0, 4, s_off, s_g);
     __syncthreads();
-    if ((int)threadIdx.x < m) {
-      const int64_t i = A.B.perm[start + c0 + threadIdx.x];
-      const float xp[3] = {x[i], x[nx + i], x[2 * nx + i]};
+    if (act) {
       const MpmKernel k = mpm_bspline(xp, inv_dx);
       float dw[3][3];
       mpm_dw(k, dw);
       const int r[3] = {k.base[0] - o[0], k.base[1] - o[1], k.base[2] - o[2]};
-      const float J = jj[i];
-      float vv[3], Am[3][3];
-#pragma unroll
-      for (int rr = 0; rr < 3; rr++) {
-        vv[rr] = v[rr * nv + i];
-#pragma unroll
-        for (int c = 0; c < 3; c++) Am[rr][c] = pm * cm[(3 * rr + c) * nc + i] + (rr == c ? kJ * (J - 1.0f) : 0.0f);
-      }
       float xbar[3] = {0.0f, 0.0f, 0.0f}, vbar[3] = {0.0f, 0.0f, 0.0f}, Ab[3][3] = {{0.0f}};
 #pragma unroll
       for (int a = 0; a < 3; a++)

@@ -1090,8 +1090,11 @@ __device__ __forceinline__ void jac_reduce_tail(const JacArgs& A, double acc) {
   }
 }
 
+#ifndef SG_JAC8_MINB
+#define SG_JAC8_MINB 4   // CTAs per SM k_jacobi8 is register-sized for (grid = SMs x this)
+#endif
 template <bool RED>
-__global__ void __launch_bounds__(256, 4) k_jacobi8(const __grid_constant__ JacArgs A) {
+__global__ void __launch_bounds__(256, SG_JAC8_MINB) k_jacobi8(const __grid_constant__ JacArgs A) {
   double acc = 0.0;
   const uint32_t* P = A.T.seg[A.T.nseg - 1].base;
   const uint32_t* __restrict__ src = P + A.s_src;
