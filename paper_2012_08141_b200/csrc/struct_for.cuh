@@ -1052,6 +1052,52 @@ __device__ __forceinline__ double jac8_half(const uint32_t* __restrict__ src, co
   return acc;
 }
 
+// A quarter block (x in [2 part, 2 part + 2)) per warp: one quad per lane;
+// lanes l and l ^ 16 hold x-adjacent quads, so each lane loads only its OUTER
+// x neighbour and takes the inner one from its partner (same loads per cell
+// as jac8_half, twice the units: 13,120 on C2 instead of 6,560 over 4,736
+// resident warps).  Same float operations in the same order as jac8_half.
+template <bool RED>
+__device__ __forceinline__ double jac8_quarter(const uint32_t* __restrict__ src, const uint32_t* __restrict__ rhs,
+                                               uint32_t* dst, uint32_t blk, const uint32_t (&nb)[6], uint32_t part,
+                                               int lane, float inv) {
+  const int xh = lane >> 4, x = (int)part * 2 + xh, y = (lane >> 1) & 7, zh = lane & 1;
+  const uint32_t j = ((uint32_t)x << 6) | ((uint32_t)y << 3) | ((uint32_t)zh << 2);
+  const uint32_t o = blk + j;
+  const uint4 cu = *reinterpret_cast<const uint4*>(src + o);
+  const uint4 ru = *reinterpret_cast<const uint4*>(rhs + o);
+  const uint32_t nz = zh ? nb[5] : nb[4];
+  const uint32_t zo = zh ? 0u : 7u;
+  const float zv = __uint_as_float(ld1_if(src + nz + (j & ~7u) + zo, nz != SG_NO_BLOCK));
+  // outer x neighbour: x - 1 for the lower lane half, x + 1 for the upper
+  const bool xin = xh ? x < 7 : x > 0;
+  const uint32_t xnb = xh ? nb[1] : nb[0];
+  const uint4 xou = ld4_if(src + (xin ? (xh ? o + 64u : o - 64u) : (xh ? xnb + j - 448u : xnb + j + 448u)),
+                           xin || xnb != SG_NO_BLOCK);
+  const bool ym_in = y > 0, yp_in = y < 7;
+  const uint4 ymu = ld4_if(src + (ym_in ? o - 8u : nb[2] + j + 56u), ym_in || nb[2] != SG_NO_BLOCK);
+  const uint4 ypu = ld4_if(src + (yp_in ? o + 8u : nb[3] + j - 56u), yp_in || nb[3] != SG_NO_BLOCK);
+  const float4 c = u2f(cu);
+  const float p = __shfl_xor_sync(0xffffffffu, zh ? c.x : c.w, 1);
+  float4 pc;   // the partner's quad: the inner x neighbour
+  pc.x = __shfl_xor_sync(0xffffffffu, c.x, 16);
+  pc.y = __shfl_xor_sync(0xffffffffu, c.y, 16);
+  pc.z = __shfl_xor_sync(0xffffffffu, c.z, 16);
+  pc.w = __shfl_xor_sync(0xffffffffu, c.w, 16);
+  const float4 xo = u2f(xou);
+  const float4 xm = xh ? pc : xo, xp = xh ? xo : pc, ym = u2f(ymu), yp = u2f(ypu), r = u2f(ru);
+  const float lo = zh ? p : zv, hi = zh ? zv : p;
+  float s0 = lo + c.y, s1 = c.x + c.z, s2 = c.y + c.w, s3 = c.z + hi;
+  s0 += xm.x; s1 += xm.y; s2 += xm.z; s3 += xm.w;
+  s0 += xp.x; s1 += xp.y; s2 += xp.z; s3 += xp.w;
+  s0 += ym.x; s1 += ym.y; s2 += ym.z; s3 += ym.w;
+  s0 += yp.x; s1 += yp.y; s2 += yp.z; s3 += yp.w;
+  const float4 out = make_float4((r.x + s0) * inv, (r.y + s1) * inv, (r.z + s2) * inv, (r.w + s3) * inv);
+  *reinterpret_cast<uint4*>(dst + o) =
+      make_uint4(__float_as_uint(out.x), __float_as_uint(out.y), __float_as_uint(out.z), __float_as_uint(out.w));
+  return RED ? (double)(((out.x + out.y) + out.z) + out.w) : 0.0;
+}
+
 // Deterministic end of a fused JACOBI + REDUCE_SUM (k_jacobi8<true>,
 // k_jacobi8_flow<true>): per-CTA f64 partials summed in CTA order by the last
 // CTA into the 0-D target.
@@ -1090,6 +1136,9 @@ __device__ __forceinline__ void jac_reduce_tail(const JacArgs& A, double acc) {
   }
 }
 
+#ifndef SG_JAC8_QUARTER
+#define SG_JAC8_QUARTER 0   // k_jacobi8 unit: 0 half block per warp, 1 quarter block
+#endif
 #ifndef SG_JAC8_MINB
 #define SG_JAC8_MINB 4   // CTAs per SM k_jacobi8 is register-sized for (grid = SMs x this)
 #endif
@@ -1104,9 +1153,10 @@ __global__ void __launch_bounds__(256, SG_JAC8_MINB) k_jacobi8(const __grid_cons
   const bool rows_ok = A.table_ctl[4] != 0u;   // set by an earlier launch
   const int lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), GW = gridDim.x * (blockDim.x >> 5);
-  // one warp per half block (jac8_half)
-  for (uint32_t wq = gw; wq < nent * 2u; wq += GW) {
-    const uint32_t e = wq >> 1, part = wq & 1u;
+  // one warp per half block (jac8_half) or per quarter block (jac8_quarter)
+  constexpr uint32_t UPB = SG_JAC8_QUARTER ? 4u : 2u, USH = SG_JAC8_QUARTER ? 2u : 1u;
+  for (uint32_t wq = gw; wq < nent * UPB; wq += GW) {
+    const uint32_t e = wq >> USH, part = wq & (UPB - 1u);
     uint32_t blk, nb[6];
     if (rows_ok) {
       const uint32_t rv = lane < 12 ? reinterpret_cast<const uint32_t*>(A.table + e)[lane] : 0u;
@@ -1124,7 +1174,8 @@ __global__ void __launch_bounds__(256, SG_JAC8_MINB) k_jacobi8(const __grid_cons
       for (int d = 0; d < 6; d++) nb[d] = r.nbr[d];
     }
     if (blk == SG_NO_BLOCK) continue;
-    acc += jac8_half<RED>(src, rhs, dst, blk, nb, part, lane, A.inv);
+    if (SG_JAC8_QUARTER) acc += jac8_quarter<RED>(src, rhs, dst, blk, nb, part, lane, A.inv);
+    else acc += jac8_half<RED>(src, rhs, dst, blk, nb, part, lane, A.inv);
   }
   if (RED) jac_reduce_tail(A, acc);
   // the rows built here (no table yet) become the list's block table
