@@ -269,10 +269,12 @@ def run_sg(args, rank, world, device):
     }
 
 
-def cpu_baseline(args, max_seconds=30.0):
+def cpu_baseline(args, max_seconds=30.0, keep=None):
     """The oracle as it stands on this host's cores (single-threaded by
     construction), on a bounded sample: the full 256^3 C2 grid with 1 and 2
-    Jacobi iterations; solves/s extrapolated to 50 iterations."""
+    Jacobi iterations; solves/s extrapolated to 50 iterations.  keep: a dict
+    that receives each run's fields (value, shadow magnitude) for the in-run
+    parity check (after the timing)."""
     import oracle
     L, lv = W.c2_layout()
     coords = W.block_ball_coords(32, 8, 68.0)
@@ -284,6 +286,8 @@ def cpu_baseline(args, max_seconds=30.0):
         for c in calls:
             o.call(c)
         times.append(time.perf_counter() - t0)
+        if keep is not None:
+            keep[iters] = {n: o.field(L.fields[n], with_mag=True) for n in ("x0", "x1", "s")}
         del o
     t_iter = max(times[1] - times[0], 1e-9)
     t_setup = max(times[0] - t_iter, 0.0)
@@ -292,6 +296,31 @@ def cpu_baseline(args, max_seconds=30.0):
             "sample": f"C2 full grid, 1 and 2 Jacobi iterations timed ({times[0]:.1f}s, {times[1]:.1f}s); "
                       f"{args.iters}-iteration solve extrapolated = {t_solve:.1f}s",
             "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "oracle_threads": 1}
+
+
+def parity_in_run(oracle_fields):
+    """SURVEY 8d.3 "parity in the same run": the C2 solve at the bench's full
+    size with 1 and 2 iterations through the same library and passes, every
+    element of x0, x1 and s against the oracle runs the CPU baseline just
+    timed, at |g - o| <= 1e-5 max(|o|, M) (reading R15)."""
+    from paper_2012_08141_b200 import sg
+    L, lv = W.c2_layout()
+    coords = W.block_ball_coords(32, 8, 68.0)
+    out = {}
+    for iters, want in sorted(oracle_fields.items()):
+        calls, _ = W.c2_solve_calls(L, lv, coords, iters)
+        g, _ = sg.run_program(W.program(L, calls + [W.flush()]))
+        worst, ok = 0.0, True
+        for name, (o, m) in want.items():
+            got = np.asarray(g.field(L.fields[name]), dtype=np.float64).reshape(o.shape)
+            r = np.abs(got - o) / np.maximum(np.maximum(np.abs(o), m), 1e-300)
+            worst = max(worst, float(r.max()))
+            ok &= bool((r <= 1e-5).all())
+        out[f"c2_{iters}_iteration{'s' if iters > 1 else ''}"] = {
+            "fields": sorted(want), "elements": int(sum(w[0].size for w in want.values())),
+            "max_err_over_M": worst, "tolerance": 1e-5, "ok": ok}
+        g.close()
+    return out
 
 
 def cpu_model():
@@ -974,8 +1003,10 @@ def main():
                 except Exception as e:  # keep the main line even if an extra fails
                     extra[name] = {"error": repr(e)[:200]}
             out["extra"] = extra
+            # against the measured copy peak AND the north star's 8 TB/s
             out["roofline_xl"] = {k: {"achieved": extra[k].get("achieved_GBps"), "frac": extra[k].get("frac"),
                                       "peak": extra[k].get("peak_GBps"), "unit": "GB/s",
+                                      "frac_of_8TBps": (extra[k].get("achieved_GBps") or 0.0) / 8000.0,
                                       "bytes_per_launch": extra[k].get("bytes_per_launch")}
                                   for k in ("jac_xl", "sf_xl", "sf_xl_interpreter", "cg_xl", "cg_xl_jit", "lg_xl")}
             jx = extra.get("jac_xl", {})
@@ -983,10 +1014,13 @@ def main():
                 out["roofline_hbm"] = {"bound": "hbm", "kernel": "k_jacobi8 at JAC-XL (1024^3, 206K 8^3 blocks)",
                                        "achieved": jx["achieved_GBps"], "peak": jx["peak_GBps"], "unit": "GB/s",
                                        "frac": jx["frac"], "peak_source": jx["peak_source"],
+                                       "frac_of_8TBps": jx["achieved_GBps"] / 8000.0,
                                        "traffic": jac_xl_traffic(),
                                        "algorithmic_bytes_per_launch": jx["bytes_per_launch"]}
         if not args.no_cpu_baseline and world == 1:
-            out["cpu_baseline"] = cpu_baseline(args)
+            keep = {}
+            out["cpu_baseline"] = cpu_baseline(args, keep=keep)
+            out["parity_in_run"] = parity_in_run(keep)
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
