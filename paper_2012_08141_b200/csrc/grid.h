@@ -87,14 +87,27 @@ struct sg_grid {
   // particle bins (binned MPM kernels) + a one-entry cache keyed by the
   // position array, its write epoch, the tree and the range
   DBins bins{};
-  int64_t bin_cap = 0;
-  uint32_t bin_keys_cap = 0;
-  bool bin_valid = false;
-  int bin_xarr = -1, bin_nb[3] = {0, 0, 0};
-  float bin_inv_dx = 0.0f;
-  uint64_t bin_epoch = 0;
-  int64_t bin_n = 0;
-  const int32_t* bin_dcount = nullptr;
+  int64_t bin_cap = 0;                 // per-particle scratch (rank, key) capacity
+  uint32_t bin_keys_cap = 0;           // per-key scratch (hist, tsum) capacity
+  // binnings of the current flush window, one slot each (perm, off, bins,
+  // nbins), assigned in the order the window first needs them -- so a
+  // replayed plan reuses the same slots (CUDA-graph arguments stay valid) --
+  // and found again by (array, write epoch, range, geometry): C4's backward
+  // pass reuses every substep's forward binning
+  struct BinSlot {
+    bool valid = false;
+    int xa = -1, nb[3] = {0, 0, 0};
+    uint64_t epoch = 0;
+    int64_t n = 0, cap = 0;
+    const int32_t* dcount = nullptr;
+    float inv_dx = 0.0f;
+    uint32_t kcap = 0;
+    uint32_t *perm = nullptr, *off = nullptr, *bins = nullptr, *nbins = nullptr;
+  };
+  std::vector<BinSlot> bin_slots;
+  int bin_next = 0;                    // next slot of this window
+  uint64_t bin_gen = 0;                // bumped by every (re)allocation: CUDA-graph signature
+  DBins bins_cur{};                    // the binning the current launch uses
   bool no_bin = false;                 // SG_NO_BIN=1: per-particle kernels (A/B measurements)
   std::vector<uint64_t> arr_epoch;     // bumped by every launched task that writes the array
   // launch profiling (benchmarks): event pairs per launch group

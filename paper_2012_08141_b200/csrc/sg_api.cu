@@ -596,6 +596,8 @@ static bool tree_lb2(const DTree& t) {
 // the same bin geometry (blocks per axis, cell size).  The geometry, not the
 // tree id: C4's adjoint tree has the grid tree's shape, so P2G, G2P_ADJ and
 // P2G_ADJ of one substep share one binning of its positions.
+constexpr int BIN_SLOTS = 160;   // C4: 65 states (T = 64) x forward + backward fit
+
 static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t n, const int32_t* dcount,
                              int64_t& aux) {
   const DTree& T = g->dtrees[tree];
@@ -606,38 +608,62 @@ static sg_status ensure_bins(sg_grid* g, int tree, int xa, float inv_dx, int64_t
   if (nk > 0x7fffffffull) return fail(SG_ERR_ARG, "too many leaf blocks for particle binning");
   const uint32_t nkeys = (uint32_t)nk;
   const int64_t cap = g->arrays[xa].n;
+  // shared scratch of the binning kernels
   if (cap > g->bin_cap) {
     g->bins.rank = (uint32_t*)g->dev_alloc((size_t)cap * 4);
     g->bins.key = (uint32_t*)g->dev_alloc((size_t)cap * 4);
-    g->bins.perm = (uint32_t*)g->dev_alloc((size_t)cap * 4);
-    if (!g->bins.rank || !g->bins.key || !g->bins.perm) return fail(SG_ERR_CUDA, "bin allocation failed");
+    if (!g->bins.rank || !g->bins.key) return fail(SG_ERR_CUDA, "bin allocation failed");
     g->bin_cap = cap;
+    g->bin_gen++;
   }
   if (nkeys > g->bin_keys_cap) {
     const uint32_t nt = bin_ntiles(nkeys);
     g->bins.hist = (uint32_t*)g->dev_alloc((size_t)nt * 2048 * 4);
-    g->bins.off = (uint32_t*)g->dev_alloc(((size_t)nkeys + 1) * 4);
     g->bins.tsum = (uint32_t*)g->dev_alloc((size_t)nt * 8);
-    g->bins.bins = (uint32_t*)g->dev_alloc((size_t)nkeys * 4);
-    if (!g->bins.nbins) g->bins.nbins = (uint32_t*)g->dev_alloc(16);
-    if (!g->bins.hist || !g->bins.off || !g->bins.tsum || !g->bins.bins || !g->bins.nbins)
-      return fail(SG_ERR_CUDA, "bin allocation failed");
+    if (!g->bins.hist || !g->bins.tsum) return fail(SG_ERR_CUDA, "bin allocation failed");
     CUDA_TRY(cudaMemsetAsync(g->bins.hist, 0, (size_t)nt * 2048 * 4, g->stream));
     g->bin_keys_cap = nkeys;
+    g->bin_gen++;
   }
-  g->bins.nkeys = nkeys;
-  for (int a = 0; a < 3; a++) g->bins.nb[a] = nb[a];
-  if (g->bin_valid && g->bin_xarr == xa && g->bin_epoch == g->arr_epoch[xa] && g->bin_nb[0] == nb[0] &&
-      g->bin_nb[1] == nb[1] && g->bin_nb[2] == nb[2] && g->bin_inv_dx == inv_dx && g->bin_n == n &&
-      g->bin_dcount == dcount)
-    return SG_OK;
-  if (launch_bin(g->bins, (const float*)g->arrays[xa].ptr, g->arrays[xa].n, n, dcount, inv_dx, g->stream))
+  auto use = [&](const sg_grid::BinSlot& sl) {
+    g->bins_cur = g->bins;
+    g->bins_cur.perm = sl.perm;
+    g->bins_cur.off = sl.off;
+    g->bins_cur.bins = sl.bins;
+    g->bins_cur.nbins = sl.nbins;
+    g->bins_cur.nkeys = nkeys;
+    for (int a = 0; a < 3; a++) g->bins_cur.nb[a] = nb[a];
+  };
+  for (const sg_grid::BinSlot& sl : g->bin_slots)
+    if (sl.valid && sl.xa == xa && sl.epoch == g->arr_epoch[xa] && sl.nb[0] == nb[0] && sl.nb[1] == nb[1] &&
+        sl.nb[2] == nb[2] && sl.inv_dx == inv_dx && sl.n == n && sl.dcount == dcount) {
+      use(sl);
+      return SG_OK;
+    }
+  const int si = g->bin_next++ % BIN_SLOTS;
+  if ((int)g->bin_slots.size() <= si) g->bin_slots.resize(si + 1);
+  sg_grid::BinSlot& sl = g->bin_slots[si];
+  if (sl.cap < cap) {
+    sl.perm = (uint32_t*)g->dev_alloc((size_t)cap * 4);
+    if (!sl.perm) return fail(SG_ERR_CUDA, "bin allocation failed");
+    sl.cap = cap;
+    g->bin_gen++;
+  }
+  if (sl.kcap < nkeys) {
+    sl.off = (uint32_t*)g->dev_alloc(((size_t)nkeys + 1) * 4);
+    sl.bins = (uint32_t*)g->dev_alloc((size_t)nkeys * 4);
+    if (!sl.nbins) sl.nbins = (uint32_t*)g->dev_alloc(16);
+    if (!sl.off || !sl.bins || !sl.nbins) return fail(SG_ERR_CUDA, "bin allocation failed");
+    sl.kcap = nkeys;
+    g->bin_gen++;
+  }
+  use(sl);
+  if (launch_bin(g->bins_cur, (const float*)g->arrays[xa].ptr, g->arrays[xa].n, n, dcount, inv_dx, g->stream))
     return fail(SG_ERR_CUDA, std::string("binning launch failed: ") + cudaGetErrorString(cudaGetLastError()));
   aux += BIN_KERNELS;
-  g->bin_valid = true;
-  g->bin_xarr = xa; g->bin_epoch = g->arr_epoch[xa]; g->bin_n = n; g->bin_dcount = dcount;
-  for (int a = 0; a < 3; a++) g->bin_nb[a] = nb[a];
-  g->bin_inv_dx = inv_dx;
+  sl.valid = true;
+  sl.xa = xa; sl.epoch = g->arr_epoch[xa]; sl.n = n; sl.dcount = dcount; sl.inv_dx = inv_dx;
+  for (int a = 0; a < 3; a++) sl.nb[a] = nb[a];
   return SG_OK;
 }
 
@@ -818,7 +844,7 @@ static sg_status launch_group(sg_grid* g, const std::vector<int>& members, const
       if (n > 0 && nops == 1 && mpm_op && gt && !g->no_bin && tree_lb2(*gt) && (!gt2 || tree_lb2(*gt2))) {
         if ((rc = ensure_bins(g, g->L.field_tree[tk.fields[0]], tk.arrays[0], ops[0].p[1], n, dcount, st.aux_kernels)))
           return rc;
-        bp = &g->bins;
+        bp = &g->bins_cur;
       }
       rc = launch_range_for(g->ctx, n, dcount, ops, nops, task, g->stream, &rs, gt, gt2, bp);
     } break;
@@ -885,7 +911,10 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
   }
   st.tasks_lowered = (int64_t)g->eager.size();
   g->last_plan.clear();
-  g->bin_valid = false;   // arrays may have been rewritten outside the library since the last flush
+  // arrays may have been rewritten outside the library since the last flush:
+  // no binning carries over; slots are reassigned in this window's order
+  for (sg_grid::BinSlot& sl : g->bin_slots) sl.valid = false;
+  g->bin_next = 0;
   if (g->eager.empty()) {
     if (out) *out = st;
     return SG_OK;
@@ -938,8 +967,7 @@ extern "C" sg_status sg_flush(sg_grid* g, uint32_t passes, const int32_t* observ
     mix((uint64_t)g->arrays.size());
     for (const DArray& a : g->arrays) { mix((uint64_t)(uintptr_t)a.ptr); mix((uint64_t)a.n); mix((uint64_t)(uintptr_t)a.dcount); }
     mix((uint64_t)jit_generation());   // a specialized kernel became ready: recapture
-    mix((uint64_t)g->bin_cap);
-    mix((uint64_t)g->bin_keys_cap);
+    mix((uint64_t)g->bin_gen);   // binning buffers (re)allocated: their pointers are baked into launches
     auto ex = g->gexec.find(key);
     if (!chain && ex != g->gexec.end() && ex->second && g->gsig[key] == sig) {
       // identical window: relaunch the graph as captured
