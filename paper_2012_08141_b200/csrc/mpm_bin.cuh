@@ -693,6 +693,26 @@ __global__ void __launch_bounds__(MB_TPB, 3) k_g2p_adj_bin(const __grid_constant
     }
     int o[3];
     bin_origin(A.B, key, o);
+    // the particle's loads first (adjoint seeds of state s+1 and its state
+    // s): they overlap the block lookups, the tile staging and its barriers
+    const bool act = (int)threadIdx.x < m;
+    int64_t i = 0;
+    float xp[3] = {0.0f, 0.0f, 0.0f}, J = 1.0f, Jb1 = 0.0f, q[12], xb[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int t = 0; t < 12; t++) q[t] = 0.0f;
+    if (act) {
+      i = A.B.perm[start + c0 + threadIdx.x];
+      xp[0] = x[i]; xp[1] = x[nx + i]; xp[2] = x[2 * nx + i];
+      J = jj[i];
+      Jb1 = jb1[i];
+#pragma unroll
+      for (int rr = 0; rr < 3; rr++) {
+        xb[rr] = xb1[rr * n1x + i];
+        q[rr] = vb1[rr * n1v + i] + dt * xb[rr];
+#pragma unroll
+        for (int d = 0; d < 3; d++) q[3 + 3 * rr + d] = cb1[(3 * rr + d) * n1c + i] + (rr == d ? Jb1 * J * dt : 0.0f);
+      }
+    }
     if (threadIdx.x == 0) S.need = 0;
     bin_blocks<false>(C, T, o, 0xffu, S.off, A.task);
     zero_tiles(S, 3);
@@ -727,24 +747,13 @@ __global__ void __launch_bounds__(MB_TPB, 3) k_g2p_adj_bin(const __grid_constant
     }
     __syncthreads();
     uint32_t need = 0;
-    if ((int)threadIdx.x < m) {
-      const int64_t i = A.B.perm[start + c0 + threadIdx.x];
-      const float xp[3] = {x[i], x[nx + i], x[2 * nx + i]};
+    if (act) {
       const MpmKernel k = mpm_bspline(xp, inv_dx);
       float dw[3][3];
       mpm_dw(k, dw);
       const int r[3] = {k.base[0] - o[0], k.base[1] - o[1], k.base[2] - o[2]};
       need = need_mask(r);
-      const float J = jj[i], Jb1 = jb1[i];
-      float q[12];
-#pragma unroll
-      for (int rr = 0; rr < 3; rr++) {
-        q[rr] = vb1[rr * n1v + i] + dt * xb1[rr * n1x + i];
-#pragma unroll
-        for (int d = 0; d < 3; d++) q[3 + 3 * rr + d] = cb1[(3 * rr + d) * n1c + i] + (rr == d ? Jb1 * J * dt : 0.0f);
-      }
       float trC = 0.0f;
-      float xb[3] = {xb1[i], xb1[n1x + i], xb1[2 * n1x + i]};
 #pragma unroll
       for (int a = 0; a < 3; a++)
 #pragma unroll
@@ -837,12 +846,18 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_adj_bin(const __grid_constant
     const bool act = (int)threadIdx.x < m;
     int64_t i = 0;
     float xp[3] = {0.0f, 0.0f, 0.0f}, J = 1.0f, vv[3] = {0.0f, 0.0f, 0.0f}, Am[3][3];
+    float xb0[3] = {0.0f, 0.0f, 0.0f}, jb0 = 0.0f;   // the adjoints this kernel accumulates into
     if (act) {
       i = A.B.perm[start + c0 + threadIdx.x];
       xp[0] = x[i]; xp[1] = x[nx + i]; xp[2] = x[2 * nx + i];
       J = jj[i];
 #pragma unroll
       for (int rr = 0; rr < 3; rr++) vv[rr] = v[rr * nv + i];
+      // read now, added at the end (ncu: the end-of-kernel read-modify-write
+      // of x-bar and J-bar was half of the stall samples)
+#pragma unroll
+      for (int d = 0; d < 3; d++) xb0[d] = xb[d * nxb + i];
+      jb0 = jb[i];
     }
 #pragma unroll
     for (int rr = 0; rr < 3; rr++)
@@ -889,12 +904,12 @@ __global__ void __launch_bounds__(MB_TPB, 4) k_p2g_adj_bin(const __grid_constant
           }
 #pragma unroll
       for (int d = 0; d < 3; d++) {
-        xb[d * nxb + i] += xbar[d];
+        xb[d * nxb + i] = xb0[d] + xbar[d];
         vb[d * nvb + i] = vbar[d];
 #pragma unroll
         for (int c = 0; c < 3; c++) cb[(3 * d + c) * ncb + i] = pm * Ab[d][c];
       }
-      jb[i] += kJ * (Ab[0][0] + Ab[1][1] + Ab[2][2]);
+      jb[i] = jb0 + kJ * (Ab[0][0] + Ab[1][1] + Ab[2][2]);
     }
     __syncthreads();
   }
