@@ -69,3 +69,30 @@ def test_c2_full_size_jit():
     g2, _ = sg.run_program(prog)
     s_int = float(g2.field(prog["layout"].fields["s"]))
     assert s_jit == pytest.approx(s_int, rel=1e-5)
+
+
+_EXIT_CHILD = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+import workloads as W
+from paper_2012_08141_b200 import sg
+sg.jit_set_mode(1)                       # asynchronous: compiles run in worker threads
+prog = W.mg_program(n=64, levels=3, block=8, cycles=1, radius_frac=0.3)
+g, _ = sg.run_program(prog)              # submits every fused group's kernel for compilation
+print("compiling", sg.jit_info()["compiling"], flush=True)
+"""   # ... and the interpreter exits right away, compiles still in flight
+
+
+def test_process_exit_with_compiles_in_flight():
+    """Exit while NVRTC worker threads are compiling must not crash: NVRTC's
+    exit-time teardown under a running compile segfaulted a 2-process test;
+    the binding's atexit hook (sg_jit_shutdown) drains the workers first."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for _ in range(3):
+        r = subprocess.run([sys.executable, "-c", _EXIT_CHILD.format(root=root)], capture_output=True, text=True,
+                           timeout=300, env=dict(os.environ, SG_JIT="1"))
+        assert r.returncode == 0, (r.returncode, r.stderr[-2000:])
+        assert "compiling" in r.stdout
