@@ -860,7 +860,17 @@ def run_c5(args, rank, world, local):
         tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
+    n_end = me.n()
+    if world > 1:
+        import torch.distributed as dist
+        cnt = torch.tensor([n_loc, n_end], device=f"cuda:{local}", dtype=torch.int64)
+        dist.all_reduce(cnt)
+        n_tot0, n_tot1 = int(cnt[0].item()), int(cnt[1].item())
+    else:
+        n_tot0, n_tot1 = n_loc, n_end
     return {"ms_per_step": ms, "launches": launches, "clocks": clocks, "n_local": n_loc,
+            "particles_conserved": {"after_timed_steps": n_tot0, "after_e2e_steps": n_tot1,
+                                    "ok": n_tot0 == n_tot1 == args.c5_particles},
             "launches_per_step_rank0": sum(s["launches"] for s in st), "transport": me.transport,
             "single_gpu": single, "roofline": roof, "e2e": args.steps / e2e_s}
 
@@ -934,6 +944,7 @@ def main():
                    "config": c5_config(args, world),
                    "gpu_launches": r["launches"], "launches_per_step_rank0": r["launches_per_step_rank0"],
                    "transport": r["transport"],
+                   "particles_conserved": r["particles_conserved"],
                    "single_gpu_same_run": r["single_gpu"],
                    "roofline": r["roofline"],
                    "e2e": {"value": r["e2e"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4,

@@ -232,7 +232,14 @@ def c3_layout(n_grid=128):
     return L, lv
 
 
-def mpm_params(n_grid=128, dt=1e-4, E=400.0, gravity=9.8, bound=3):
+def mpm_params(n_grid=128, dt=None, E=400.0, gravity=9.8, bound=3):
+    """mpm3d-style constants (reading R28).  dt defaults to 1e-4 up to a 128^3
+    grid and shrinks with dx above it (reading R42): the sound speed
+    sqrt(E / rho) = 20 makes the CFL number 20 dt / dx, 0.26 at 128^3 with
+    1e-4 but 1.02 at 512^3 -- C5 blew up after ~15 steps (particles left the
+    domain into the per-particle overflow path, the step went 3 -> 290 ms)."""
+    if dt is None:
+        dt = 1e-4 * min(1.0, 128.0 / n_grid)
     dx = 1.0 / n_grid
     p_vol = (dx * 0.5) ** 3
     p_rho = 1.0
