@@ -247,6 +247,39 @@ __device__ __forceinline__ void make_block_row(const DTree& T, uint32_t e, Block
   *out = r;
 }
 
+// make_block_row by a whole warp (same e on every lane): the entry is resolved
+// once per lane, then lanes 0..5 walk to one face neighbour each and the row
+// is assembled by shuffles -- two dependent tree walks instead of seven (the
+// first struct-for after a listgen builds every row of the table: C2's fused
+// FILLs spent ~12 us on serial walks).  Every lane returns the full row.
+__device__ __forceinline__ void make_block_row_warp(const DTree& T, uint32_t e, int lane, BlockRow* out) {
+  BlockRow r;
+  uint32_t* cont = nullptr;
+  uint32_t first = 0;
+  int org[3] = {0, 0, 0};
+  bool ok = resolve_entry(T, e, cont, first, org);
+  const uint32_t* base = T.seg[T.nseg - 1].base;
+  r.blk = ok ? (uint32_t)(cont - base) + T.payload_off + first : SG_NO_BLOCK;
+  r.maskw = ok && T.leaf_bitmasked ? (uint32_t)(cont - base) + T.lev[T.nlev - 1].mask_off + (first >> 5) : 0u;
+  r.first = first;
+  r.org[0] = org[0]; r.org[1] = org[1]; r.org[2] = org[2];
+  const uint32_t lowmask = ~((1u << T.lblk) - 1u);
+  uint32_t mine = SG_NO_BLOCK;   // absent: reads 0
+  const int axis = lane >> 1;
+  if (lane < 6 && ok && axis < T.nd && T.driving >= 0) {
+    int q[3] = {org[0], org[1], org[2]};
+    q[axis] += (lane & 1) ? (1 << T.lev[T.driving].lbelow[axis]) : -1;
+    if (in_domain(T, q)) {
+      uint32_t idx;
+      uint32_t* c2 = locate(T, q, idx);
+      if (c2) mine = (uint32_t)(c2 - base) + T.payload_off + (idx & lowmask);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 6; d++) r.nbr[d] = __shfl_sync(0xffffffffu, mine, d);
+  *out = r;
+}
+
 // ---------------------------------------------------------------------------
 // Activation
 // ---------------------------------------------------------------------------

@@ -984,6 +984,10 @@ struct JacArgs {
 __device__ __noinline__ void jac_row_slow(const DTree& T, uint32_t entry, BlockRow* out) {
   make_block_row(T, entry, out);
 }
+// The same row built by the whole warp (every lane calls it with the same entry)
+__device__ __noinline__ void jac_row_warp(const DTree& T, uint32_t entry, int lane, BlockRow* out) {
+  make_block_row_warp(T, entry, lane, out);
+}
 
 __device__ __forceinline__ float4 u2f(uint4 u) {
   return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
@@ -1167,7 +1171,7 @@ __global__ void __launch_bounds__(256, SG_JAC8_MINB) k_jacobi8(const __grid_cons
       // no table yet (first struct-for after a listgen): every lane resolves
       // the row; the part-0 warp stores it for the following launches
       BlockRow r;
-      jac_row_slow(A.T, A.entries[e], &r);
+      jac_row_warp(A.T, A.entries[e], lane, &r);
       if (part == 0 && lane == 0) A.table[e] = r;
       blk = r.blk;
 #pragma unroll
@@ -1277,7 +1281,7 @@ __device__ __forceinline__ void stream8_body(const SFArgs& A, const OPS& ops) {
       for (int d = 0; d < 6; d++) nb[d] = __shfl_sync(0xffffffffu, rv, 6 + d);
     } else {
       BlockRow r;
-      make_block_row(A.T, A.entries[e], &r);
+      make_block_row_warp(A.T, A.entries[e], lane, &r);
       if (part == 0 && lane == 0) A.table[e] = r;
       blk = r.blk;
 #pragma unroll
