@@ -110,7 +110,9 @@ typedef struct sg_grid sg_grid;
 sg_status sg_create(const sg_snode_desc* nodes, int32_t n, const sg_opts* opts, sg_grid** out);
 /* Waits for the grid's stream and frees everything the grid allocated (pools,
  * lists, cached plans and CUDA graphs, exchange buffers; mapped peer buffers
- * are unmapped).  Borrowed buffers are not touched.  NULL is a no-op. */
+ * are unmapped) -- the end of the program's lifetime of the SNode tree and its
+ * allocator states.  Borrowed buffers are not touched.  NULL
+ * is a no-op. */
 sg_status sg_destroy(sg_grid* g);
 
 /* Registers an external SoA particle array (ncomp components of n elements,
@@ -122,7 +124,9 @@ sg_status sg_register_array(sg_grid* g, void* dev_ptr, int64_t n, int32_t dtype,
 /* Gives array `id` a device-resident element count (int32 at dev_count,
  * borrowed; <= the registered n, which becomes the capacity).  Range-for tasks
  * with range_n < 0 iterate [0, *dev_count of arrays[0]) read on the device, and
- * the migration / halo ops (below) update it on the device. */
+ * the migration / halo ops (below) update it on the device (a range-for over a
+ * range known only on the device: "no host round trip until an
+ * output is needed"). */
 sg_status sg_set_array_count(sg_grid* g, int32_t id, int32_t* dev_count);
 
 /* --- task vocabulary --------------------------------------------------------- */
@@ -233,7 +237,9 @@ sg_status sg_listgen(sg_grid* g, int32_t snode);
  * count, dtype or tree mismatch) return SG_ERR_ARG at enqueue time. */
 sg_status sg_struct_for(sg_grid* g, const sg_task* t);
 /* Enqueue n tasks (host array, borrowed for the call) in order: the same as n
- * sg_struct_for calls, one library call (a solver loop re-submitted each step). */
+ * sg_struct_for calls, one library call (a solver loop
+ * re-submitted each step).  Errors as sg_struct_for, reported for the first
+ * failing task; the tasks before it stay enqueued. */
 sg_status sg_struct_for_batch(sg_grid* g, const sg_task* tasks, int32_t n);
 
 enum { SG_CLEAR_VALUES = 0, SG_DEACTIVATE = 1 };
@@ -308,9 +314,11 @@ sg_status sg_export_list(sg_grid* g, int32_t snode, int32_t* host_coords, int64_
  * cells); inactive -> 0 (PAPER.md:195 reads of inactive cells return 0). */
 sg_status sg_read_field(sg_grid* g, int32_t field, void* host_dense, int64_t bytes);
 /* Enqueue (no flush, no sync) the device-to-host copy of a 0-D field's 4 bytes
- * into host_dst, ordered after everything flushed so far on the grid's stream.
- * host_dst should be pinned (else the copy is synchronous); it is valid once
- * the stream reaches this point (sg_sync, or an event the caller records). */
+ * into host_dst, ordered after everything flushed so far on the grid's stream
+ * (an output read without forcing a sync: PAPER.md:390).  host_dst should be
+ * pinned (else the copy is synchronous); it is valid once the stream reaches
+ * this point (sg_sync, or an event the caller records).  Errors: SG_ERR_ARG
+ * (not a 0-D field). */
 sg_status sg_read_scalar_async(sg_grid* g, int32_t field, void* host_dst);
 /* State handoff (SURVEY.md s8c reading 17, sg_load_state): overwrite the
  * values of the ACTIVE cells of a field from a dense host array (inactive
@@ -353,15 +361,18 @@ sg_status sg_device_info(sg_grid* g, int64_t* out, int32_t n);
  * out (n <= 7 int64): [mode, kernels ready, compiling, failed, hits, misses,
  * total compile time in microseconds]. */
 sg_status sg_jit_info(int64_t* out, int32_t n);
-/* Process-wide JIT mode (0, 1, 2 as SG_JIT; -1 = back to the environment). */
+/* Process-wide JIT mode (0, 1, 2 as SG_JIT; -1 = back to the environment) of
+ * the parallel compilation of PAPER.md:265-266.  Errors: SG_ERR_ARG. */
 sg_status sg_jit_set_mode(int32_t mode);
-/* Stops the JIT for the rest of the process: queued compilations are dropped,
+/* Stops the JIT (PAPER.md:265-266 compiler threads) for the rest of the
+ * process: queued compilations are dropped,
  * in-flight ones are waited for (<= 60 s), later launches use the op-table
  * interpreter.  Call before process exit while compilations may be running:
  * NVRTC's exit-time teardown under a running compile crashes the process
  * (the Python binding calls it from an atexit hook).  Always SG_OK. */
 sg_status sg_jit_shutdown(void);
-/* Host-side check (no GPU needed): NVRTC-compiles, without loading, the
+/* Host-side check (no GPU needed) of the specialization of PAPER.md:394-396
+ * (one compiled kernel per fused task content): NVRTC-compiles, without loading, the
  * specialized kernel of a group of `nops` op codes with placeholder operands
  * (nd / gl: quad-path dimensionality and constant block geometry, i32: value
  * type); the compile log is copied into log (cap bytes).  SG_ERR_STATE when
@@ -409,19 +420,24 @@ const char* sg_last_error(void);
  * kind before any rank's WAIT of it.  Errors: SG_ERR_ARG, SG_ERR_STATE (called
  * twice), SG_ERR_NCCL, SG_ERR_CUDA. */
 sg_status sg_dist_init(sg_grid* g, int32_t rank, int32_t world, const void* nccl_uid, int32_t axis);
-/* out (n >= 16 int32): [0] transport (0 none, 1 peer, 2 nccl), [1] rank,
+/* The data plane of sg_dist_init.  out (n >= 16 int32):
+ * [0] transport (0 none, 1 peer, 2 nccl), [1] rank,
  * [2] world, [3] axis, [4 + 2k + s] send array id of kind k side s,
  * [10 + 2k + s] receive array id (on a side without a neighbour the arrays
  * exist but nothing arrives: counts stay 0). */
 sg_status sg_dist_info(sg_grid* g, int32_t* out, int32_t n);
-/* ncclGetUniqueId into out (128 bytes), for rank 0 to broadcast. */
+/* ncclGetUniqueId into out (128 bytes), for rank 0 to broadcast (the NCCL
+ * halo exchange of the north star).  SG_ERR_NCCL when NCCL
+ * cannot be loaded. */
 sg_status sg_nccl_unique_id(void* out);
 /* This rank's 256-byte connection blob (IPC handle of its exchange arena,
- * PCI bus id, host, pid) after sg_dist_init(nccl_uid = NULL). */
+ * PCI bus id, host, pid) after sg_dist_init(nccl_uid = NULL): the N3 peer
+ * transport.  Errors: SG_ERR_STATE before sg_dist_init. */
 sg_status sg_dist_peer_info(sg_grid* g, void* out);
 /* Connects the neighbours from every rank's blob (world x 256 bytes, rank
- * order): maps their arenas (peer transport).  SG_ERR_CUDA when a neighbour
- * cannot be mapped (other host, same process, no peer access). */
+ * order): maps their arenas (peer transport).  SG_ERR_CUDA
+ * when a neighbour cannot be mapped (other host, same process, no peer
+ * access). */
 sg_status sg_dist_connect(sg_grid* g, const void* all_infos);
 
 #ifdef __cplusplus
